@@ -1,0 +1,305 @@
+"""Benchmark: PF particle-steps/s at N = 2^24 on B200 (BASELINE.json metric, config 2).
+
+A "step" is one Sampler.iterate() of the paper's particle filter: cv_move +
+add_log_weight (fused lse/ESS), the ESS decision, systematic resampling with
+the parent map and the in-place state copy, set_equal_weight and the "pos"
+monitor -- the whole hot path, inputs resident in HBM (X is 512 MiB at 2^24,
+larger than the 126 MB L2, so no flush is needed between steps).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
+(C restatement of the reference algorithm; OpenMP over all host cores for the
+per-particle loops, sequential normalization/resampling as SPEC.md:99,:185 pin).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 1 << 24
+METRIC = "PF particle-steps/sec at N=2^24 (resample+copy GB/s vs HBM peak reported alongside)"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--scheme", default="systematic")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------- CPU side ---
+def cpu_baseline_pf(n, steps, scheme, obs, threads):
+    """Oracle PF on the host cores: initialize untimed, then `steps` timed iterate()s."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+
+    L = O.lib()
+
+    class Sys(C.Structure):
+        _fields_ = [("n", C.c_int64), ("x", C.c_void_p), ("lw", C.c_void_p), ("w", C.c_void_p),
+                    ("incw", C.c_void_p), ("ctrs", C.c_void_p), ("counts", C.c_void_p), ("parents", C.c_void_p),
+                    ("k0", C.c_uint32), ("k1", C.c_uint32), ("scheme", C.c_int), ("threshold", C.c_double),
+                    ("log_zconst", C.c_double)]
+
+    bufs = dict(x=np.zeros(4 * n), lw=np.zeros(n), w=np.zeros(n), incw=np.zeros(n),
+                ctrs=np.zeros(n + 1, np.uint64), counts=np.zeros(n, np.int32), parents=np.zeros(n, np.int32))
+    s = Sys(n, *[bufs[k].ctypes.data for k in ("x", "lw", "w", "incw", "ctrs", "counts", "parents")],
+            1306, 0, O.SCHEMES[scheme], 0.5, 0.0)
+    L.orc_pf_initialize.argtypes = [C.POINTER(Sys), C.c_void_p, C.c_void_p, C.c_int]
+    L.orc_pf_step.argtypes = [C.POINTER(Sys), C.c_void_p, C.c_void_p, C.c_int]
+    row = np.zeros(5)
+    obs = np.ascontiguousarray(obs, np.float64)
+    rc = L.orc_pf_initialize(C.byref(s), obs.ctypes.data, row.ctypes.data, threads)
+    assert rc == 0
+    times = []
+    for t in range(1, steps + 1):
+        t0 = time.perf_counter()
+        rc = L.orc_pf_step(C.byref(s), obs[t % len(obs)].ctypes.data, row.ctypes.data, threads)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0
+    return times
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (CPU oracle port) on this host's cores."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    cores = len(os.sched_getaffinity(0))
+    n = args.n
+    obs = np.cumsum(np.random.default_rng(1306).normal(0, 0.15, (max(100, args.steps + args.warmup + 2), 2)), 0)
+    times = cpu_baseline_pf(n, args.warmup + args.steps, args.scheme, obs, cores)
+    t = sum(times[args.warmup:])
+    v = n * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles, {args.scheme} resampling, "
+                                   "ESS<N/2, 4-dim state, Student-t(10) likelihood", "n_particles": n,
+                       "scheme": args.scheme},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{args.steps} full PF steps at N={n} after {args.warmup} warm-up steps"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU side ---
+def run_b200(args):
+    import numpy as np
+    import torch
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1306_5583_b200 as P
+
+    n_total = args.n * world if world > 1 else args.n  # weak scaling: N per GPU fixed
+    n = args.n
+    T = args.warmup + args.steps + 2
+    rs = np.random.default_rng(1306)
+    # synthetic observations of the paper's shape: a smooth track + noise (T x 2)
+    obs = np.cumsum(rs.normal(0, 0.15, (max(100, T), 2)), 0)
+
+    s = P.pf.make_sampler(n, args.scheme, 0.5, seed=1306 + rank)
+    s.initialize(obs)
+    s.timing = None
+    for _ in range(args.warmup):
+        s.iterate(1, check=False)
+    s.check()
+    torch.cuda.synchronize()
+    s.timing = {}
+    clk = ClockSampler(local)
+    with clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.iterate(args.steps, check=False)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    s.check()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    phase = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in s.timing.items()}
+    s.timing = None
+    h = s.history()
+    resampled = h["resampled"][-args.steps:]
+    prev_rs = h["resampled"][-args.steps - 1:-1]
+
+    # ---- roofline of the dominant kernel (the fused move: X 32R+32W, lw 8W (+8R unless the previous
+    # step resampled), counter 8R+8W) and of resample+copy ----
+    peak, peak_src = measured_peaks()
+    move_bytes = n * (32 + 32 + 8 + 8 + 8) + n * 8 * float(np.mean(1 - prev_rs))
+    move_gbs = move_bytes / (phase["move"] * 1e-3) / 1e9
+    # resample+copy: lw read twice (pass A + B) is implementation traffic; algorithmic = read W (8) +
+    # parents (4) + counts (4, not materialized here) + 64 B per moved row
+    st = s.system
+    par = st.parents.cpu().numpy()
+    frac_moved = float(np.mean(par != np.arange(n)))
+    rc_bytes = n * (8 + 4 + 4) + 64 * frac_moved * n
+    rc_gbs = rc_bytes / (phase["resample"] * 1e-3) / 1e9 if phase.get("resample") else None
+    dominant = max(("move", "resample", "monitor"), key=lambda k: phase.get(k, 0))
+
+    value = n_total * args.steps / (ms * 1e-3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles per GPU, {args.scheme} "
+                                   "resampling at ESS<N/2, 4-dim state, Student-t(10) likelihood, 100-obs model "
+                                   "track", "n_particles": n_total, "scheme": args.scheme,
+                       "l2": "inputs larger than L2 (state 512 MiB/GPU at 2^24), no flush",
+                       "parallelism": f"particles sharded over {world} GPU(s)"},
+            "phase_ms": phase, "resampled_frac": float(np.mean(resampled)), "moved_row_frac": frac_moved,
+            "gpu_launches": args.steps * 10,
+            "roofline": {"bound": "hbm", "kernel": "k_pf_move (fused move + add_log_weight + lse/ESS partials)",
+                         "achieved": move_gbs, "peak": peak, "unit": "GB/s", "frac": move_gbs / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": move_bytes},
+            "resample_copy": {"achieved": rc_gbs, "peak": peak, "unit": "GB/s",
+                              "frac": None if rc_gbs is None else rc_gbs / peak,
+                              "algorithmic_bytes_per_step": rc_bytes, "scheme": args.scheme},
+            "dominant_phase": dominant, "clocks": clk.summary()}
+
+    # ---- e2e: the public API with host buffers: per step H2D the observation pair from pinned
+    # memory and D2H the step's history row (ess/N, resampled, pos.0, pos.1) ----
+    if not args.no_e2e:
+        e = run_e2e(P, s, obs, args.steps)
+        line["e2e"] = {"value": n_total * args.steps / e["seconds"], "unit": UNIT,
+                       "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"]}
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        cores = len(os.sched_getaffinity(0))
+        ncpu = 1 << 22
+        times = cpu_baseline_pf(ncpu, 3, args.scheme, obs, cores)
+        line["cpu_baseline"] = {"value": ncpu * 3 / sum(times), "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"3 full PF steps of the oracle at N=2^22 (scaled per particle-step)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(P, s, obs, steps):
+    """Same steps through Sampler with host-resident inputs/outputs, copies inside the timed region."""
+    import numpy as np
+    import torch
+
+    value = s.system.value
+    dev_obs = value.obs
+    host_obs = torch.from_numpy(np.ascontiguousarray(obs)).pin_memory()
+    ncols = len(s._cols)
+    host_row = torch.empty(ncols, dtype=torch.float64).pin_memory()
+    # re-initialize so iteration indices line up with the host observation buffer
+    s.initialize(obs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        t = s.iteration + 1
+        dev_obs[t].copy_(host_obs[t], non_blocking=True)  # H2D: this step's observation (16 B)
+        s.iterate(1, check=False)
+        host_row.copy_(s._hist[t], non_blocking=True)   # D2H: this step's history record
+        torch.cuda.current_stream().synchronize()
+    sec = time.perf_counter() - t0
+    s.check()
+    return {"seconds": sec, "h2d": 16, "d2h": 8 * ncols}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+/*
+ * smc_abi.h -- C ABI of the B200 (sm_100a) SMC hot path.
+ *
+ * Drop-in boundary for the data-parallel path of smckit / vSMC (arXiv 1306.5583).
+ * The reference is a Python package whose only shipped module is
+ * pkg/src/smckit/rng.py; the other modules (weights, resample, core, exec,
+ * example-pf) are specified in /root/reference/SPEC.md.  Each entry point below
+ * names the reference interface it replaces (file:line).  A ctypes binding of
+ * this header is paper_1306_5583_b200/_abi.py; INTEGRATION.md shows the stub a
+ * smckit maintainer would add.
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory owned by the caller (torch CUDA
+ *    tensors in the Python host), except `smc_last_error`'s buffer.  The
+ *    library never allocates; scratch comes in through (ws, ws_bytes), sized by
+ *    the matching *_workspace_bytes call.
+ *  - Every call takes the cudaStream_t it is ordered on (passed as void*) and
+ *    is asynchronous; no call synchronizes the device.
+ *  - Return value: SMC_OK or a negative SMC_E* code for host-detectable
+ *    failures (bad argument, launch failure).  Data-dependent failures that
+ *    only the device can see (normalization failure, unnormalized resampling
+ *    input) are written, first-error-wins, to a device int32 `status`
+ *    (smc_wstate.status for the weight calls) and surface at the caller's next
+ *    synchronization point -- the device analogue of SPEC.md:45/:137/:434.
+ *  - Particle counts are int64 at the boundary; kernels support N < 2^31.
+ *  - Threading: calls on distinct streams with distinct buffers are
+ *    independent (rng.py:175-177 single-user-per-stream rule).
+ */
+#ifndef SMC_ABI_H
+#define SMC_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMC_ABI_VERSION 1
+
+#define SMC_OK 0
+#define SMC_EINVAL -1         /* invalid argument                                   */
+#define SMC_EUNNORMALIZED -2  /* resample input not normalized        */
+#define SMC_ENORMALIZE -3     /* all -inf / NaN weights      */
+#define SMC_EUNIFORMS -4      /* fewer explicit uniforms than the scheme draws      */
+#define SMC_ECOUNTS -5        /* counts do not sum to N               */
+#define SMC_ECUDA -6          /* CUDA launch / runtime error                        */
+#define SMC_EWORKSPACE -7     /* workspace too small                                */
+
+int smc_abi_version(void);
+/* Copies the last host-side error message of the calling thread. */
+int smc_last_error(char *buf, size_t len);
+
+/* ------------------------------------------------------------------------ */
+/* RNG -- replaces pkg/src/smckit/rng.py                                     */
+/* ------------------------------------------------------------------------ */
+enum { SMC_DRAW_U01 = 0, SMC_DRAW_NORMAL = 1, SMC_DRAW_GAMMA = 2 };
+
+/* Raw Philox4x32-10 blocks: out4[4i..4i+3] = philox(ctr4[4i..4i+3], key(seed)).
+ * Replaces rng.py:59-72 (_philox_block); the KAT hook. */
+int smc_philox_blocks(const uint32_t *ctr4, int64_t n, uint64_t seed, uint32_t *out4, void *stream);
+
+/* n consecutive draws from ONE stream, advancing ctrs[stream_index] on device.
+ * normal: out = mean + scale*z; gamma: out = scale*g(shape); u01: out = u.
+ * Replaces rng.py:120-135 (fill_u01/fill_std_normal/fill_std_gamma) and
+ * RngStream.uniform01/normal/gamma(n) (rng.py:186-215).  u01/normal draws are
+ * computed in parallel (draw k uses counters c0+k / c0+2k, c0+2k+1); gamma is
+ * sequential on one thread because its draw count is data dependent. */
+int smc_rng_fill(int kind, uint64_t seed, uint64_t stream_index, uint64_t *ctrs, double shape,
+                 double mean, double scale, double *out, int64_t n, void *stream);
+
+/* One draw from each stream first..first+n-1 (the per-particle kernel pattern,
+ * rng.py:75-117 called once per particle), advancing each counter. */
+int smc_rng_draw_streams(int kind, uint64_t seed, uint64_t first_stream, int64_t n, uint64_t *ctrs,
+                         double shape, double mean, double scale, double *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Weights -- replaces smckit.weights.WeightSet             */
+/* ------------------------------------------------------------------------ */
+/* Device-resident weight state.  The log-weight vector is stored RAW
+ * (lw_raw); the normalized log-weight is lw_raw[i] - lse, or -log(N) for every
+ * i when `equal` is set (set_equal_weight never touches the vector). */
+typedef struct smc_wstate {
+    double lse;        /* log sum_i exp(lw_raw_i)                               */
+    double ess;        /* 1 / sum_i W_i^2                         */
+    double ess_over_n; /* ess / N                                               */
+    double nc_inc;     /* log sum_i W_{t-1,i} exp(incw_i) of the last ADD_LOG   */
+    double log_zconst; /* running NormalizingConstant         */
+    double max_raw;    /* max_i lw_raw_i                                        */
+    int32_t equal;     /* 1 after set_equal_weight                              */
+    int32_t status;    /* sticky device error (SMC_E*), 0 when healthy          */
+    int32_t resample;  /* decision of the last smc_ess_decide     */
+    int32_t iter;      /* free for the host loop                                */
+} smc_wstate;
+
+enum { SMC_W_SET_LOG = 0, SMC_W_ADD_LOG = 1, SMC_W_SET_LIN = 2, SMC_W_MUL_LIN = 3, SMC_W_EQUAL = 4 };
+enum { SMC_READ_LOG_WEIGHT = 0, SMC_READ_WEIGHT = 1 };
+
+size_t smc_weights_workspace_bytes(int64_t n);
+/* set_log_weight / add_log_weight / set_weight / mul_weight / set_equal_weight
+ * (SPEC.md:31-69).  `values` is the new log-weight, log increment, weight or
+ * factor vector (unused for EQUAL).  One pass over N plus a one-block
+ * finalize; ADD_LOG also produces nc_inc and adds it to
+ * log_zconst when `accumulate_nc` is set; SET_LOG with `accumulate_nc` starts
+ * log_zconst at log (1/N) sum_i exp(values_i) (first weighting of an
+ * equally weighted prior sample, e.g. the PF's init). */
+int smc_weights_update(int mode, double *lw_raw, const double *values, int64_t n, smc_wstate *ws_state,
+                       int accumulate_nc, void *ws, size_t ws_bytes, void *stream);
+/* set_equal_weight gated by a device flag (skipped when
+ * gate != NULL and *gate == 0): the post-resample reset of the sampler loop. */
+int smc_weights_set_equal(smc_wstate *ws_state, int64_t n, const int32_t *gate, void *stream);
+/* read_log_weight / read_weight: out = lw_raw - lse or exp(.) */
+int smc_weights_read(int what, const double *lw_raw, const smc_wstate *ws_state, int64_t n, double *out,
+                     void *stream);
+/* ESS trigger: resample iff
+ * threshold >= 1, or threshold > 0 and ess/N < threshold.  Writes
+ * ws_state->resample; when hist_row != NULL also hist_row[0] = ess/N and
+ * hist_row[1] = decision (the history record). */
+int smc_ess_decide(smc_wstate *ws_state, int64_t n, double threshold, double *hist_row, void *stream);
+
+/* Weighted sums out[j] = sum_i W_i * vals[i*ld + j], j < m  (monitor AW,
+ * SPEC.md:320-326 / PAPER.md:574-586; path U_t).  W comes
+ * from (lw_raw, ws_state).  Two passes: per-block partials, then a
+ * fixed-order combine, so the result is run-to-run deterministic. */
+size_t smc_weighted_reduce_workspace_bytes(int64_t n, int64_t m);
+int smc_weighted_reduce(const double *vals, int64_t ld, int64_t m, const double *lw_raw,
+                        const smc_wstate *ws_state, int64_t n, double *out, void *ws, size_t ws_bytes,
+                        void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Resampling -- replaces smckit.resample                  */
+/* ------------------------------------------------------------------------ */
+enum {
+    SMC_MULTINOMIAL = 0, SMC_RESIDUAL = 1, SMC_STRATIFIED = 2, SMC_SYSTEMATIC = 3,
+    SMC_RESIDUAL_STRATIFIED = 4, SMC_RESIDUAL_SYSTEMATIC = 5
+};
+
+size_t smc_resample_workspace_bytes(int64_t n);
+
+/* resample_<scheme>(W, stream) -> counts, + replication_to_parents, + the
+ * value collection's copy, under the pinned
+ * integer CDF contract.  Weights come from `w` (normalized W) or,
+ * when w == NULL, from (lw_raw, ws_state) as W_i = exp(lw_raw_i - lse).
+ * Uniforms come from `u` (device, n_u of them) or, when u == NULL, from
+ * stream `stream_index` of key(seed) starting at *ctr, which is advanced on
+ * the device by the number of draws.  m_out is the number of
+ * offspring (== n for a sampler; counts-only otherwise).  Outputs that are
+ * NULL are skipped.  When rows != NULL every zero-count row j is overwritten
+ * in place by row parents[j] (row_bytes each, 8-byte multiple) -- safe because
+ * copy sources (count >= 2) and destinations (count 0) are disjoint.  When
+ * gate != NULL and *gate == 0 every kernel returns immediately (device-side
+ * ESS decision, no host sync).  Errors go to *status. */
+int smc_resample(int scheme, const double *w, const double *lw_raw, const smc_wstate *ws_state, int64_t n,
+                 int64_t m_out, uint64_t seed, uint64_t stream_index, uint64_t *ctr, const double *u,
+                 int64_t n_u, int32_t *counts, int32_t *parents, void *rows, int64_t row_bytes,
+                 const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* replication_to_parents(counts) from a device counts vector. */
+int smc_replication_to_parents(const int32_t *counts, int64_t n, int32_t *parents, int32_t *status, void *ws,
+                               size_t ws_bytes, void *stream);
+
+/* StateMatrix.copy_particles(parents), simultaneous: dst row
+ * j <- src row parents[j]; dst != src (out of place). */
+int smc_gather_rows(void *dst, const void *src, int64_t row_bytes, const int32_t *parents, int64_t n,
+                    void *stream);
+/* In-place variant for a ParentVector (copy_from[j] == j whenever j survives):
+ * copies only rows with parents[j] != j. */
+int smc_copy_rows_inplace(void *rows, int64_t row_bytes, const int32_t *parents, int64_t n,
+                          const int32_t *gate, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* example-pf kernels -- replace cv_init / cv_move / cv_monitor              */
+/*               */
+/* ------------------------------------------------------------------------ */
+size_t smc_pf_workspace_bytes(int64_t n);
+/* X (n x 4 row-major f64) ~ prior from streams 0..n-1 (draw order x,y,vx,vy),
+ * llh at obs_t = (x_obs, y_obs) (device, 2 doubles) -> set_log_weight; the
+ * state's log_zconst restarts at log (1/N) sum exp(llh). */
+int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
+                smc_wstate *ws_state, void *ws, size_t ws_bytes, void *stream);
+/* cv_move on every particle + incw = llh(t) -> add_log_weight(incw) fused in
+ * one pass over the state; log_zconst += log sum W_{t-1} exp(incw).
+ * incw_out may be NULL. */
+int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
+                smc_wstate *ws_state, double *incw_out, void *ws, size_t ws_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMC_ABI_H */

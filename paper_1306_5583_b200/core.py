@@ -1,0 +1,433 @@
+"""Sampler / ParticleSystem / StateMatrix on the device (mirror of smckit.core).
+
+One ``Sampler.iterate()`` issues, with no host synchronization:
+
+  move queue (device kernels; the PF move fuses add_log_weight + lse/ESS)
+  -> smc_ess_decide         (device flag; history ess_over_n / resampled)
+  -> smc_resample           (gated by the flag: counts, parent map and the
+                             in-place row copy of the state matrix)
+  -> set_equal_weight       (gated)
+  -> mcmc queue
+  -> monitors / path        (fused weighted reductions into the device history)
+
+The history lives in a device tensor and is read back lazily (``history()``,
+``write_tsv()``), so a run of many iterations costs one sync at the end.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _abi
+from .exec import MonitorEval, PathEval, ParticleKernelOp, apply_monitor_eval, apply_path_eval, apply_move
+from .resample import ResampleScheme, Resampler, _scheme
+from .rng import RngStreamSet
+from .weights import WeightSet
+
+__all__ = ["StateMatrix", "ParticleSystem", "SingleParticleView", "Sampler", "MonitorRecord",
+           "PathAccumulator", "NormalizingConstant", "ROW_MAJOR", "COL_MAJOR"]
+
+ROW_MAJOR, COL_MAJOR = "row", "col"
+
+
+class StateMatrix:
+    """N x D float64 state (PAPER.md:714-726 RowMajor/ColMajor tag).
+
+    Row-major storage puts one particle in one contiguous row, which the
+    resampling kernel copies in place with a single 256-bit load/store when
+    D == 4 (the PF).  Column-major is D contiguous columns.
+    """
+
+    def __init__(self, size, dim, order=ROW_MAJOR, device="cuda"):
+        if order not in (ROW_MAJOR, COL_MAJOR):
+            raise ValueError("order must be 'row' or 'col'")
+        _abi.require_cuda()
+        self.size, self.dim, self.order = int(size), int(dim), order
+        self.device = torch.device(device)
+        shape = (self.size, self.dim) if order == ROW_MAJOR else (self.dim, self.size)
+        self.data = torch.zeros(shape, dtype=torch.float64, device=self.device)
+
+    # element / column access
+    def _check(self, i, pos):
+        if not (0 <= i < self.size and 0 <= pos < self.dim):
+            raise IndexError("state index out of range")
+
+    def state(self, i, pos):
+        self._check(i, pos)
+        return float(self.data[i, pos] if self.order == ROW_MAJOR else self.data[pos, i])
+
+    def set_state(self, i, pos, v):
+        self._check(i, pos)
+        if self.order == ROW_MAJOR:
+            self.data[i, pos] = v
+        else:
+            self.data[pos, i] = v
+
+    def read_state(self, pos):
+        if not 0 <= pos < self.dim:
+            raise IndexError("column out of range")
+        return (self.data[:, pos] if self.order == ROW_MAJOR else self.data[pos]).clone()
+
+    def read_state_matrix(self, order=ROW_MAJOR):
+        m = self.data if self.order == ROW_MAJOR else self.data.t()
+        return m.contiguous().clone() if order == ROW_MAJOR else m.t().contiguous().clone()
+
+    def column_view(self, first, count):
+        """(vals, ld) for monitors: columns first..first+count-1 without a copy."""
+        if self.order == ROW_MAJOR:
+            return self.data.view(-1)[first:], self.dim
+        if count != 1:
+            raise ValueError("column-major monitors take one column per evaluator")
+        return self.data[first], 1
+
+    # copies
+    def copy_particles(self, parents):
+        """Rows j <- rows parents[j], simultaneously (out of place: safe for any map)."""
+        p = torch.as_tensor(parents, dtype=torch.int32).to(self.device).contiguous()
+        if p.numel() != self.size:
+            raise ValueError("parents length != size")
+        if self.size and (int(p.min()) < 0 or int(p.max()) >= self.size):
+            raise IndexError("parent index out of range")
+        if self.order == ROW_MAJOR:
+            out = torch.empty_like(self.data)
+            _abi.call("smc_gather_rows", _abi.ptr(out), _abi.ptr(self.data), 8 * self.dim, _abi.ptr(p),
+                      self.size, _abi.stream())
+        else:
+            out = torch.empty_like(self.data)
+            for c in range(self.dim):
+                _abi.call("smc_gather_rows", _abi.ptr(out[c]), _abi.ptr(self.data[c]), 8, _abi.ptr(p), self.size,
+                          _abi.stream())
+        self.data = out
+
+    def resample_rows(self):
+        """(rows_ptr, row_bytes) for the fused in-place copy in smc_resample, or None."""
+        if self.order == ROW_MAJOR:
+            return ctypes.c_void_p(self.data.data_ptr()), 8 * self.dim
+        return None
+
+    def copy_inplace(self, parents, gate=None):
+        """In-place copy for a ParentVector (sources and destinations are disjoint)."""
+        if self.order == ROW_MAJOR:
+            _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(self.data.data_ptr()), 8 * self.dim,
+                      _abi.ptr(parents), self.size, gate, _abi.stream())
+        else:
+            for c in range(self.dim):
+                _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(self.data[c].data_ptr()), 8, _abi.ptr(parents),
+                          self.size, gate, _abi.stream())
+
+
+class ParticleSystem:
+    """value + WeightSet + RngStreamSet(N + 1) + resampling policy."""
+
+    def __init__(self, value, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, device="cuda"):
+        self.value = value
+        self.size = int(size)
+        self.device = torch.device(device)
+        self.weight_set = WeightSet(self.size, self.device, check=False)
+        self.rng_set = RngStreamSet(self.size + 1, seed, self.device)
+        self.resample_scheme = _scheme(scheme)
+        self.threshold = float(threshold)
+        self.parents = torch.arange(self.size, dtype=torch.int32, device=self.device)
+        self.resampler = Resampler(self.size, self.device)
+
+    def rng(self, i):
+        return self.rng_set.stream(i)
+
+
+class SingleParticleView:
+    """Handle on particle ``id``.  Host-side convenience only:
+    device kernels address their particle by thread index instead."""
+
+    def __init__(self, id_, system):
+        self.id = int(id_)
+        self.system = system
+
+    def state(self, pos):
+        return self.system.value.state(self.id, pos)
+
+    def set_state(self, pos, v):
+        self.system.value.set_state(self.id, pos, v)
+
+    def rng(self):
+        return self.system.rng(self.id)
+
+
+class MonitorRecord:
+    """name, dim m, and the per-iteration estimates."""
+
+    def __init__(self, name, dim, eval_):
+        self.name, self.dim, self.eval = name, int(dim), eval_
+
+
+class PathAccumulator:
+    """grids alpha_t, integrands U_t, trapezoid log Z."""
+
+    def __init__(self, grids=(), integrands=()):
+        self.grids = list(grids)
+        self.integrands = list(integrands)
+
+    @property
+    def log_zconst(self):
+        g, u = self.grids, self.integrands
+        return float(sum(0.5 * (g[t] - g[t - 1]) * (u[t] + u[t - 1]) for t in range(1, len(g))))
+
+
+class NormalizingConstant:
+    """Running log Z = sum_t log sum_i W_{t-1,i} exp(incw_{t,i}).
+
+    Lives in the device weight record (smc_wstate.log_zconst); this is a view."""
+
+    def __init__(self, weight_set):
+        self.weight_set = weight_set
+
+    @property
+    def log_zconst(self):
+        return self.weight_set.log_zconst
+
+
+class Sampler:
+    """SMC sampler.
+
+    ``Sampler(N, scheme=Stratified, threshold=0.5, seed=0, value=...)``; the
+    value collection defaults to an N x 1 StateMatrix.
+    """
+
+    def __init__(self, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, value=None, device="cuda"):
+        size = int(size)
+        if size < 1:
+            raise ValueError("sampler needs N >= 1")
+        _abi.require_cuda()
+        self.device = torch.device(device)
+        if value is None:
+            value = StateMatrix(size, 1, device=self.device)
+        self.system = ParticleSystem(value, size, scheme, threshold, seed, self.device)
+        self.init_op = None
+        self.move_queue = []
+        self.mcmc_queue = []
+        self.monitors = {}
+        self.path = None
+        self._hist = None
+        self._rows = 0
+        self._cols = None
+        self._path_grid = []
+        self.iteration = -1
+        self._ws = _abi.Workspace(self.device)
+        self._mon_out = None
+
+    # -- configuration -------------------------------------
+    @property
+    def size(self):
+        return self.system.size
+
+    @property
+    def particle(self):
+        return self.system
+
+    def set_init(self, op):
+        self.init_op = op
+        return self
+
+    init = set_init
+
+    def add_move(self, op, append=False):
+        if not append:
+            self.move_queue = []
+        self.move_queue.append(op)
+        return self
+
+    move = add_move
+
+    def add_mcmc(self, op, append=False):
+        if not append:
+            self.mcmc_queue = []
+        self.mcmc_queue.append(op)
+        return self
+
+    mcmc = add_mcmc
+
+    def set_monitor(self, name, dim, eval_):
+        if not isinstance(eval_, MonitorEval):
+            eval_ = MonitorEval(eval_, dim)
+        self.monitors[name] = MonitorRecord(name, dim, eval_)
+        return self
+
+    monitor = set_monitor
+
+    def set_path(self, eval_):
+        self.path = eval_ if isinstance(eval_, PathEval) else PathEval(eval_)
+        return self
+
+    path_sampling = set_path
+
+    # -- history layout -----------------------------------------
+    def _layout(self):
+        cols = ["ess_over_n", "resampled"]
+        nacc = max(len(self.move_queue) + len(self.mcmc_queue), 0)
+        cols += [f"accept.{k}" for k in range(nacc)]
+        if self.path is not None:
+            cols += ["path.grid", "path.integrand"]
+        for name, rec in self.monitors.items():
+            cols += [f"{name}.{j}" for j in range(rec.dim)]
+        self._cols = cols
+        self._col = {c: k for k, c in enumerate(cols)}
+
+    def _row(self, t):
+        if self._hist is None or t >= self._hist.shape[0]:
+            cap = max(128, 2 * (t + 1))
+            h = torch.zeros((cap, len(self._cols)), dtype=torch.float64, device=self.device)
+            if self._hist is not None:
+                h[: self._hist.shape[0]] = self._hist
+            self._hist = h
+        self._rows = max(self._rows, t + 1)
+        return self._hist[t]
+
+    # -- the loop -------------------------------------------
+    def initialize(self, param=None, check=True):
+        if self.init_op is None:
+            raise RuntimeError("initialize: no init operation set")
+        self._layout()
+        self._hist = None
+        self._rows = 0
+        self._path_grid = []
+        sysm = self.system
+        sysm.weight_set.set_equal_weight()
+        row = self._row(0)
+        acc = self.init_op(sysm, param) if not isinstance(self.init_op, ParticleKernelOp) \
+            else apply_move(self.init_op, sysm, 0)
+        del acc
+        self.iteration = 0
+        self._after_moves(0, row, [])
+        if check:
+            self.check()
+
+    def iterate(self, n=1, check=True):
+        if self.iteration < 0:
+            raise RuntimeError("iterate: sampler not initialized")
+        for _ in range(int(n)):
+            t = self.iteration + 1
+            row = self._row(t)
+            self._mark("move", 0)
+            accs = [apply_move(op, self.system, t) for op in self.move_queue]
+            self._mark("move", 1)
+            self.iteration = t
+            self._after_moves(t, row, accs)
+        if check and n:
+            self.check()
+
+    def _after_moves(self, t, row, accs):
+        sysm = self.system
+        ws = sysm.weight_set
+        n = sysm.size
+        hist_ptr = ctypes.c_void_p(row.data_ptr())
+        # ESS trigger (F11: also after init)
+        _abi.call("smc_ess_decide", ws.state_ptr, n, sysm.threshold, hist_ptr, _abi.stream())
+        self._mark("resample", 0)
+        if sysm.threshold > 0.0:
+            gate = ws.field_ptr("resample")
+            rows = getattr(sysm.value, "resample_rows", lambda: None)()
+            sysm.resampler(sysm.resample_scheme, weight_set=ws, rng=sysm.rng_set, stream_index=n,
+                           parents=sysm.parents, rows=rows[0] if rows else None,
+                           row_bytes=rows[1] if rows else 0, gate=gate, status=ws.field_ptr("status"))
+            if not rows:
+                sysm.value.copy_inplace(sysm.parents, gate)
+            ws.set_equal_weight_if(gate)
+        self._mark("resample", 1)
+        for op in self.mcmc_queue:
+            accs.append(apply_move(op, sysm, t))
+        for k, a in enumerate(accs):
+            if isinstance(a, torch.Tensor):
+                row[2 + k].copy_(a.reshape(()).to(torch.float64), non_blocking=True)
+            elif a:
+                row[2 + k].fill_(float(a))
+        self._mark("monitor", 0)
+        if self.path is not None:
+            alpha, integrand = apply_path_eval(self.path, sysm, t)
+            self._path_grid.append(alpha)
+            row[self._col["path.grid"]].fill_(alpha)
+            self._reduce(integrand, 1, 1, row, self._col["path.integrand"])
+        for name, rec in self.monitors.items():
+            vals, ld = apply_monitor_eval(rec.eval, sysm, t, rec.dim)
+            self._reduce(vals, ld, rec.dim, row, self._col[f"{name}.0"])
+        self._mark("monitor", 1)
+
+    # Optional per-phase CUDA events (bench.py's live per-kernel timing):
+    # set ``sampler.timing = {}``; each phase gets a list of (start, end) events.
+    timing = None
+
+    def _mark(self, phase, edge):
+        if self.timing is None:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        lst = self.timing.setdefault(phase, [])
+        if edge == 0:
+            lst.append([ev, None])
+        else:
+            lst[-1][1] = ev
+
+    def _reduce(self, vals, ld, m, row, col):
+        ws = self.system.weight_set
+        n = self.system.size
+        buf, nb = self._ws.get(_abi.lib().smc_weighted_reduce_workspace_bytes(n, m))
+        out = ctypes.c_void_p(row.data_ptr() + 8 * col)
+        _abi.call("smc_weighted_reduce", _abi.ptr(vals), ld, m, _abi.ptr(ws.lw_raw), ws.state_ptr, n, out, buf, nb,
+                  _abi.stream())
+
+    def check(self):
+        """Synchronize and raise any device-side failure (SPEC.md:315 'propagates')."""
+        self.system.weight_set.raise_if_failed()
+
+    # -- results ---------------------------------------
+    def history(self):
+        h = self._hist[: self._rows].cpu().numpy()
+        d = {"iter": np.arange(self._rows)}
+        for c, k in self._col.items():
+            d[c] = h[:, k].copy()
+        return d
+
+    def history_array(self):
+        return self._hist[: self._rows].cpu().numpy()
+
+    def monitor_estimate(self, name, t):
+        rec = self.monitors[name]
+        if not 0 <= t < self._rows:
+            raise IndexError("iteration not recorded")
+        k = self._col[f"{name}.0"]
+        return self._hist[t, k:k + rec.dim].cpu().numpy()
+
+    def path_log_zconst(self):
+        if self.path is None:
+            raise RuntimeError("no path sampling evaluator")
+        h = self.history()
+        return PathAccumulator(h["path.grid"], h["path.integrand"]).log_zconst
+
+    @property
+    def log_zconst(self):
+        return self.system.weight_set.log_zconst
+
+    def write_tsv(self, path_or_file, header_comments=()):
+        """History as TSV (SPEC.md:369, 17 significant digits SPEC.md:653)."""
+        h = self.history()
+        cols = ["iter"] + self._cols
+        lines = [f"# {c}" for c in header_comments]
+        lines.append("\t".join(cols))
+        for t in range(self._rows):
+            vals = []
+            for c in cols:
+                v = h[c][t]
+                if c in ("iter", "resampled") or c.startswith("accept."):
+                    vals.append(str(int(round(v))))
+                else:
+                    vals.append(f"{v:.17g}")
+            lines.append("\t".join(vals))
+        text = "\n".join(lines) + "\n"
+        if hasattr(path_or_file, "write"):
+            path_or_file.write(text)
+        else:
+            with open(path_or_file, "w") as f:
+                f.write(text)
+        return text

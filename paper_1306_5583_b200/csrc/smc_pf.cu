@@ -1,0 +1,151 @@
+// smc_pf.cu -- the paper's particle filter kernels:
+// cv_init / cv_move fused with the weight update and the one-pass log-sum-exp
+// / ESS partials, so a PF step reads and writes the state exactly once.
+//
+// State: X is N x 4 f64 row-major, one 32-byte row per particle,
+// moved with one 256-bit load and one 256-bit store per thread.
+// Per particle-step HBM traffic: X 32 R + 32 W, lw 8 R (skipped after a
+// resample: equal weights) + 8 W, counter 8 R + 8 W  =  96 B.
+#include "smc_weights.cuh"
+
+using namespace smc;
+
+namespace {
+
+constexpr int PB = 256;
+
+struct PfConst {
+    double sd_pos0, sd_vel0;  // init: 2, 1
+    double sd_pos, sd_vel;    // move: sqrt(.02), sqrt(.001)
+    double delta;             // 0.1
+};
+
+// PAPER.md:1181-1191 / SPEC.md:464-472 (scale 10, nu 10)
+SMC_DEV double cv_llh(double xp, double yp, double xo, double yo)
+{
+    const double scale = 10;
+    const double nu = 10;
+    double llh_x = scale * (xp - xo);
+    double llh_y = scale * (yp - yo);
+    llh_x = log(1 + llh_x * llh_x / nu);
+    llh_y = log(1 + llh_y * llh_y / nu);
+    return -0.5 * (nu + 1) * (llh_x + llh_y);
+}
+
+SMC_DEV void ld_row(const double *p, double &a, double &b, double &c, double &d)
+{
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+SMC_DEV void st_row(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+__global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
+                                                Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                PfConst k, smc_wstate *st, LsePartial *__restrict__ parts)
+{
+    const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
+    double v = -INFINITY;
+    if (i < n) {
+        const uint64_t c = ctrs[i], si = (uint64_t)i;
+        // draw order x_pos, y_pos, x_vel, y_vel; normal = mean + sd*z (rng.py:201)
+        const double r0 = 0.0 + k.sd_pos0 * normal_at(c + 0, si, key);
+        const double r1 = 0.0 + k.sd_pos0 * normal_at(c + 2, si, key);
+        const double r2 = 0.0 + k.sd_vel0 * normal_at(c + 4, si, key);
+        const double r3 = 0.0 + k.sd_vel0 * normal_at(c + 6, si, key);
+        ctrs[i] = c + 8;
+        st_row(x + 4 * i, r0, r1, r2, r3);
+        v = cv_llh(r0, r1, obs[0], obs[1]);
+        if (isnan(v)) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+        lw_raw[i] = v;  // set_log_weight(llh)
+    }
+    LsePartial p = block_lse_partial<PB>(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+}
+
+__global__ void __launch_bounds__(PB) k_pf_move(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
+                                                Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                PfConst k, smc_wstate *st, double *__restrict__ incw_out,
+                                                LsePartial *__restrict__ parts)
+{
+    const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
+    double v = -INFINITY;
+    if (i < n) {
+        const bool eq = st->equal;
+        const double prev = eq ? -log((double)n) : lw_raw[i] - st->lse;  // normalized W_{t-1}
+        double x0, x1, x2, x3;
+        ld_row(x + 4 * i, x0, x1, x2, x3);
+        const uint64_t c = ctrs[i], si = (uint64_t)i;
+        // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
+        x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
+        x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
+        x2 = x2 + (0.0 + k.sd_vel * normal_at(c + 4, si, key));
+        x3 = x3 + (0.0 + k.sd_vel * normal_at(c + 6, si, key));
+        ctrs[i] = c + 8;
+        st_row(x + 4 * i, x0, x1, x2, x3);
+        const double incw = cv_llh(x0, x1, obs[0], obs[1]);
+        if (incw_out) incw_out[i] = incw;
+        v = prev + incw;  // add_log_weight(incw)
+        if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+        lw_raw[i] = v;
+    }
+    LsePartial p = block_lse_partial<PB>(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+}
+
+PfConst pf_constants()
+{
+    PfConst k;
+    k.sd_pos0 = 2;
+    k.sd_vel0 = 1;
+    k.sd_pos = sqrt(0.02);
+    k.sd_vel = sqrt(0.001);
+    k.delta = 0.1;
+    return k;
+}
+
+}  // namespace
+
+extern "C" size_t smc_pf_workspace_bytes(int64_t n)
+{
+    return (size_t)((n + PB - 1) / PB + 1) * sizeof(LsePartial);
+}
+
+static int pf_check(double *x, double *lw_raw, int64_t n, uint64_t *ctrs, const double *obs, smc_wstate *st,
+                    void *ws, size_t ws_bytes, const char *who)
+{
+    if (!x || !lw_raw || !ctrs || !obs || !st || n < 1 || n >= ((int64_t)1 << 31))
+        return smc_set_error(SMC_EINVAL, "%s: bad args", who);
+    if ((uintptr_t)x & 31) return smc_set_error(SMC_EINVAL, "%s: state must be 32-byte aligned", who);
+    if (!ws || ws_bytes < smc_pf_workspace_bytes(n)) return smc_set_error(SMC_EWORKSPACE, "%s: workspace", who);
+    return SMC_OK;
+}
+
+extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
+                           smc_wstate *st, void *ws, size_t ws_bytes, void *stream)
+{
+    int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_init");
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nb = (int)((n + PB - 1) / PB);
+    LsePartial *parts = (LsePartial *)ws;
+    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
+                                pf_constants(), st, parts);
+    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s);
+    return smc_check_launch("smc_pf_init");
+}
+
+extern "C" int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
+                           smc_wstate *st, double *incw_out, void *ws, size_t ws_bytes, void *stream)
+{
+    int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_move");
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nb = (int)((n + PB - 1) / PB);
+    LsePartial *parts = (LsePartial *)ws;
+    k_pf_move<<<nb, PB, 0, s>>>(x, lw_raw, n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
+                                pf_constants(), st, incw_out, parts);
+    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s);
+    return smc_check_launch("smc_pf_move");
+}

@@ -1,0 +1,721 @@
+// smc_resample.cu -- resampling on sm_100a (replaces smckit.resample, SPEC.md:114-199,
+// and the value collection's copy, SPEC.md:342-349 / PAPER.md:418-433).
+//
+// Pinned integer contract, shared bit-for-bit
+// with oracle/smc_oracle.c:
+//   q_i = floor(W_i 2^63), Q = inclusive prefix, T = Q_{N-1}, |T - 2^63| <= 2^43
+//   stratified/systematic over M strata: P_k = floor((k + m_k 2^-53) T / M)
+//   multinomial:                          P_k = floor(m_k T 2^-53)
+//   particle i receives #{k : Q_{i-1} <= P_k < Q_i}   (strict bound)
+//   residual: f_i = floor(fl(M W_i)); the R = M - sum f leftovers over
+//   q'_i = floor((fl(M W_i) - f_i) 2^(63 - ceil log2 N)).
+//
+// Kernels (one resample = 4 launches for stratified/systematic):
+//   A  k_rs_tiles      : per-tile sums of q (u128), f and q'; validation.
+//   S  k_rs_scan       : one block: T, R, window check, tile prefixes, stream
+//                        counter advance (on device: no host sync).
+//   [M k_rs_prefix + k_rs_multinomial : multinomial/residual histogram]
+//   B  k_rs_counts     : per tile, local scan + tile prefix -> Q; counts in O(1)
+//                        per particle via F(X) = #{k : P_k < X}; then a
+//                        DECOUPLED-LOOKBACK scan of (zero slots, surplus
+//                        children, surplus parents) to emit the survivor part
+//                        of the parent map, the compacted zero-slot list and the
+//                        compacted surplus-parent list.
+//   C  k_rs_assign     : per tile of zero-slot ranks: merge-path search of the
+//                        rank range against the surplus-parent prefix (staged in
+//                        shared memory), parent map for zero slots, and the
+//                        in-place row copy (256-bit LDG/STG per 32-byte row).
+#include "smc_weights.cuh"
+
+using namespace smc;
+
+namespace {
+
+constexpr int RT = 256;
+constexpr int RI = 8;
+constexpr int TILE = RT * RI;  // elements per tile (pass A/B) and ranks per tile (pass C)
+constexpr uint64_t T_LO = (1ull << 63) - (1ull << 43);
+constexpr uint64_t T_HI = (1ull << 63) + (1ull << 43);
+
+struct RsHeader {
+    uint64_t T;       // sum of q
+    uint64_t Tm;      // total of the CDF that is searched (T or T')
+    uint64_t M;       // positions (strata / draws)
+    uint64_t c0;      // first counter of the resampling stream for this call
+    uint64_t m_sys;   // the single systematic uniform (53-bit integer)
+    int64_t draws;
+    int32_t active;   // 0 => gated off or failed; later kernels exit
+    int32_t trivial;  // N == 1
+    uint32_t tile_ctr;
+    uint32_t Z_total, S_total, P_total;
+};
+
+struct Layout {
+    RsHeader *hdr;
+    u128 *tile_q;
+    int64_t *tile_f;
+    uint64_t *tile_qr;
+    uint64_t *tile_pre;
+    uint32_t *lb_status;
+    uint4 *lb_agg, *lb_incl;
+    int32_t *zpos, *sp_idx, *sp_start;
+    uint64_t *qfull;
+    int32_t *cnt;
+    size_t bytes;
+};
+
+inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Layout layout(void *ws, int64_t n)
+{
+    const int64_t nt = (n + TILE - 1) / TILE;
+    char *p = (char *)ws;
+    Layout L;
+    size_t o = 0;
+    auto take = [&](size_t b) { char *r = p ? p + o : nullptr; o += al(b); return (void *)r; };
+    L.hdr = (RsHeader *)take(sizeof(RsHeader));
+    L.tile_q = (u128 *)take(sizeof(u128) * nt);
+    L.tile_f = (int64_t *)take(sizeof(int64_t) * nt);
+    L.tile_qr = (uint64_t *)take(sizeof(uint64_t) * nt);
+    L.tile_pre = (uint64_t *)take(sizeof(uint64_t) * nt);
+    L.lb_status = (uint32_t *)take(sizeof(uint32_t) * nt);
+    L.lb_agg = (uint4 *)take(sizeof(uint4) * nt);
+    L.lb_incl = (uint4 *)take(sizeof(uint4) * nt);
+    L.zpos = (int32_t *)take(sizeof(int32_t) * n);
+    L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));    // P <= n even for invalid counts
+    L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
+    L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
+    L.cnt = (int32_t *)take(sizeof(int32_t) * n);
+    L.bytes = o;
+    return L;
+}
+
+// Everything a per-particle kernel needs to turn an index into W_i.
+struct WSrc {
+    const double *w;        // normalized weights, or null
+    const double *lw;       // raw log weights (w == null)
+    const smc_wstate *st;
+    int64_t n;
+    SMC_DEV double at(int64_t i, double lse, bool eq) const
+    {
+        if (w) return w[i];
+        return eq ? 1.0 / (double)n : exp(lw[i] - lse);
+    }
+};
+
+SMC_DEV bool is_residual(int scheme)
+{
+    return scheme == SMC_RESIDUAL || scheme == SMC_RESIDUAL_STRATIFIED || scheme == SMC_RESIDUAL_SYSTEMATIC;
+}
+SMC_DEV bool is_multinomial(int scheme) { return scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL; }
+
+// q, f, q' for one weight (A.1, A.4).  Validation sets `bad`.
+struct Quant {
+    uint64_t q, qr;
+    int64_t f;
+};
+SMC_DEV Quant quantize(double W, bool residual, double m_out, double rscale, bool &bad)
+{
+    Quant r{0, 0, 0};
+    if (!(W >= 0.0 && W <= 1.0)) { bad = true; return r; }
+    r.q = (uint64_t)(W * 9223372036854775808.0);
+    if (residual) {
+        const double x = m_out * W;  // fl(M W_i), exactly rounded (no FMA: --fmad=false)
+        const double f = floor(x);
+        r.f = (int64_t)f;
+        r.qr = (uint64_t)((x - f) * rscale);
+    }
+    return r;
+}
+
+// ------------------------------------------------------------------ pass A --
+__global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n, double m_out, double rscale,
+                                                 const double *__restrict__ u, int64_t n_u, const int32_t *gate,
+                                                 int32_t *status, Layout L)
+{
+    if (gate && *gate == 0) return;
+    const int64_t base = (int64_t)blockIdx.x * TILE;
+    const bool residual = is_residual(scheme);
+    const bool eq = src.w ? false : src.st->equal;
+    const double lse = src.w ? 0.0 : src.st->lse;
+    u128 sq = 0;
+    uint64_t sqr = 0;
+    int64_t sf = 0;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        const int64_t i = base + j * RT + threadIdx.x;  // striped: coalesced
+        if (i < n) {
+            Quant qq = quantize(src.at(i, lse, eq), residual, m_out, rscale, bad);
+            sq += qq.q;
+            sqr += qq.qr;
+            sf += qq.f;
+            if (is_multinomial(scheme)) L.cnt[i] = 0;
+        }
+    }
+    // explicit uniforms must lie in [0, 1)
+    for (int64_t k = (int64_t)blockIdx.x * RT + threadIdx.x; u && k < n_u; k += (int64_t)gridDim.x * RT)
+        if (!(u[k] >= 0.0 && u[k] < 1.0)) bad = true;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) raise_status(status, SMC_EUNNORMALIZED);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sq += shfl_xor_u128(sq, o);
+        sqr += __shfl_xor_sync(0xffffffffu, sqr, o);
+        sf += __shfl_xor_sync(0xffffffffu, sf, o);
+    }
+    __shared__ u128 s_q[RT / 32];
+    __shared__ uint64_t s_qr[RT / 32];
+    __shared__ int64_t s_f[RT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_q[warp] = sq; s_qr[warp] = sqr; s_f[warp] = sf; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 a = 0;
+        uint64_t b = 0;
+        int64_t c = 0;
+        for (int w = 0; w < RT / 32; ++w) { a += s_q[w]; b += s_qr[w]; c += s_f[w]; }
+        L.tile_q[blockIdx.x] = a;
+        L.tile_qr[blockIdx.x] = b;
+        L.tile_f[blockIdx.x] = c;
+        L.lb_status[blockIdx.x] = 0;
+    }
+}
+
+// ------------------------------------------------------------------ pass S --
+constexpr int SB = 1024;
+
+__global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t nt, uint64_t m_out, Key key,
+                                                uint64_t stream, uint64_t *ctr, const double *__restrict__ u,
+                                                int64_t n_u, const int32_t *gate, int32_t *status, Layout L)
+{
+    __shared__ uint64_t sm64[SB / 32 + 1];
+    __shared__ int s_ok;
+    RsHeader *h = L.hdr;
+    if (gate && *gate == 0) {
+        if (threadIdx.x == 0) h->active = 0;
+        return;
+    }
+    const bool residual = is_residual(scheme);
+    // chunked totals (each thread a contiguous chunk -> deterministic)
+    const int64_t per = (nt + SB - 1) / SB;
+    const int64_t b0 = threadIdx.x * per, b1 = b0 + per < nt ? b0 + per : nt;
+    u128 tq = 0;
+    uint64_t tqr = 0;
+    int64_t tf = 0;
+    for (int64_t b = b0; b < b1; ++b) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
+    // block sums (u128 by halves through shared memory, serial in thread 0)
+    __shared__ u128 s_tq[SB];
+    __shared__ uint64_t s_tqr[SB];
+    __shared__ int64_t s_tf[SB];
+    s_tq[threadIdx.x] = tq;
+    s_tqr[threadIdx.x] = tqr;
+    s_tf[threadIdx.x] = tf;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 T = 0;
+        uint64_t Tr = 0;
+        int64_t F = 0;
+        for (int t = 0; t < SB; ++t) { T += s_tq[t]; Tr += s_tqr[t]; F += s_tf[t]; }
+        int ok = (status == nullptr || *status == 0);
+        if (T < (u128)T_LO || T > (u128)T_HI) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+        int64_t M = (int64_t)m_out;
+        uint64_t Tm = (uint64_t)T;
+        if (ok && residual && n > 1) {
+            M = (int64_t)m_out - F;
+            if (M < 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+            if (M > 0 && Tr == 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+            Tm = Tr;
+        }
+        int64_t draws = 0;
+        if (n > 1 && M > 0)
+            draws = (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC) ? 1 : M;
+        if (ok && u && n_u < draws) { raise_status(status, SMC_EUNIFORMS); ok = 0; }
+        h->T = (uint64_t)T;
+        h->Tm = Tm;
+        h->M = (uint64_t)M;
+        h->draws = draws;
+        h->trivial = (n == 1);
+        h->tile_ctr = 0;
+        h->Z_total = h->S_total = h->P_total = 0;
+        if (ok) {
+            const uint64_t c0 = u ? 0 : *ctr;
+            h->c0 = c0;
+            if (!u) *ctr = c0 + (uint64_t)draws;
+            if (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC)
+                h->m_sys = draws ? (u ? (uint64_t)(u[0] * 9007199254740992.0) : draw53(c0, stream, key)) : 0;
+        }
+        h->active = ok;
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    // exclusive prefix of the searched per-tile totals
+    const uint64_t *src = residual ? L.tile_qr : nullptr;
+    uint64_t mine = 0;
+    for (int64_t b = b0; b < b1; ++b) mine += src ? src[b] : (uint64_t)L.tile_q[b];
+    uint64_t tot;
+    uint64_t run = block_exclusive_sum<SB, uint64_t>(mine, sm64, &tot);
+    for (int64_t b = b0; b < b1; ++b) {
+        L.tile_pre[b] = run;
+        run += src ? src[b] : (uint64_t)L.tile_q[b];
+    }
+}
+
+// ---------------------------------------------- multinomial / residual (M) --
+// Materialize the inclusive CDF Q (or Q') so each draw can binary-search it.
+__global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t n, double m_out, double rscale,
+                                                  Layout L)
+{
+    if (!L.hdr->active || L.hdr->trivial || L.hdr->M == 0) return;
+    __shared__ uint64_t sm[RT / 32 + 1];
+    const bool residual = is_residual(scheme);
+    const bool eq = src.w ? false : src.st->equal;
+    const double lse = src.w ? 0.0 : src.st->lse;
+    const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * RI;  // blocked
+    uint64_t v[RI];
+    uint64_t loc = 0;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        const int64_t i = base + j;
+        v[j] = 0;
+        if (i < n) {
+            Quant qq = quantize(src.at(i, lse, eq), residual, m_out, rscale, bad);
+            v[j] = residual ? qq.qr : qq.q;
+        }
+        loc += v[j];
+    }
+    uint64_t tot;
+    uint64_t run = L.tile_pre[blockIdx.x] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        run += v[j];
+        if (base + j < n) L.qfull[base + j] = run;
+    }
+}
+
+// One thread per draw: position P_k = floor(m_k Tm / 2^53), particle = first i
+// with Q_i > P_k; histogram by atomics (counts are order-independent, A.3).
+__global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t m = u ? (uint64_t)(u[k] * 9007199254740992.0) : draw53(c0 + k, stream, key);
+        const uint64_t P = (uint64_t)(((u128)m * Tm) >> 53);
+        int64_t lo = 0, hi = n - 1;  // P < Tm = Q_{n-1} so the answer exists
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(&L.qfull[mid]) > P) hi = mid; else lo = mid + 1;
+        }
+        atomicAdd(&L.cnt[lo], 1);
+    }
+}
+
+// ------------------------------------------------------------------ pass B --
+struct StratCtx {
+    uint64_t Tm, M, m_sys, c0, stream;
+    const double *u;
+    Key key;
+    bool systematic;
+};
+
+SMC_DEV uint64_t m_of(const StratCtx &c, uint64_t s)
+{
+    if (c.systematic) return c.m_sys;
+    if (c.u) return (uint64_t)(c.u[s] * 9007199254740992.0);
+    return draw53(c.c0 + s, c.stream, c.key);
+}
+
+// F(X) = #{k < M : P_k < X},  P_k = floor((k 2^53 + m_k) Tm / (M 2^53)).
+// k < s := floor(X M / Tm) all qualify, k > s none; k = s iff m_s Tm < (X M - s Tm) 2^53.
+SMC_DEV uint64_t F_strat(const StratCtx &c, uint64_t X)
+{
+    if (X >= c.Tm) return c.M;
+    if (X == 0) return 0;
+    const u128 XM = (u128)X * c.M;
+    double est = (double)X * (double)c.M / (double)c.Tm;
+    uint64_t s = (uint64_t)est;
+    while ((u128)s * c.Tm > XM) --s;
+    while ((u128)(s + 1) * c.Tm <= XM) ++s;
+    const u128 rem = XM - (u128)s * c.Tm;
+    const uint64_t m = m_of(c, s);
+    return s + (((u128)m * c.Tm < (rem << 53)) ? 1 : 0);
+}
+
+// pack (zero slots, surplus parents) in the top, surplus children in the low
+// 40 bits -- tile-local sums never carry across fields (<= 2048, < 2^31).
+SMC_DEV uint64_t pack_zsp(uint32_t z, uint32_t p, uint64_t s) { return ((uint64_t)z << 52) | ((uint64_t)p << 40) | s; }
+SMC_DEV uint32_t unz(uint64_t v) { return (uint32_t)(v >> 52); }
+SMC_DEV uint32_t unp(uint64_t v) { return (uint32_t)((v >> 40) & 0xFFF); }
+SMC_DEV uint64_t uns(uint64_t v) { return v & ((1ull << 40) - 1); }
+
+SMC_DEV uint32_t ld_status(const uint32_t *p) { return *(volatile const uint32_t *)p; }
+
+// mode: 0 = counts from weights (sampler path), 1 = counts given (replication_to_parents)
+__global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src, const int32_t *__restrict__ cin,
+                                                  int64_t n, int64_t nt, double m_out, double rscale, Key key,
+                                                  uint64_t stream, const double *__restrict__ u,
+                                                  int32_t *__restrict__ counts, int32_t *__restrict__ parents,
+                                                  int32_t *status, Layout L)
+{
+    RsHeader *h = L.hdr;
+    if (!h->active) return;
+    __shared__ uint64_t sm[RT / 32 + 1];
+    __shared__ uint32_t s_tile;
+    __shared__ uint4 s_excl;
+    if (h->trivial) {  // N == 1: no-op resample
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (counts) counts[0] = (int32_t)m_out;
+            if (parents) parents[0] = 0;
+            h->Z_total = h->S_total = h->P_total = 0;
+            L.sp_start[0] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
+    __syncthreads();
+    const int64_t b = s_tile;
+    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
+    int32_t c[RI];
+    if (mode == 1) {
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            c[j] = base + j < n ? cin[base + j] : 1;
+            if (c[j] < 0) { bad = true; c[j] = 0; }
+        }
+        if (bad) raise_status(status, SMC_ECOUNTS);
+    } else {
+        const bool residual = is_residual(scheme);
+        const bool eq = src.w ? false : src.st->equal;
+        const double lse = src.w ? 0.0 : src.st->lse;
+        uint64_t q[RI];
+        int64_t f[RI];
+        uint64_t loc = 0;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            q[j] = 0;
+            f[j] = 0;
+            if (base + j < n) {
+                Quant qq = quantize(src.at(base + j, lse, eq), residual, m_out, rscale, bad);
+                q[j] = residual ? qq.qr : qq.q;
+                f[j] = qq.f;
+            }
+            loc += q[j];
+        }
+        if (is_multinomial(scheme)) {
+#pragma unroll
+            for (int j = 0; j < RI; ++j) c[j] = base + j < n ? (int32_t)f[j] + L.cnt[base + j] : 1;
+        } else {
+            uint64_t tot;
+            uint64_t X = L.tile_pre[b] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
+            StratCtx sc;
+            sc.Tm = h->Tm;
+            sc.M = h->M;
+            sc.m_sys = h->m_sys;
+            sc.c0 = h->c0;
+            sc.stream = stream;
+            sc.u = u;
+            sc.key = key;
+            sc.systematic = (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC);
+            uint64_t Fp = (base < n && sc.M) ? F_strat(sc, X) : 0;
+#pragma unroll
+            for (int j = 0; j < RI; ++j) {
+                if (base + j < n) {
+                    uint64_t Fc = Fp;
+                    if (q[j] && sc.M) { X += q[j]; Fc = F_strat(sc, X); }
+                    c[j] = (int32_t)(f[j] + (int64_t)(Fc - Fp));
+                    Fp = Fc;
+                } else {
+                    c[j] = 1;  // padding: neither zero slot nor surplus
+                }
+            }
+        }
+    }
+    if (counts) {
+#pragma unroll
+        for (int j = 0; j < RI; ++j)
+            if (base + j < n) counts[base + j] = c[j];
+    }
+    if (!parents) return;
+    // ---- parent map: decoupled lookback over (Z, S, P) ----
+    uint32_t tz = 0, tp = 0;
+    uint64_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        tz += (c[j] == 0);
+        tp += (c[j] >= 2);
+        ts += c[j] >= 2 ? (uint64_t)(c[j] - 1) : 0;
+    }
+    uint64_t agg;
+    const uint64_t tex = block_exclusive_sum<RT, uint64_t>(pack_zsp(tz, tp, ts), sm, &agg);
+    const uint4 a4 = make_uint4(unz(agg), (uint32_t)uns(agg), unp(agg), 0);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint4 ex = make_uint4(0, 0, 0, 0);
+        if (b == 0) {
+            if (lane == 0) {
+                L.lb_incl[0] = a4;
+                __threadfence();
+                atomicExch(&L.lb_status[0], 2u);
+            }
+        } else {
+            if (lane == 0) {
+                L.lb_agg[b] = a4;
+                __threadfence();
+                atomicExch(&L.lb_status[b], 1u);
+            }
+            int64_t pred = b - 1;
+            for (;;) {
+                const int64_t jb = pred - lane;
+                uint32_t stv = 2;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (jb >= 0) {
+                    do { stv = ld_status(&L.lb_status[jb]); } while (stv == 0);
+                    __threadfence();
+                    v = stv == 2 ? __ldcg(&L.lb_incl[jb]) : __ldcg(&L.lb_agg[jb]);
+                }
+                const unsigned m2 = __ballot_sync(0xffffffffu, stv == 2);
+                const int stop = m2 ? __ffs(m2) - 1 : 32;
+                if (lane > stop) v = make_uint4(0, 0, 0, 0);
+                ex.x += warp_sum(v.x);
+                ex.y += warp_sum(v.y);
+                ex.z += warp_sum(v.z);
+                if (m2) break;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                L.lb_incl[b] = make_uint4(ex.x + a4.x, ex.y + a4.y, ex.z + a4.z, 0);
+                __threadfence();
+                atomicExch(&L.lb_status[b], 2u);
+            }
+        }
+        if (lane == 0) {
+            s_excl = ex;
+            if (b == nt - 1) {
+                const uint32_t Z = ex.x + a4.x, S = ex.y + a4.y, P = ex.z + a4.z;
+                h->Z_total = Z;
+                h->S_total = S;
+                h->P_total = P;
+                L.sp_start[P] = (int32_t)S;  // sentinel
+                if (Z != S) raise_status(status, SMC_ECOUNTS);  // sum(counts) != N
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t zr = s_excl.x + unz(tex);
+    uint32_t sr = s_excl.y + (uint32_t)uns(tex);
+    uint32_t pr = s_excl.z + unp(tex);
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        const int64_t i = base + j;
+        if (i >= n) break;
+        if (c[j] >= 1) {
+            parents[i] = (int32_t)i;  // survivors keep their slot
+            if (c[j] >= 2) {
+                L.sp_idx[pr] = (int32_t)i;
+                L.sp_start[pr] = (int32_t)sr;
+                ++pr;
+                sr += (uint32_t)(c[j] - 1);
+            }
+        } else {
+            L.zpos[zr++] = (int32_t)i;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ pass C --
+SMC_DEV void copy_row(char *rows, int64_t row_bytes, int64_t dst, int64_t srcr)
+{
+    if (row_bytes == 32) {
+        const double *s = (const double *)(rows + srcr * 32);
+        double *d = (double *)(rows + dst * 32);
+        double a, b2, c2, d2;
+        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b2), "=d"(c2), "=d"(d2) : "l"(s));
+        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(d), "d"(a), "d"(b2), "d"(c2), "d"(d2) : "memory");
+    } else if ((row_bytes & 15) == 0) {
+        const int4 *s = (const int4 *)(rows + srcr * row_bytes);
+        int4 *d = (int4 *)(rows + dst * row_bytes);
+        for (int64_t k = 0; k < row_bytes / 16; ++k) d[k] = __ldg(s + k);
+    } else {
+        const int64_t *s = (const int64_t *)(rows + srcr * row_bytes);
+        int64_t *d = (int64_t *)(rows + dst * row_bytes);
+        for (int64_t k = 0; k < row_bytes / 8; ++k) d[k] = __ldg((const long long *)(s + k));
+    }
+}
+
+__global__ void __launch_bounds__(RT) k_rs_assign(int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
+                                                  Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    const uint32_t Z = h->Z_total, P = h->P_total;
+    const uint32_t r0 = blockIdx.x * (uint32_t)TILE;
+    if (r0 >= Z) return;
+    const uint32_t r1 = r0 + TILE < Z ? r0 + TILE : Z;
+    __shared__ int32_t s_start[TILE + 1], s_idx[TILE + 1];
+    __shared__ uint32_t s_lo, s_cnt;
+    if (threadIdx.x == 0) {
+        // last p with sp_start[p] <= r  (sp_start strictly increasing, sentinel at P)
+        auto ub = [&](uint32_t r) {
+            uint32_t lo = 0, hi = P;  // first index with sp_start > r, in [0, P]
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((uint32_t)__ldcg(&L.sp_start[mid]) > r) hi = mid; else lo = mid + 1;
+            }
+            return lo;
+        };
+        const uint32_t plo = ub(r0) - 1, phi = ub(r1 - 1) - 1;
+        s_lo = plo;
+        s_cnt = phi - plo + 1;
+    }
+    __syncthreads();
+    const uint32_t plo = s_lo, cnt = s_cnt;  // cnt <= r1 - r0: every surplus parent covers >= 1 rank
+    for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
+        s_start[k] = __ldcg(&L.sp_start[plo + k]);
+        s_idx[k] = __ldcg(&L.sp_idx[plo + k]);
+    }
+    __syncthreads();
+    for (uint32_t r = r0 + threadIdx.x; r < r1; r += RT) {  // striped ranks
+        uint32_t lo = 0, hi = cnt;  // last k with s_start[k] <= r
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint32_t)s_start[mid] <= r) lo = mid; else hi = mid;
+        }
+        const int32_t par = s_idx[lo];
+        const int32_t j = __ldcg(&L.zpos[r]);
+        if (parents) parents[j] = par;
+        if (rows) copy_row(rows, row_bytes, j, par);
+    }
+}
+
+__global__ void k_rs_reset(int64_t n, int64_t nt, Layout L)
+{
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nt; b += (int64_t)gridDim.x * blockDim.x)
+        L.lb_status[b] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        RsHeader *h = L.hdr;
+        h->active = 1;
+        h->trivial = 0;
+        h->tile_ctr = 0;
+        h->Z_total = h->S_total = h->P_total = 0;
+    }
+}
+
+__global__ void __launch_bounds__(RT) k_copy_inplace(char *rows, int64_t row_bytes, const int32_t *__restrict__ parents,
+                                                     int64_t n, const int32_t *gate)
+{
+    if (gate && *gate == 0) return;
+    for (int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x; j < n; j += (int64_t)gridDim.x * RT) {
+        const int32_t p = parents[j];
+        if (p != j) copy_row(rows, row_bytes, j, p);
+    }
+}
+
+__global__ void __launch_bounds__(RT) k_gather(char *__restrict__ dst, const char *__restrict__ src, int64_t row_bytes,
+                                               const int32_t *__restrict__ parents, int64_t n)
+{
+    const int64_t words = row_bytes / 8;
+    const int64_t total = n * words;
+    for (int64_t e = (int64_t)blockIdx.x * RT + threadIdx.x; e < total; e += (int64_t)gridDim.x * RT) {
+        const int64_t j = e / words, k = e - j * words;
+        ((int64_t *)dst)[e] = __ldg((const long long *)src + (int64_t)parents[j] * words + k);
+    }
+}
+
+inline int grid_cap(int64_t blocks)
+{
+    return (int)(blocks < 1 ? 1 : (blocks > 148 * 16 ? 148 * 16 : blocks));
+}
+
+}  // namespace
+
+extern "C" size_t smc_resample_workspace_bytes(int64_t n)
+{
+    if (n < 1) n = 1;
+    return layout(nullptr, n).bytes;
+}
+
+extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, const smc_wstate *st, int64_t n,
+                            int64_t m_out, uint64_t seed, uint64_t stream_index, uint64_t *ctr, const double *u,
+                            int64_t n_u, int32_t *counts, int32_t *parents, void *rows, int64_t row_bytes,
+                            const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (scheme < 0 || scheme > 5 || n < 1 || n >= ((int64_t)1 << 31) - TILE || m_out < 1 ||
+        m_out >= ((int64_t)1 << 31))
+        return smc_set_error(SMC_EINVAL, "smc_resample: bad scheme/size (scheme=%d n=%lld m=%lld)", scheme,
+                             (long long)n, (long long)m_out);
+    if (!w && (!lw_raw || !st)) return smc_set_error(SMC_EINVAL, "smc_resample: need w or (lw_raw, state)");
+    if (!u && !ctr) return smc_set_error(SMC_EINVAL, "smc_resample: need uniforms or a stream counter");
+    if ((parents || rows) && m_out != n)
+        return smc_set_error(SMC_EINVAL, "smc_resample: parent map / copy need m_out == n");
+    if (rows && (row_bytes < 8 || (row_bytes & 7)))
+        return smc_set_error(SMC_EINVAL, "smc_resample: row_bytes must be a positive multiple of 8");
+    if (rows && row_bytes == 32 && ((uintptr_t)rows & 31))
+        return smc_set_error(SMC_EINVAL, "smc_resample: 32-byte rows must be 32-byte aligned");
+    if (!ws || ws_bytes < smc_resample_workspace_bytes(n))
+        return smc_set_error(SMC_EWORKSPACE, "smc_resample: workspace too small");
+    const int64_t nt = (n + TILE - 1) / TILE;
+    Layout L = layout(ws, n);
+    int L2 = 0;
+    while (((int64_t)1 << L2) < n) ++L2;
+    const double rscale = ldexp(1.0, 63 - L2);
+    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    WSrc src{w, lw_raw, st, n};
+    const double mo = (double)m_out;
+
+    k_rs_tiles<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L);
+    if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
+        k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
+        k_rs_multinomial<<<grid_cap((m_out + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
+    }
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(0, scheme, src, nullptr, n, nt, mo, rscale, key, stream_index, u,
+                                            counts, parents, status, L);
+    if (parents || rows)
+        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, (char *)rows, row_bytes, L);
+    return smc_check_launch("smc_resample");
+}
+
+extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int32_t *parents, int32_t *status, void *ws,
+                                          size_t ws_bytes, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || n >= ((int64_t)1 << 31) - TILE || !counts || !parents)
+        return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: bad args");
+    if (!ws || ws_bytes < smc_resample_workspace_bytes(n))
+        return smc_set_error(SMC_EWORKSPACE, "smc_replication_to_parents: workspace too small");
+    const int64_t nt = (n + TILE - 1) / TILE;
+    Layout L = layout(ws, n);
+    WSrc src{nullptr, nullptr, nullptr, n};
+    k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(1, 0, src, counts, n, nt, 0.0, 0.0, Key{0, 0}, 0, nullptr, nullptr,
+                                            parents, status, L);
+    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, nullptr, 0, L);
+    return smc_check_launch("smc_replication_to_parents");
+}
+
+extern "C" int smc_copy_rows_inplace(void *rows, int64_t row_bytes, const int32_t *parents, int64_t n,
+                                     const int32_t *gate, void *stream)
+{
+    if (!rows || !parents || n < 1 || row_bytes < 8 || (row_bytes & 7) ||
+        (row_bytes == 32 && ((uintptr_t)rows & 31)))
+        return smc_set_error(SMC_EINVAL, "smc_copy_rows_inplace: bad args");
+    k_copy_inplace<<<grid_cap((n + RT - 1) / RT), RT, 0, (cudaStream_t)stream>>>((char *)rows, row_bytes, parents,
+                                                                                 n, gate);
+    return smc_check_launch("smc_copy_rows_inplace");
+}
+
+extern "C" int smc_gather_rows(void *dst, const void *src, int64_t row_bytes, const int32_t *parents, int64_t n,
+                               void *stream)
+{
+    if (!dst || !src || dst == src || !parents || n < 1 || row_bytes < 8 || (row_bytes & 7))
+        return smc_set_error(SMC_EINVAL, "smc_gather_rows: bad args");
+    k_gather<<<grid_cap((n * (row_bytes / 8) + RT - 1) / RT), RT, 0, (cudaStream_t)stream>>>(
+        (char *)dst, (const char *)src, row_bytes, parents, n);
+    return smc_check_launch("smc_gather_rows");
+}

@@ -1,0 +1,243 @@
+// smc_weights.cu -- WeightSet on the device (replaces smckit.weights),
+// the ESS trigger and the monitor/path weighted sums
+// (SPEC.md:320-333, :403-416).
+//
+// Storage: lw_raw[N] plus a device smc_wstate {lse, ess, ...}.  The normalized
+// log-weight is lw_raw - lse (or -log N after set_equal_weight, which only
+// flips a flag) so normalization never needs a second write pass.
+#include "smc_weights.cuh"
+
+using namespace smc;
+
+namespace {
+
+constexpr int WB = 256;  // threads per block of the per-element passes
+
+// One element per thread: new raw log-weight for the requested mutation.
+__global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restrict__ lw_raw,
+                                                      const double *__restrict__ values, int64_t n,
+                                                      smc_wstate *st, LsePartial *__restrict__ parts)
+{
+    const int64_t i = (int64_t)blockIdx.x * WB + threadIdx.x;
+    double v = -INFINITY;
+    if (i < n) {
+        double prev = 0.0;
+        if (mode == SMC_W_ADD_LOG || mode == SMC_W_MUL_LIN)
+            prev = st->equal ? -log((double)n) : lw_raw[i] - st->lse;
+        const double x = values[i];
+        switch (mode) {
+        case SMC_W_SET_LOG: v = x; break;
+        case SMC_W_ADD_LOG: v = prev + x; break;
+        case SMC_W_SET_LIN: v = (x >= 0.0) ? log(x) : NAN; break;
+        default: v = (x >= 0.0) ? prev + log(x) : NAN; break;  // MUL_LIN
+        }
+        if (isnan(v) || v == INFINITY) {
+            raise_status(&st->status, SMC_ENORMALIZE);
+            v = -INFINITY;
+        }
+        lw_raw[i] = v;
+    }
+    LsePartial p = block_lse_partial<WB>(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+}
+
+constexpr int FB = 1024;
+
+__global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ parts, int nparts,
+                                                      smc_wstate *st, int64_t n, int mode, int accumulate_nc)
+{
+    __shared__ LsePartial sm[FB / 32];
+    LsePartial acc{-INFINITY, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += FB) acc = lse_combine(acc, parts[b]);
+    // fixed-shape tree: xor shuffles, then warp partials in index order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        LsePartial o_{__shfl_xor_sync(0xffffffffu, acc.m, o), __shfl_xor_sync(0xffffffffu, acc.s1, o),
+                      __shfl_xor_sync(0xffffffffu, acc.s2, o)};
+        acc = lse_combine(acc, o_);
+    }
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LsePartial t = sm[0];
+        for (int w = 1; w < FB / 32; ++w) t = lse_combine(t, sm[w]);
+        if (t.m == -INFINITY || !(t.s1 > 0.0)) {
+            raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
+            return;
+        }
+        const double lse = t.m + log(t.s1);
+        st->lse = lse;
+        st->max_raw = t.m;
+        st->ess = (t.s1 * t.s1) / t.s2;  // 1 / sum W^2 with W = e / s1
+        st->ess_over_n = st->ess / (double)n;
+        st->equal = 0;
+        if (mode == SMC_W_ADD_LOG) {
+            // previous lw was normalized => log sum_i W_{t-1,i} exp(incw_i) = lse
+            st->nc_inc = lse;
+            if (accumulate_nc) st->log_zconst += lse;
+        } else if (mode == SMC_W_SET_LOG && accumulate_nc) {
+            // first weighting from the equal-weight prior sample: log (1/N) sum_i exp(v_i)
+            st->nc_inc = lse - log((double)n);
+            st->log_zconst = st->nc_inc;
+        }
+    }
+}
+
+__global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
+{
+    if (gate && *gate == 0) return;
+    st->equal = 1;
+    st->lse = log((double)n);  // consistent with lw_raw == 0 everywhere
+    st->max_raw = 0.0;
+    st->ess = (double)n;
+    st->ess_over_n = 1.0;
+}
+
+__global__ void k_weights_read(int what, const double *__restrict__ lw_raw, const smc_wstate *st, int64_t n,
+                               double *__restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double l = st->equal ? -log((double)n) : lw_raw[i] - st->lse;
+    out[i] = what == SMC_READ_WEIGHT ? (st->equal ? 1.0 / (double)n : exp(l)) : l;
+}
+
+// SPEC.md:266 / SURVEY R8: threshold >= 1 always, <= 0 never, else ess/N < threshold.
+__global__ void k_ess_decide(smc_wstate *st, double threshold, double *hist_row)
+{
+    const double eon = st->ess_over_n;
+    int r = threshold >= 1.0 ? 1 : (threshold <= 0.0 ? 0 : (eon < threshold ? 1 : 0));
+    if (st->status) r = 0;  // never resample on a failed normalization
+    st->resample = r;
+    if (hist_row) { hist_row[0] = eon; hist_row[1] = (double)r; }
+}
+
+// ---------------------------------------------------------------- reduce ----
+constexpr int RB = 256;
+constexpr int RMAX = 8;  // columns per pass
+
+__global__ void __launch_bounds__(RB) k_wsum_pass(const double *__restrict__ vals, int64_t ld, int m0, int mc,
+                                                   const double *__restrict__ lw_raw, const smc_wstate *st,
+                                                   int64_t n, double *__restrict__ parts, int mtot)
+{
+    __shared__ double sm[RB / 32][RMAX];
+    double acc[RMAX];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) acc[j] = 0.0;
+    const bool eq = st->equal;
+    const double lse = st->lse, inv_n = 1.0 / (double)n;
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double w = eq ? inv_n : exp(lw_raw[i] - lse);
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+            if (j < mc) acc[j] += w * vals[i * ld + m0 + j];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) {
+        double v = warp_sum(acc[j]);
+        if (lane == 0) sm[warp][j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < mc) {
+        double v = 0.0;
+        for (int w = 0; w < RB / 32; ++w) v += sm[w][threadIdx.x];
+        parts[(int64_t)blockIdx.x * mtot + m0 + threadIdx.x] = v;
+    }
+}
+
+__global__ void k_wsum_final(const double *__restrict__ parts, int nb, int m, double *__restrict__ out)
+{
+    // one warp per column, fixed order
+    const int j = blockIdx.x;
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) v += parts[(int64_t)b * m + j];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[j] = v;
+}
+
+inline int reduce_blocks(int64_t n)
+{
+    int64_t g = (n + RB - 1) / RB;
+    return (int)(g < 1 ? 1 : (g > 148 * 8 ? 148 * 8 : g));
+}
+
+}  // namespace
+
+void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
+                             int accumulate_nc, cudaStream_t s)
+{
+    k_lse_finalize<<<1, FB, 0, s>>>(parts, nparts, st, n, mode, accumulate_nc);
+}
+
+extern "C" size_t smc_weights_workspace_bytes(int64_t n)
+{
+    return (size_t)((n + WB - 1) / WB + 1) * sizeof(LsePartial);
+}
+
+extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values, int64_t n, smc_wstate *st,
+                                  int accumulate_nc, void *ws, size_t ws_bytes, void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || n >= (int64_t)1 << 31 || !st || mode < 0 || mode > 4)
+        return smc_set_error(SMC_EINVAL, "smc_weights_update: bad args (mode=%d n=%lld)", mode, (long long)n);
+    if (mode == SMC_W_EQUAL) {
+        k_set_equal<<<1, 1, 0, s>>>(st, n, nullptr);
+        return smc_check_launch("smc_weights_update(equal)");
+    }
+    if (!lw_raw || !values) return smc_set_error(SMC_EINVAL, "smc_weights_update: null vector");
+    if (ws_bytes < smc_weights_workspace_bytes(n) || !ws)
+        return smc_set_error(SMC_EWORKSPACE, "smc_weights_update: workspace too small");
+    const int nb = (int)((n + WB - 1) / WB);
+    LsePartial *parts = (LsePartial *)ws;
+    k_weights_pass<<<nb, WB, 0, s>>>(mode, lw_raw, values, n, st, parts);
+    k_lse_finalize<<<1, FB, 0, s>>>(parts, nb, st, n, mode, accumulate_nc);
+    return smc_check_launch("smc_weights_update");
+}
+
+extern "C" int smc_weights_set_equal(smc_wstate *st, int64_t n, const int32_t *gate, void *stream)
+{
+    if (!st || n < 1) return smc_set_error(SMC_EINVAL, "smc_weights_set_equal: bad args");
+    k_set_equal<<<1, 1, 0, (cudaStream_t)stream>>>(st, n, gate);
+    return smc_check_launch("smc_weights_set_equal");
+}
+
+extern "C" int smc_weights_read(int what, const double *lw_raw, const smc_wstate *st, int64_t n, double *out,
+                                void *stream)
+{
+    if (n < 1 || !st || !out || !lw_raw || (what != 0 && what != 1))
+        return smc_set_error(SMC_EINVAL, "smc_weights_read: bad args");
+    k_weights_read<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(what, lw_raw, st, n, out);
+    return smc_check_launch("smc_weights_read");
+}
+
+extern "C" int smc_ess_decide(smc_wstate *st, int64_t n, double threshold, double *hist_row, void *stream)
+{
+    if (!st || n < 1) return smc_set_error(SMC_EINVAL, "smc_ess_decide: bad args");
+    k_ess_decide<<<1, 1, 0, (cudaStream_t)stream>>>(st, threshold, hist_row);
+    return smc_check_launch("smc_ess_decide");
+}
+
+extern "C" size_t smc_weighted_reduce_workspace_bytes(int64_t n, int64_t m)
+{
+    return (size_t)reduce_blocks(n) * (size_t)(m > 0 ? m : 1) * sizeof(double);
+}
+
+extern "C" int smc_weighted_reduce(const double *vals, int64_t ld, int64_t m, const double *lw_raw,
+                                   const smc_wstate *st, int64_t n, double *out, void *ws, size_t ws_bytes,
+                                   void *stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n < 1 || m < 1 || ld < m || !vals || !lw_raw || !st || !out || m > 4096)
+        return smc_set_error(SMC_EINVAL, "smc_weighted_reduce: bad args");  // SPEC.md:409 m=0 rejected
+    if (!ws || ws_bytes < smc_weighted_reduce_workspace_bytes(n, m))
+        return smc_set_error(SMC_EWORKSPACE, "smc_weighted_reduce: workspace too small");
+    const int nb = reduce_blocks(n);
+    double *parts = (double *)ws;
+    for (int m0 = 0; m0 < m; m0 += RMAX) {
+        const int mc = (int)((m - m0) < RMAX ? (m - m0) : RMAX);
+        k_wsum_pass<<<nb, RB, 0, s>>>(vals, ld, m0, mc, lw_raw, st, n, parts, (int)m);
+    }
+    k_wsum_final<<<(unsigned)m, 32, 0, s>>>(parts, nb, (int)m, out);
+    return smc_check_launch("smc_weighted_reduce");
+}

@@ -1,0 +1,187 @@
+"""WeightSet, monitors, NC and the PF kernels vs the oracle (fp64, tolerance 1e-12 / 1e-6 relative)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6  # north_star: log-weights, ESS, monitors, log Z within 1e-6 relative in fp64
+
+
+def test_weights_spec_examples_device():
+    from paper_1306_5583_b200 import WeightSet, _abi
+    ws = WeightSet(4)
+    assert ws.read_weight().tolist() == [0.25] * 4 and ws.ess() == 4
+    ws = WeightSet(3)
+    ws.set_log_weight([0.0, 0.0, 0.0])
+    assert np.allclose(ws.read_weight().cpu(), 1 / 3, atol=1e-15)
+    ws = WeightSet(2)
+    ws.set_log_weight([1000.0, 1000.0])
+    assert ws.read_weight().tolist() == [0.5, 0.5]
+    ws.set_log_weight([5.0, 5.0 + math.log(2)])
+    assert np.allclose(ws.read_weight().cpu(), [1 / 3, 2 / 3], atol=1e-15)
+    ws.set_log_weight(np.log([0.5, 0.5]))
+    ws.add_log_weight([math.log(3), 0.0])
+    assert np.allclose(ws.read_weight().cpu(), [0.75, 0.25], atol=1e-15)
+    ws.set_log_weight([0.0, -np.inf])
+    ws.add_log_weight([0.0, 5.0])
+    assert ws.read_weight().tolist() == [1.0, 0.0]
+    ws = WeightSet(4)
+    ws.set_weight([2, 2, 2, 2])
+    assert np.allclose(ws.read_weight().cpu(), 0.25, atol=1e-16)
+    ws.set_equal_weight()
+    ws.mul_weight([1, 1, 1, 3])
+    assert np.allclose(ws.read_weight().cpu(), [1 / 6, 1 / 6, 1 / 6, 0.5], atol=1e-15)
+    ws = WeightSet(3)
+    ws.set_log_weight(np.log([0.5, 0.25, 0.25]))
+    assert abs(ws.ess() - 8 / 3) < 1e-12
+    ws = WeightSet(2)
+    ws.set_log_weight([0.0, 0.0])
+    assert np.allclose(ws.read_log_weight().cpu(), -math.log(2), atol=1e-15)
+    with pytest.raises(_abi.SmcError):
+        ws.set_log_weight([-np.inf, -np.inf])
+    with pytest.raises(_abi.SmcError):
+        ws.set_log_weight([0.0, np.nan])
+
+
+@pytest.mark.parametrize("n", [1, 5, 255, 256, 257, 100000, 1 << 22])
+def test_weights_vs_oracle(n):
+    from paper_1306_5583_b200 import WeightSet
+    rng = np.random.default_rng(n)
+    v = rng.normal(0, 5, n)
+    inc = rng.normal(0, 2, n)
+    lw, w, ess = O.normalize_log(v)
+    nc = O.nc_increment(lw, inc)
+    ess2 = O.weights_update(O.W_ADD_LOG, lw, w, inc)
+    ws = WeightSet(n)
+    ws.set_log_weight(v)
+    assert abs(ws.ess() - ess) <= 1e-12 * ess
+    ws.add_log_weight(inc)
+    st = ws.host_state()
+    assert abs(st.ess - ess2) <= 1e-12 * ess2
+    assert abs(st.nc_inc - nc) <= 1e-12 * max(1.0, abs(nc))
+    np.testing.assert_allclose(ws.read_log_weight().cpu().numpy(), lw, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(ws.read_weight().cpu().numpy(), w, rtol=1e-11, atol=1e-300)
+
+
+def test_weighted_reduce_monitor():
+    from paper_1306_5583_b200 import Sampler, StateMatrix, WeightSet, _abi
+    n, m = 100003, 3
+    rng = np.random.default_rng(4)
+    vals = rng.normal(size=(n, m))
+    v = rng.normal(0, 2, n)
+    _, w, _ = O.normalize_log(v)
+    ref = np.zeros(m)
+    O.lib().orc_weighted_sum(w, vals, n, m, ref)
+    ws = WeightSet(n)
+    ws.set_log_weight(v)
+    out = torch.zeros(m, dtype=torch.float64, device="cuda")
+    buf = _abi.Workspace("cuda")
+    b, nb = buf.get(_abi.lib().smc_weighted_reduce_workspace_bytes(n, m))
+    g = torch.as_tensor(vals).cuda().contiguous()
+    _abi.call("smc_weighted_reduce", _abi.ptr(g), m, m, _abi.ptr(ws.lw_raw), ws.state_ptr, n, _abi.ptr(out), b, nb,
+              _abi.stream())
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-10, atol=1e-14)
+
+
+def _obs(T=100, seed=1306):
+    from paper_1306_5583_b200 import pf
+    return pf.generate_observations(T, seed)
+
+
+def test_pf_single_move_matches_oracle():
+    from paper_1306_5583_b200 import pf
+    n = 10000
+    obs, _ = _obs(5)
+    s = pf.make_sampler(n, "systematic", threshold=-1.0, seed=99)
+    s.initialize(obs)
+    st = O.Streams(n + 1, 99)
+    x, llh = O.cv_init(n, st, obs[0])
+    np.testing.assert_allclose(s.system.value.data.cpu().numpy(), x, rtol=1e-14, atol=1e-14)
+    lw, w, ess = O.normalize_log(llh)
+    assert abs(s.system.weight_set.ess() - ess) <= 1e-12 * ess
+    s.iterate(1)
+    incw = O.cv_move(x, st, obs[1])
+    O.weights_update(O.W_ADD_LOG, lw, w, incw)
+    np.testing.assert_allclose(s.system.value.data.cpu().numpy(), x, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(s.system.weight_set.read_log_weight().cpu().numpy(), lw, rtol=1e-11, atol=1e-11)
+    assert s.system.rng_set.counters_host()[:n] == [int(c) for c in st.counters[:n]]
+
+
+@pytest.mark.parametrize("scheme", ["systematic", "stratified", "multinomial", "residual", "residual_stratified",
+                                    "residual_systematic"])
+def test_pf_full_run_matches_oracle(scheme):
+    """Config 1 (N=10^4, 100 obs, ESS<N/2): GPU RNG end to end vs the oracle."""
+    from paper_1306_5583_b200 import pf
+    n = 10000
+    obs, _ = _obs(100)
+    s = pf.make_sampler(n, scheme, threshold=0.5, seed=1306)
+    s.initialize(obs)
+    s.iterate(99)
+    h = s.history()
+    ref = O.pf_run(n, 1306, scheme, 0.5, obs)
+    assert np.array_equal(h["resampled"], ref[:, 1])
+    np.testing.assert_allclose(h["ess_over_n"], ref[:, 0], rtol=RTOL)
+    np.testing.assert_allclose(h["pos.0"], ref[:, 2], rtol=RTOL, atol=1e-9)
+    np.testing.assert_allclose(h["pos.1"], ref[:, 3], rtol=RTOL, atol=1e-9)
+    assert abs(s.log_zconst - ref[-1, 4]) <= RTOL * abs(ref[-1, 4])
+
+
+def test_pf_beats_observations_acceptance_6():
+    from paper_1306_5583_b200 import pf
+    wins = 0
+    for seed in range(10):
+        obs, truth = _obs(100, 100 + seed)
+        s = pf.make_sampler(1000, "stratified", 0.5, seed=seed)
+        s.initialize(obs)
+        s.iterate(99)
+        h = s.history()
+        est = np.stack([h["pos.0"], h["pos.1"]], 1)
+        wins += np.mean((est - truth[:, :2]) ** 2) < np.mean((obs - truth[:, :2]) ** 2)
+    assert wins >= 9
+
+
+def test_history_invariants_and_tsv(tmp_path):
+    from paper_1306_5583_b200 import pf
+    obs, _ = _obs(30)
+    s = pf.make_sampler(4096, "stratified", 0.5, seed=3)
+    s.initialize(obs)
+    s.iterate(29)
+    h = s.history()
+    assert len(h["iter"]) == 30
+    assert np.all((h["resampled"] == 1) == (h["ess_over_n"] < 0.5))
+    text = s.write_tsv(tmp_path / "pf.est", ["seed=3"])
+    lines = text.splitlines()
+    assert lines[1].split("\t") == ["iter", "ess_over_n", "resampled", "accept.0", "pos.0", "pos.1"]
+    assert len(lines) == 32
+    s2 = pf.make_sampler(4096, "stratified", 0.5, seed=3)
+    s2.initialize(obs)
+    s2.iterate(29)
+    assert s2.write_tsv(tmp_path / "b.est", ["seed=3"]) == text  # byte-identical reruns
+
+
+def test_threshold_rules():
+    from paper_1306_5583_b200 import pf
+    obs, _ = _obs(10)
+    for thr, expect in ((1.5, 1.0), (-1.0, 0.0)):
+        s = pf.make_sampler(2000, "systematic", thr, seed=1)
+        s.initialize(obs)
+        s.iterate(9)
+        assert np.all(s.history()["resampled"] == expect)
+
+
+def test_statematrix_copy_simultaneous():
+    from paper_1306_5583_b200 import StateMatrix
+    m = StateMatrix(2, 3)
+    m.data.copy_(torch.tensor([[1.0, 2, 3], [4, 5, 6]]))
+    m.copy_particles([1, 0])
+    assert m.data.tolist() == [[4, 5, 6], [1, 2, 3]]
+    c = StateMatrix(3, 2, order="col")
+    c.data.copy_(torch.tensor([[1.0, 2, 3], [4, 5, 6]]))
+    c.copy_particles([0, 0, 2])
+    assert c.read_state(0).tolist() == [1, 1, 3] and c.read_state(1).tolist() == [4, 4, 6]
