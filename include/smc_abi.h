@@ -78,8 +78,10 @@ int smc_rng_draw_streams(int kind, uint64_t seed, uint64_t first_stream, int64_t
 /* Weights -- replaces smckit.weights.WeightSet             */
 /* ------------------------------------------------------------------------ */
 /* Device-resident weight state.  The log-weight vector is stored RAW
- * (lw_raw); the normalized log-weight is lw_raw[i] - lse, or -log(N) for every
- * i when `equal` is set (set_equal_weight never touches the vector). */
+ * (lw_raw); the normalized log-weight is (lw_raw[i] - max_raw) - log_sum,
+ * the oracle's max-shift + log-sum-exp order, or -log(N) for
+ * every i when `equal` is set (set_equal_weight never touches the vector;
+ * it sets max_raw = 0, log_sum = log N). */
 typedef struct smc_wstate {
     double lse;        /* log sum_i exp(lw_raw_i)                               */
     double ess;        /* 1 / sum_i W_i^2                         */
@@ -87,6 +89,7 @@ typedef struct smc_wstate {
     double nc_inc;     /* log sum_i W_{t-1,i} exp(incw_i) of the last ADD_LOG   */
     double log_zconst; /* running NormalizingConstant         */
     double max_raw;    /* max_i lw_raw_i                                        */
+    double log_sum;    /* log sum_i exp(lw_raw_i - max_raw); lse = max + this   */
     int32_t equal;     /* 1 after set_equal_weight                              */
     int32_t status;    /* sticky device error (SMC_E*), 0 when healthy          */
     int32_t resample;  /* decision of the last smc_ess_decide     */
@@ -109,7 +112,7 @@ int smc_weights_update(int mode, double *lw_raw, const double *values, int64_t n
 /* set_equal_weight gated by a device flag (skipped when
  * gate != NULL and *gate == 0): the post-resample reset of the sampler loop. */
 int smc_weights_set_equal(smc_wstate *ws_state, int64_t n, const int32_t *gate, void *stream);
-/* read_log_weight / read_weight: out = lw_raw - lse or exp(.) */
+/* read_log_weight / read_weight: the normalized log-weight or its exp */
 int smc_weights_read(int what, const double *lw_raw, const smc_wstate *ws_state, int64_t n, double *out,
                      void *stream);
 /* ESS trigger: resample iff
@@ -140,7 +143,7 @@ size_t smc_resample_workspace_bytes(int64_t n);
 /* resample_<scheme>(W, stream) -> counts, + replication_to_parents, + the
  * value collection's copy, under the pinned
  * integer CDF contract.  Weights come from `w` (normalized W) or,
- * when w == NULL, from (lw_raw, ws_state) as W_i = exp(lw_raw_i - lse).
+ * when w == NULL, from (lw_raw, ws_state) as W_i = exp(normalized lw_i).
  * Uniforms come from `u` (device, n_u of them) or, when u == NULL, from
  * stream `stream_index` of key(seed) starting at *ctr, which is advanced on
  * the device by the number of draws.  m_out is the number of

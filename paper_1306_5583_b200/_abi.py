@@ -44,7 +44,7 @@ class SmcWState(C.Structure):
 
     _fields_ = [
         ("lse", C.c_double), ("ess", C.c_double), ("ess_over_n", C.c_double), ("nc_inc", C.c_double),
-        ("log_zconst", C.c_double), ("max_raw", C.c_double), ("equal", C.c_int32), ("status", C.c_int32),
+        ("log_zconst", C.c_double), ("max_raw", C.c_double), ("log_sum", C.c_double), ("equal", C.c_int32), ("status", C.c_int32),
         ("resample", C.c_int32), ("iter", C.c_int32),
     ]
 

@@ -96,6 +96,17 @@ SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, Key key, double shape)
 }
 
 // ---------------------------------------------------------------------------
+// Normalized log-weights from the raw vector + device record (smc_abi.h).
+// ---------------------------------------------------------------------------
+struct NormLw {
+    double m, ls;
+    bool eq;
+    SMC_DEV double operator()(double raw) const { return eq ? -ls : (raw - m) - ls; }
+    SMC_DEV bool needs_raw() const { return !eq; }
+};
+SMC_DEV NormLw norm_of(const smc_wstate *st) { return NormLw{st->max_raw, st->log_sum, st->equal != 0}; }
+
+// ---------------------------------------------------------------------------
 // Device status: first error wins ("first failing ... reported").
 // ---------------------------------------------------------------------------
 SMC_DEV void raise_status(int32_t *status, int32_t code)

@@ -72,8 +72,8 @@ __global__ void __launch_bounds__(PB) k_pf_move(double *__restrict__ x, double *
     const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
     double v = -INFINITY;
     if (i < n) {
-        const bool eq = st->equal;
-        const double prev = eq ? -log((double)n) : lw_raw[i] - st->lse;  // normalized W_{t-1}
+        const NormLw nl = norm_of(st);
+        const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
         double x0, x1, x2, x3;
         ld_row(x + 4 * i, x0, x1, x2, x3);
         const uint64_t c = ctrs[i], si = (uint64_t)i;

@@ -96,11 +96,12 @@ struct WSrc {
     const double *lw;       // raw log weights (w == null)
     const smc_wstate *st;
     int64_t n;
-    SMC_DEV double at(int64_t i, double lse, bool eq) const
+    SMC_DEV double at(int64_t i, const NormLw &nl) const
     {
         if (w) return w[i];
-        return eq ? 1.0 / (double)n : exp(lw[i] - lse);
+        return nl.eq ? 1.0 / (double)n : exp(nl(lw[i]));
     }
+    SMC_DEV NormLw norm() const { return w ? NormLw{0.0, 0.0, false} : norm_of(st); }
 };
 
 SMC_DEV bool is_residual(int scheme)
@@ -136,8 +137,7 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
     if (gate && *gate == 0) return;
     const int64_t base = (int64_t)blockIdx.x * TILE;
     const bool residual = is_residual(scheme);
-    const bool eq = src.w ? false : src.st->equal;
-    const double lse = src.w ? 0.0 : src.st->lse;
+    const NormLw nl = src.norm();
     u128 sq = 0;
     uint64_t sqr = 0;
     int64_t sf = 0;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
     for (int j = 0; j < RI; ++j) {
         const int64_t i = base + j * RT + threadIdx.x;  // striped: coalesced
         if (i < n) {
-            Quant qq = quantize(src.at(i, lse, eq), residual, m_out, rscale, bad);
+            Quant qq = quantize(src.at(i, nl), residual, m_out, rscale, bad);
             sq += qq.q;
             sqr += qq.qr;
             sf += qq.f;
@@ -269,8 +269,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     if (!L.hdr->active || L.hdr->trivial || L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
     const bool residual = is_residual(scheme);
-    const bool eq = src.w ? false : src.st->equal;
-    const double lse = src.w ? 0.0 : src.st->lse;
+    const NormLw nl = src.norm();
     const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * RI;  // blocked
     uint64_t v[RI];
     uint64_t loc = 0;
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
         const int64_t i = base + j;
         v[j] = 0;
         if (i < n) {
-            Quant qq = quantize(src.at(i, lse, eq), residual, m_out, rscale, bad);
+            Quant qq = quantize(src.at(i, nl), residual, m_out, rscale, bad);
             v[j] = residual ? qq.qr : qq.q;
         }
         loc += v[j];
@@ -389,8 +388,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
         if (bad) raise_status(status, SMC_ECOUNTS);
     } else {
         const bool residual = is_residual(scheme);
-        const bool eq = src.w ? false : src.st->equal;
-        const double lse = src.w ? 0.0 : src.st->lse;
+        const NormLw nl = src.norm();
         uint64_t q[RI];
         int64_t f[RI];
         uint64_t loc = 0;
@@ -400,7 +398,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
             q[j] = 0;
             f[j] = 0;
             if (base + j < n) {
-                Quant qq = quantize(src.at(base + j, lse, eq), residual, m_out, rscale, bad);
+                Quant qq = quantize(src.at(base + j, nl), residual, m_out, rscale, bad);
                 q[j] = residual ? qq.qr : qq.q;
                 f[j] = qq.f;
             }

@@ -2,9 +2,10 @@
 // the ESS trigger and the monitor/path weighted sums
 // (SPEC.md:320-333, :403-416).
 //
-// Storage: lw_raw[N] plus a device smc_wstate {lse, ess, ...}.  The normalized
-// log-weight is lw_raw - lse (or -log N after set_equal_weight, which only
-// flips a flag) so normalization never needs a second write pass.
+// Storage: lw_raw[N] plus a device smc_wstate {max_raw, log_sum, ess, ...}.  The
+// normalized log-weight is (lw_raw - max_raw) - log_sum (or -log N after
+// set_equal_weight, which only flips a flag) so normalization never needs a
+// second write pass.
 #include "smc_weights.cuh"
 
 using namespace smc;
@@ -22,8 +23,10 @@ __global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restric
     double v = -INFINITY;
     if (i < n) {
         double prev = 0.0;
-        if (mode == SMC_W_ADD_LOG || mode == SMC_W_MUL_LIN)
-            prev = st->equal ? -log((double)n) : lw_raw[i] - st->lse;
+        if (mode == SMC_W_ADD_LOG || mode == SMC_W_MUL_LIN) {
+            const NormLw nl = norm_of(st);
+            prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
+        }
         const double x = values[i];
         switch (mode) {
         case SMC_W_SET_LOG: v = x; break;
@@ -65,9 +68,11 @@ __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restric
             raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
             return;
         }
-        const double lse = t.m + log(t.s1);
+        const double ls = log(t.s1);
+        const double lse = t.m + ls;
         st->lse = lse;
         st->max_raw = t.m;
+        st->log_sum = ls;
         st->ess = (t.s1 * t.s1) / t.s2;  // 1 / sum W^2 with W = e / s1
         st->ess_over_n = st->ess / (double)n;
         st->equal = 0;
@@ -89,6 +94,7 @@ __global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
     st->equal = 1;
     st->lse = log((double)n);  // consistent with lw_raw == 0 everywhere
     st->max_raw = 0.0;
+    st->log_sum = log((double)n);
     st->ess = (double)n;
     st->ess_over_n = 1.0;
 }
@@ -98,8 +104,9 @@ __global__ void k_weights_read(int what, const double *__restrict__ lw_raw, cons
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const double l = st->equal ? -log((double)n) : lw_raw[i] - st->lse;
-    out[i] = what == SMC_READ_WEIGHT ? (st->equal ? 1.0 / (double)n : exp(l)) : l;
+    const NormLw nl = norm_of(st);
+    const double l = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
+    out[i] = what == SMC_READ_WEIGHT ? (nl.eq ? 1.0 / (double)n : exp(l)) : l;
 }
 
 // SPEC.md:266 / SURVEY R8: threshold >= 1 always, <= 0 never, else ess/N < threshold.
@@ -124,10 +131,10 @@ __global__ void __launch_bounds__(RB) k_wsum_pass(const double *__restrict__ val
     double acc[RMAX];
 #pragma unroll
     for (int j = 0; j < RMAX; ++j) acc[j] = 0.0;
-    const bool eq = st->equal;
-    const double lse = st->lse, inv_n = 1.0 / (double)n;
+    const NormLw nl = norm_of(st);
+    const double inv_n = 1.0 / (double)n;
     for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        const double w = eq ? inv_n : exp(lw_raw[i] - lse);
+        const double w = nl.eq ? inv_n : exp(nl(lw_raw[i]));
 #pragma unroll
         for (int j = 0; j < RMAX; ++j)
             if (j < mc) acc[j] += w * vals[i * ld + m0 + j];
