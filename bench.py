@@ -286,7 +286,7 @@ def run_e2e(P, s, obs, steps):
         t = s.iteration + 1
         dev_obs[t].copy_(host_obs[t], non_blocking=True)  # H2D: this step's observation (16 B)
         s.iterate(1, check=False)
-        host_row.copy_(s._hist[t], non_blocking=True)   # D2H: this step's history record
+        host_row.copy_(s.history_row(t), non_blocking=True)  # D2H: this step's history record
         torch.cuda.current_stream().synchronize()
     sec = time.perf_counter() - t0
     s.check()

@@ -158,6 +158,12 @@ int smc_resample(int scheme, const double *w, const double *lw_raw, const smc_ws
                  int64_t n_u, int32_t *counts, int32_t *parents, void *rows, int64_t row_bytes,
                  const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes, void *stream);
 
+/* Test hook: SMC_DEBUG_FORCE_EXACT_F = 1 makes the stratified/systematic count
+ * kernel always take its exact 128-bit path instead of the fp64 fast path
+ * with guard band (the two are bit-identical by construction; tests check). */
+#define SMC_DEBUG_FORCE_EXACT_F 1
+int smc_debug_set(int key, int value);
+
 /* replication_to_parents(counts) from a device counts vector. */
 int smc_replication_to_parents(const int32_t *counts, int64_t n, int32_t *parents, int32_t *status, void *ws,
                                size_t ws_bytes, void *stream);
@@ -185,7 +191,12 @@ int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *c
  * one pass over the state; log_zconst += log sum W_{t-1} exp(incw).
  * incw_out may be NULL. */
 int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                smc_wstate *ws_state, double *incw_out, void *ws, size_t ws_bytes, void *stream);
+                smc_wstate *ws_state, double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes,
+                void *stream);
+/* monitor_prev (device, 2 doubles, may be NULL): receives the "pos" monitor
+ * sum_i W_i (x_i, y_i) of the state the move CONSUMES -- the previous
+ * iteration's estimate -- reduced from registers the move
+ * already holds, so the monitor costs no extra pass over the state. */
 
 #ifdef __cplusplus
 }

@@ -70,12 +70,13 @@ _SIGS = {
     "smc_resample_workspace_bytes": ([_i64], _sz),
     "smc_resample": ([_i32, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                       _vp, _vp, _sz, _vp], C.c_int),
+    "smc_debug_set": ([C.c_int, C.c_int], C.c_int),
     "smc_replication_to_parents": ([_vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gather_rows": ([_vp, _vp, _i64, _vp, _i64, _vp], C.c_int),
     "smc_copy_rows_inplace": ([_vp, _i64, _vp, _i64, _vp, _vp], C.c_int),
     "smc_pf_workspace_bytes": ([_i64], _sz),
     "smc_pf_init": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
-    "smc_pf_move": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_pf_move": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -133,9 +133,15 @@ class ParticleSystem:
         self.threshold = float(threshold)
         self.parents = torch.arange(self.size, dtype=torch.int32, device=self.device)
         self.resampler = Resampler(self.size, self.device)
+        self.pending_monitors = {}  # name -> device address a fused move kernel writes into
 
     def rng(self, i):
         return self.rng_set.stream(i)
+
+    def take_pending_monitor(self, name):
+        """Device address for a monitor the calling move kernel reduces in passing (or None)."""
+        p = self.pending_monitors.pop(name, None)
+        return None if p is None else ctypes.c_void_p(p[0])
 
 
 class SingleParticleView:
@@ -277,6 +283,8 @@ class Sampler:
 
     def _row(self, t):
         if self._hist is None or t >= self._hist.shape[0]:
+            if self._hist is not None:
+                self.flush()  # pending monitor addresses point into the old buffer
             cap = max(128, 2 * (t + 1))
             h = torch.zeros((cap, len(self._cols)), dtype=torch.float64, device=self.device)
             if self._hist is not None:
@@ -290,6 +298,7 @@ class Sampler:
         if self.init_op is None:
             raise RuntimeError("initialize: no init operation set")
         self._layout()
+        self.system.pending_monitors.clear()
         self._hist = None
         self._rows = 0
         self._path_grid = []
@@ -350,9 +359,25 @@ class Sampler:
             row[self._col["path.grid"]].fill_(alpha)
             self._reduce(integrand, 1, 1, row, self._col["path.integrand"])
         for name, rec in self.monitors.items():
+            col = self._col[f"{name}.0"]
+            fw = getattr(rec.eval, "fused_with", None)
+            if fw and self.move_queue and self.move_queue[0].name == fw:
+                # deferred: the next move reduces it from the state it loads (no extra pass);
+                # flush() evaluates it here instead if the history is read first
+                sysm.pending_monitors[name] = (row.data_ptr() + 8 * col, t)
+                continue
             vals, ld = apply_monitor_eval(rec.eval, sysm, t, rec.dim)
-            self._reduce(vals, ld, rec.dim, row, self._col[f"{name}.0"])
+            self._reduce(vals, ld, rec.dim, row, col)
         self._mark("monitor", 1)
+
+    def flush(self):
+        """Evaluate deferred monitors now (state and weights are unchanged since their step)."""
+        sysm = self.system
+        for name, (addr, t) in list(sysm.pending_monitors.items()):
+            rec = self.monitors[name]
+            vals, ld = apply_monitor_eval(rec.eval, sysm, t, rec.dim)
+            self._reduce(vals, ld, rec.dim, self._hist[t], self._col[f"{name}.0"])
+            del sysm.pending_monitors[name]
 
     # Optional per-phase CUDA events (bench.py's live per-kernel timing):
     # set ``sampler.timing = {}``; each phase gets a list of (start, end) events.
@@ -383,6 +408,7 @@ class Sampler:
 
     # -- results ---------------------------------------
     def history(self):
+        self.flush()
         h = self._hist[: self._rows].cpu().numpy()
         d = {"iter": np.arange(self._rows)}
         for c, k in self._col.items():
@@ -390,9 +416,16 @@ class Sampler:
         return d
 
     def history_array(self):
+        self.flush()
         return self._hist[: self._rows].cpu().numpy()
 
+    def history_row(self, t):
+        """Device view of row t (after flushing deferred monitors)."""
+        self.flush()
+        return self._hist[t]
+
     def monitor_estimate(self, name, t):
+        self.flush()
         rec = self.monitors[name]
         if not 0 <= t < self._rows:
             raise IndexError("iteration not recorded")

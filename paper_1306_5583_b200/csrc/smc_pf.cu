@@ -64,18 +64,28 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
     if (threadIdx.x == 0) parts[blockIdx.x] = p;
 }
 
-__global__ void __launch_bounds__(PB) k_pf_move(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
-                                                Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
-                                                PfConst k, smc_wstate *st, double *__restrict__ incw_out,
-                                                LsePartial *__restrict__ parts)
+// MON: also reduce the "pos" monitor of the INCOMING state, sum_i W_{t-1,i} (x_i, y_i) -- the
+// previous iteration's estimate (evaluated after its resample) --
+// from the registers the move already holds: the monitor costs no extra HBM pass.
+template <bool MON>
+__global__ void __launch_bounds__(PB, 4) k_pf_move(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
+                                                   Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                   PfConst k, smc_wstate *st, double *__restrict__ incw_out,
+                                                   LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
     const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
     double v = -INFINITY;
+    double h0 = 0.0, h1 = 0.0;
     if (i < n) {
         const NormLw nl = norm_of(st);
         const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
         double x0, x1, x2, x3;
         ld_row(x + 4 * i, x0, x1, x2, x3);
+        if (MON) {
+            const double w = nl.eq ? 1.0 / (double)n : exp(prev);
+            h0 = w * x0;
+            h1 = w * x1;
+        }
         const uint64_t c = ctrs[i], si = (uint64_t)i;
         // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
         x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
@@ -92,6 +102,18 @@ __global__ void __launch_bounds__(PB) k_pf_move(double *__restrict__ x, double *
     }
     LsePartial p = block_lse_partial<PB>(v);
     if (threadIdx.x == 0) parts[blockIdx.x] = p;
+    if (MON) {
+        __shared__ double s_h[2][PB / 32];
+        h0 = warp_sum(h0);
+        h1 = warp_sum(h1);
+        if ((threadIdx.x & 31) == 0) { s_h[0][threadIdx.x >> 5] = h0; s_h[1][threadIdx.x >> 5] = h1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0.0, b = 0.0;
+            for (int w = 0; w < PB / 32; ++w) { a += s_h[0][w]; b += s_h[1][w]; }
+            mon_parts[blockIdx.x] = make_double2(a, b);
+        }
+    }
 }
 
 PfConst pf_constants()
@@ -109,7 +131,7 @@ PfConst pf_constants()
 
 extern "C" size_t smc_pf_workspace_bytes(int64_t n)
 {
-    return (size_t)((n + PB - 1) / PB + 1) * sizeof(LsePartial);
+    return (size_t)((n + PB - 1) / PB + 1) * (sizeof(LsePartial) + sizeof(double2)) + 256;
 }
 
 static int pf_check(double *x, double *lw_raw, int64_t n, uint64_t *ctrs, const double *obs, smc_wstate *st,
@@ -137,15 +159,23 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, 
 }
 
 extern "C" int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                           smc_wstate *st, double *incw_out, void *ws, size_t ws_bytes, void *stream)
+                           smc_wstate *st, double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes,
+                           void *stream)
 {
     int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_move");
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
-    k_pf_move<<<nb, PB, 0, s>>>(x, lw_raw, n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
-                                pf_constants(), st, incw_out, parts);
-    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s);
+    double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
+    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    if (monitor_prev) {
+        k_pf_move<true><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts, mon);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, mon, monitor_prev);
+    } else {
+        k_pf_move<false><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts,
+                                           nullptr);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s);
+    }
     return smc_check_launch("smc_pf_move");
 }

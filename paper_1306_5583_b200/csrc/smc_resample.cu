@@ -10,21 +10,23 @@
 //   residual: f_i = floor(fl(M W_i)); the R = M - sum f leftovers over
 //   q'_i = floor((fl(M W_i) - f_i) 2^(63 - ceil log2 N)).
 //
-// Kernels (one resample = 4 launches for stratified/systematic):
-//   A  k_rs_tiles      : per-tile sums of q (u128), f and q'; validation.
-//   S  k_rs_scan       : one block: T, R, window check, tile prefixes, stream
-//                        counter advance (on device: no host sync).
-//   [M k_rs_prefix + k_rs_multinomial : multinomial/residual histogram]
-//   B  k_rs_counts     : per tile, local scan + tile prefix -> Q; counts in O(1)
-//                        per particle via F(X) = #{k : P_k < X}; then a
-//                        DECOUPLED-LOOKBACK scan of (zero slots, surplus
-//                        children, surplus parents) to emit the survivor part
-//                        of the parent map, the compacted zero-slot list and the
-//                        compacted surplus-parent list.
-//   C  k_rs_assign     : per tile of zero-slot ranks: merge-path search of the
-//                        rank range against the surplus-parent prefix (staged in
-//                        shared memory), parent map for zero slots, and the
-//                        in-place row copy (256-bit LDG/STG per 32-byte row).
+// Kernels (one stratified/systematic resample = 4 launches):
+//   A  k_rs_tiles   : per-tile u128 sums of q, sums of f and q'; validation.
+//   S  k_rs_scan    : one block: T, R, window check, tile prefixes, the stream
+//                     counter advance (on device: no host sync).
+//  [M  k_rs_prefix + k_rs_multinomial: multinomial/residual histogram]
+//   B  k_rs_counts  : per tile (coalesced loads staged through shared memory),
+//                     local scan + tile prefix -> Q; counts in O(1) per particle
+//                     via F(X) = #{k : P_k < X} (fp64 with a guard band, exact
+//                     128-bit fallback inside it); then a DECOUPLED-LOOKBACK scan
+//                     of (zero slots, surplus children, surplus parents) that
+//                     emits the survivor half of the parent map, the compacted
+//                     zero-slot list and the compacted surplus-parent list.
+//   C  k_rs_assign  : per tile of zero-slot ranks: the tile's slice of the
+//                     surplus-parent prefix staged in shared memory (merge-path
+//                     boundaries by binary search), a linear merge walk per
+//                     thread, the parent map for zero slots, and the in-place
+//                     row copy (256-bit LDG/STG per 32-byte row, 8 in flight).
 #include "smc_weights.cuh"
 
 using namespace smc;
@@ -36,6 +38,10 @@ constexpr int RI = 8;
 constexpr int TILE = RT * RI;  // elements per tile (pass A/B) and ranks per tile (pass C)
 constexpr uint64_t T_LO = (1ull << 63) - (1ull << 43);
 constexpr uint64_t T_HI = (1ull << 63) + (1ull << 43);
+constexpr double TWO53 = 9007199254740992.0;
+constexpr double INV53 = 1.0 / 9007199254740992.0;
+
+__device__ int g_force_exact = 0;  // test hook: always take the exact 128-bit F path
 
 struct RsHeader {
     uint64_t T;       // sum of q
@@ -43,6 +49,8 @@ struct RsHeader {
     uint64_t M;       // positions (strata / draws)
     uint64_t c0;      // first counter of the resampling stream for this call
     uint64_t m_sys;   // the single systematic uniform (53-bit integer)
+    double ratio;     // fl(M / Tm) for the fast F path
+    double guard;     // guard band of the fast F path
     int64_t draws;
     int32_t active;   // 0 => gated off or failed; later kernels exit
     int32_t trivial;  // N == 1
@@ -81,8 +89,8 @@ Layout layout(void *ws, int64_t n)
     L.lb_status = (uint32_t *)take(sizeof(uint32_t) * nt);
     L.lb_agg = (uint4 *)take(sizeof(uint4) * nt);
     L.lb_incl = (uint4 *)take(sizeof(uint4) * nt);
-    L.zpos = (int32_t *)take(sizeof(int32_t) * n);
-    L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));    // P <= n even for invalid counts
+    L.zpos = (int32_t *)take(sizeof(int32_t) * (n + 8));
+    L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));  // P <= n even for invalid counts
     L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
@@ -92,16 +100,21 @@ Layout layout(void *ws, int64_t n)
 
 // Everything a per-particle kernel needs to turn an index into W_i.
 struct WSrc {
-    const double *w;        // normalized weights, or null
-    const double *lw;       // raw log weights (w == null)
+    const double *w;   // normalized weights, or null
+    const double *lw;  // raw log weights (w == null)
     const smc_wstate *st;
     int64_t n;
-    SMC_DEV double at(int64_t i, const NormLw &nl) const
-    {
-        if (w) return w[i];
-        return nl.eq ? 1.0 / (double)n : exp(nl(lw[i]));
-    }
     SMC_DEV NormLw norm() const { return w ? NormLw{0.0, 0.0, false} : norm_of(st); }
+    SMC_DEV double raw(int64_t i, const NormLw &nl) const  // the load (coalescable)
+    {
+        if (w) return __ldg(w + i);
+        return nl.eq ? 0.0 : __ldg(lw + i);
+    }
+    SMC_DEV double weight(double r, const NormLw &nl) const  // the math
+    {
+        if (w) return r;
+        return nl.eq ? 1.0 / (double)n : exp(nl(r));
+    }
 };
 
 SMC_DEV bool is_residual(int scheme)
@@ -109,6 +122,7 @@ SMC_DEV bool is_residual(int scheme)
     return scheme == SMC_RESIDUAL || scheme == SMC_RESIDUAL_STRATIFIED || scheme == SMC_RESIDUAL_SYSTEMATIC;
 }
 SMC_DEV bool is_multinomial(int scheme) { return scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL; }
+SMC_DEV bool is_systematic(int scheme) { return scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC; }
 
 // q, f, q' for one weight (A.1, A.4).  Validation sets `bad`.
 struct Quant {
@@ -138,25 +152,32 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
     const int64_t base = (int64_t)blockIdx.x * TILE;
     const bool residual = is_residual(scheme);
     const NormLw nl = src.norm();
+    double r[RI];
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {  // striped: each warp load is 256 contiguous bytes; all issued up front
+        const int64_t i = base + j * RT + threadIdx.x;
+        r[j] = i < n ? src.raw(i, nl) : 0.0;
+    }
     u128 sq = 0;
     uint64_t sqr = 0;
     int64_t sf = 0;
     bool bad = false;
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
-        const int64_t i = base + j * RT + threadIdx.x;  // striped: coalesced
+        const int64_t i = base + j * RT + threadIdx.x;
         if (i < n) {
-            Quant qq = quantize(src.at(i, nl), residual, m_out, rscale, bad);
+            const Quant qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
             sq += qq.q;
             sqr += qq.qr;
             sf += qq.f;
             if (is_multinomial(scheme)) L.cnt[i] = 0;
         }
     }
-    // explicit uniforms must lie in [0, 1)
+    bool badu = false;  // explicit uniforms must lie in [0, 1)
     for (int64_t k = (int64_t)blockIdx.x * RT + threadIdx.x; u && k < n_u; k += (int64_t)gridDim.x * RT)
-        if (!(u[k] >= 0.0 && u[k] < 1.0)) bad = true;
+        if (!(u[k] >= 0.0 && u[k] < 1.0)) badu = true;
     if (__syncthreads_or(bad) && threadIdx.x == 0) raise_status(status, SMC_EUNNORMALIZED);
+    if (__syncthreads_or(badu) && threadIdx.x == 0) raise_status(status, SMC_EINVAL);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sq += shfl_xor_u128(sq, o);
@@ -189,6 +210,9 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
                                                 int64_t n_u, const int32_t *gate, int32_t *status, Layout L)
 {
     __shared__ uint64_t sm64[SB / 32 + 1];
+    __shared__ u128 s_q[SB / 32];
+    __shared__ uint64_t s_qr[SB / 32];
+    __shared__ int64_t s_f[SB / 32];
     __shared__ int s_ok;
     RsHeader *h = L.hdr;
     if (gate && *gate == 0) {
@@ -196,26 +220,28 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         return;
     }
     const bool residual = is_residual(scheme);
-    // chunked totals (each thread a contiguous chunk -> deterministic)
+    // each thread a contiguous chunk of tiles (deterministic), then a shuffle tree
     const int64_t per = (nt + SB - 1) / SB;
-    const int64_t b0 = threadIdx.x * per, b1 = b0 + per < nt ? b0 + per : nt;
+    const int64_t b0 = threadIdx.x * per < nt ? threadIdx.x * per : nt;
+    const int64_t b1 = b0 + per < nt ? b0 + per : nt;
     u128 tq = 0;
     uint64_t tqr = 0;
     int64_t tf = 0;
     for (int64_t b = b0; b < b1; ++b) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
-    // block sums (u128 by halves through shared memory, serial in thread 0)
-    __shared__ u128 s_tq[SB];
-    __shared__ uint64_t s_tqr[SB];
-    __shared__ int64_t s_tf[SB];
-    s_tq[threadIdx.x] = tq;
-    s_tqr[threadIdx.x] = tqr;
-    s_tf[threadIdx.x] = tf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tq += shfl_xor_u128(tq, o);
+        tqr += __shfl_xor_sync(0xffffffffu, tqr, o);
+        tf += __shfl_xor_sync(0xffffffffu, tf, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_q[warp] = tq; s_qr[warp] = tqr; s_f[warp] = tf; }
     __syncthreads();
     if (threadIdx.x == 0) {
         u128 T = 0;
         uint64_t Tr = 0;
         int64_t F = 0;
-        for (int t = 0; t < SB; ++t) { T += s_tq[t]; Tr += s_tqr[t]; F += s_tf[t]; }
+        for (int w = 0; w < SB / 32; ++w) { T += s_q[w]; Tr += s_qr[w]; F += s_f[w]; }
         int ok = (status == nullptr || *status == 0);
         if (T < (u128)T_LO || T > (u128)T_HI) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
         int64_t M = (int64_t)m_out;
@@ -227,12 +253,14 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
             Tm = Tr;
         }
         int64_t draws = 0;
-        if (n > 1 && M > 0)
-            draws = (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC) ? 1 : M;
+        if (n > 1 && M > 0) draws = is_systematic(scheme) ? 1 : M;
         if (ok && u && n_u < draws) { raise_status(status, SMC_EUNIFORMS); ok = 0; }
         h->T = (uint64_t)T;
         h->Tm = Tm;
-        h->M = (uint64_t)M;
+        h->M = (uint64_t)(M > 0 ? M : 0);
+        h->ratio = Tm ? (double)(M > 0 ? M : 0) / (double)Tm : 0.0;
+        // |fl(X) fl(M/Tm) - X M/Tm| <= 3.4e-16 * M; flag anything within 2^-47 M of a decision boundary
+        h->guard = (double)(M > 0 ? M : 1) * 7.105427357601002e-15;
         h->draws = draws;
         h->trivial = (n == 1);
         h->tile_ctr = 0;
@@ -241,23 +269,22 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
             const uint64_t c0 = u ? 0 : *ctr;
             h->c0 = c0;
             if (!u) *ctr = c0 + (uint64_t)draws;
-            if (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC)
-                h->m_sys = draws ? (u ? (uint64_t)(u[0] * 9007199254740992.0) : draw53(c0, stream, key)) : 0;
+            if (is_systematic(scheme))
+                h->m_sys = draws ? (u ? (uint64_t)(u[0] * TWO53) : draw53(c0, stream, key)) : 0;
         }
         h->active = ok;
         s_ok = ok;
     }
     __syncthreads();
     if (!s_ok) return;
-    // exclusive prefix of the searched per-tile totals
-    const uint64_t *src = residual ? L.tile_qr : nullptr;
+    // exclusive prefix of the searched per-tile totals (all < 2^64 once T is validated)
     uint64_t mine = 0;
-    for (int64_t b = b0; b < b1; ++b) mine += src ? src[b] : (uint64_t)L.tile_q[b];
+    for (int64_t b = b0; b < b1; ++b) mine += residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b];
     uint64_t tot;
     uint64_t run = block_exclusive_sum<SB, uint64_t>(mine, sm64, &tot);
     for (int64_t b = b0; b < b1; ++b) {
         L.tile_pre[b] = run;
-        run += src ? src[b] : (uint64_t)L.tile_q[b];
+        run += residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b];
     }
 }
 
@@ -279,7 +306,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
         const int64_t i = base + j;
         v[j] = 0;
         if (i < n) {
-            Quant qq = quantize(src.at(i, nl), residual, m_out, rscale, bad);
+            const Quant qq = quantize(src.weight(src.raw(i, nl), nl), residual, m_out, rscale, bad);
             v[j] = residual ? qq.qr : qq.q;
         }
         loc += v[j];
@@ -301,7 +328,7 @@ __global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const doub
     if (!h->active || h->trivial) return;
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M; k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t m = u ? (uint64_t)(u[k] * 9007199254740992.0) : draw53(c0 + k, stream, key);
+        const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c0 + k, stream, key);
         const uint64_t P = (uint64_t)(((u128)m * Tm) >> 53);
         int64_t lo = 0, hi = n - 1;  // P < Tm = Q_{n-1} so the answer exists
         while (lo < hi) {
@@ -315,6 +342,7 @@ __global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const doub
 // ------------------------------------------------------------------ pass B --
 struct StratCtx {
     uint64_t Tm, M, m_sys, c0, stream;
+    double ratio, guard;
     const double *u;
     Key key;
     bool systematic;
@@ -323,24 +351,41 @@ struct StratCtx {
 SMC_DEV uint64_t m_of(const StratCtx &c, uint64_t s)
 {
     if (c.systematic) return c.m_sys;
-    if (c.u) return (uint64_t)(c.u[s] * 9007199254740992.0);
+    if (c.u) return (uint64_t)(c.u[s] * TWO53);
     return draw53(c.c0 + s, c.stream, c.key);
 }
 
-// F(X) = #{k < M : P_k < X},  P_k = floor((k 2^53 + m_k) Tm / (M 2^53)).
+// Exact F(X) = #{k < M : P_k < X},  P_k = floor((k 2^53 + m_k) Tm / (M 2^53)):
 // k < s := floor(X M / Tm) all qualify, k > s none; k = s iff m_s Tm < (X M - s Tm) 2^53.
-SMC_DEV uint64_t F_strat(const StratCtx &c, uint64_t X)
+SMC_DEV uint64_t F_exact(const StratCtx &c, uint64_t X)
 {
     if (X >= c.Tm) return c.M;
     if (X == 0) return 0;
     const u128 XM = (u128)X * c.M;
-    double est = (double)X * (double)c.M / (double)c.Tm;
-    uint64_t s = (uint64_t)est;
+    uint64_t s = (uint64_t)((double)X * c.ratio);
     while ((u128)s * c.Tm > XM) --s;
     while ((u128)(s + 1) * c.Tm <= XM) ++s;
     const u128 rem = XM - (u128)s * c.Tm;
     const uint64_t m = m_of(c, s);
     return s + (((u128)m * c.Tm < (rem << 53)) ? 1 : 0);
+}
+
+// Same value in ~10 instructions: z = X M / Tm in fp64 (|error| <= 3.4e-16 M);
+// F = floor(z) + [u_s < frac(z)].  Whenever frac(z) or frac(z) - u_s lies
+// inside the guard band the exact path decides, so the result is bit-identical.
+SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
+{
+    if (X >= c.Tm) return c.M;
+    if (X == 0) return 0;
+    const double z = (double)X * c.ratio;
+    const double fl = floor(z);
+    const double fr = z - fl;
+    if (g_force_exact || fr < c.guard || fr > 1.0 - c.guard) return F_exact(c, X);
+    const uint64_t s = (uint64_t)fl;
+    const double us = (double)m_of(c, s) * INV53;
+    const double d = fr - us;
+    if (d < c.guard && d > -c.guard) return F_exact(c, X);
+    return s + (d > 0.0 ? 1 : 0);
 }
 
 // pack (zero slots, surplus parents) in the top, surplus children in the low
@@ -351,6 +396,9 @@ SMC_DEV uint32_t unp(uint64_t v) { return (uint32_t)((v >> 40) & 0xFFF); }
 SMC_DEV uint64_t uns(uint64_t v) { return v & ((1ull << 40) - 1); }
 
 SMC_DEV uint32_t ld_status(const uint32_t *p) { return *(volatile const uint32_t *)p; }
+
+// blocked smem index with one pad word per 16: conflict-free for 64-bit reads of t*8+j
+SMC_DEV int pad16(int i) { return i + (i >> 4); }
 
 // mode: 0 = counts from weights (sampler path), 1 = counts given (replication_to_parents)
 __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src, const int32_t *__restrict__ cin,
@@ -364,6 +412,8 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
     __shared__ uint64_t sm[RT / 32 + 1];
     __shared__ uint32_t s_tile;
     __shared__ uint4 s_excl;
+    __shared__ uint64_t s_q[TILE + TILE / 16];
+    __shared__ int32_t s_fb[TILE + TILE / 16];
     if (h->trivial) {  // N == 1: no-op resample
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             if (counts) counts[0] = (int32_t)m_out;
@@ -376,7 +426,8 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
     if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
     __syncthreads();
     const int64_t b = s_tile;
-    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
+    const int64_t tbase = b * TILE;
+    const int64_t base = tbase + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
     int32_t c[RI];
     if (mode == 1) {
         bool bad = false;
@@ -389,24 +440,36 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
     } else {
         const bool residual = is_residual(scheme);
         const NormLw nl = src.norm();
-        uint64_t q[RI];
-        int64_t f[RI];
-        uint64_t loc = 0;
+        // stage: coalesced striped loads -> q (and f) -> shared memory -> blocked per thread
+        double r[RI];
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            const int64_t i = tbase + j * RT + threadIdx.x;
+            r[j] = i < n ? src.raw(i, nl) : 0.0;
+        }
         bool bad = false;
 #pragma unroll
         for (int j = 0; j < RI; ++j) {
-            q[j] = 0;
-            f[j] = 0;
-            if (base + j < n) {
-                Quant qq = quantize(src.at(base + j, nl), residual, m_out, rscale, bad);
-                q[j] = residual ? qq.qr : qq.q;
-                f[j] = qq.f;
-            }
+            const int li = j * RT + threadIdx.x;
+            const int64_t i = tbase + li;
+            Quant qq{0, 0, 0};
+            if (i < n) qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
+            s_q[pad16(li)] = residual ? qq.qr : qq.q;
+            s_fb[pad16(li)] = (int32_t)qq.f;
+        }
+        __syncthreads();
+        uint64_t q[RI];
+        int32_t f[RI];
+        uint64_t loc = 0;
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            q[j] = s_q[pad16(threadIdx.x * RI + j)];
+            f[j] = s_fb[pad16(threadIdx.x * RI + j)];
             loc += q[j];
         }
         if (is_multinomial(scheme)) {
 #pragma unroll
-            for (int j = 0; j < RI; ++j) c[j] = base + j < n ? (int32_t)f[j] + L.cnt[base + j] : 1;
+            for (int j = 0; j < RI; ++j) c[j] = base + j < n ? f[j] + L.cnt[base + j] : 1;
         } else {
             uint64_t tot;
             uint64_t X = L.tile_pre[b] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
@@ -415,17 +478,19 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
             sc.M = h->M;
             sc.m_sys = h->m_sys;
             sc.c0 = h->c0;
+            sc.ratio = h->ratio;
+            sc.guard = h->guard;
             sc.stream = stream;
             sc.u = u;
             sc.key = key;
-            sc.systematic = (scheme == SMC_SYSTEMATIC || scheme == SMC_RESIDUAL_SYSTEMATIC);
-            uint64_t Fp = (base < n && sc.M) ? F_strat(sc, X) : 0;
+            sc.systematic = is_systematic(scheme);
+            uint64_t Fp = (base < n && sc.M) ? F_fast(sc, X) : 0;
 #pragma unroll
             for (int j = 0; j < RI; ++j) {
                 if (base + j < n) {
                     uint64_t Fc = Fp;
-                    if (q[j] && sc.M) { X += q[j]; Fc = F_strat(sc, X); }
-                    c[j] = (int32_t)(f[j] + (int64_t)(Fc - Fp));
+                    if (q[j] && sc.M) { X += q[j]; Fc = F_fast(sc, X); }
+                    c[j] = f[j] + (int32_t)(Fc - Fp);
                     Fp = Fc;
                 } else {
                     c[j] = 1;  // padding: neither zero slot nor surplus
@@ -434,9 +499,14 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
         }
     }
     if (counts) {
+        if (base + RI <= n) {
+            reinterpret_cast<int4 *>(counts + base)[0] = make_int4(c[0], c[1], c[2], c[3]);
+            reinterpret_cast<int4 *>(counts + base)[1] = make_int4(c[4], c[5], c[6], c[7]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < RI; ++j)
-            if (base + j < n) counts[base + j] = c[j];
+            for (int j = 0; j < RI; ++j)
+                if (base + j < n) counts[base + j] = c[j];
+        }
     }
     if (!parents) return;
     // ---- parent map: decoupled lookback over (Z, S, P) ----
@@ -526,14 +596,21 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
 }
 
 // ------------------------------------------------------------------ pass C --
+SMC_DEV void ld256(const double *p, double4 &v)
+{
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+}
+SMC_DEV void st256(double *p, const double4 &v)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+}
+
 SMC_DEV void copy_row(char *rows, int64_t row_bytes, int64_t dst, int64_t srcr)
 {
     if (row_bytes == 32) {
-        const double *s = (const double *)(rows + srcr * 32);
-        double *d = (double *)(rows + dst * 32);
-        double a, b2, c2, d2;
-        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b2), "=d"(c2), "=d"(d2) : "l"(s));
-        asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(d), "d"(a), "d"(b2), "d"(c2), "d"(d2) : "memory");
+        double4 v;
+        ld256((const double *)(rows + srcr * 32), v);
+        st256((double *)(rows + dst * 32), v);
     } else if ((row_bytes & 15) == 0) {
         const int4 *s = (const int4 *)(rows + srcr * row_bytes);
         int4 *d = (int4 *)(rows + dst * row_bytes);
@@ -577,16 +654,48 @@ __global__ void __launch_bounds__(RT) k_rs_assign(int32_t *__restrict__ parents,
         s_idx[k] = __ldcg(&L.sp_idx[plo + k]);
     }
     __syncthreads();
-    for (uint32_t r = r0 + threadIdx.x; r < r1; r += RT) {  // striped ranks
-        uint32_t lo = 0, hi = cnt;  // last k with s_start[k] <= r
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((uint32_t)s_start[mid] <= r) lo = mid; else hi = mid;
+    // blocked ranks: thread owns RI consecutive ranks; one binary search, then a merge walk
+    const uint32_t ra = r0 + threadIdx.x * RI;
+    if (ra >= r1) return;
+    uint32_t lo = 0, hi = cnt;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((uint32_t)s_start[mid] <= ra) lo = mid; else hi = mid;
+    }
+    int32_t dst[RI], par[RI];
+    const int nr = (int)(r1 - ra < (uint32_t)RI ? r1 - ra : RI);
+    if (nr == RI) {
+        const int4 z0 = __ldcg(reinterpret_cast<const int4 *>(L.zpos + ra));
+        const int4 z1 = __ldcg(reinterpret_cast<const int4 *>(L.zpos + ra) + 1);
+        dst[0] = z0.x; dst[1] = z0.y; dst[2] = z0.z; dst[3] = z0.w;
+        dst[4] = z1.x; dst[5] = z1.y; dst[6] = z1.z; dst[7] = z1.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < RI; ++j) dst[j] = j < nr ? __ldcg(L.zpos + ra + j) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        const uint32_t r = ra + j;
+        while (lo + 1 < cnt && (uint32_t)s_start[lo + 1] <= r) ++lo;
+        par[j] = s_idx[lo];
+    }
+    if (parents) {
+#pragma unroll
+        for (int j = 0; j < RI; ++j)
+            if (j < nr) parents[dst[j]] = par[j];
+    }
+    if (rows) {
+        if (row_bytes == 32) {
+            double4 v[RI];
+#pragma unroll
+            for (int j = 0; j < RI; ++j)
+                if (j < nr) ld256((const double *)(rows + (int64_t)par[j] * 32), v[j]);  // 8 loads in flight
+#pragma unroll
+            for (int j = 0; j < RI; ++j)
+                if (j < nr) st256((double *)(rows + (int64_t)dst[j] * 32), v[j]);
+        } else {
+            for (int j = 0; j < nr; ++j) copy_row(rows, row_bytes, dst[j], par[j]);
         }
-        const int32_t par = s_idx[lo];
-        const int32_t j = __ldcg(&L.zpos[r]);
-        if (parents) parents[j] = par;
-        if (rows) copy_row(rows, row_bytes, j, par);
     }
 }
 
@@ -655,6 +764,8 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         return smc_set_error(SMC_EINVAL, "smc_resample: row_bytes must be a positive multiple of 8");
     if (rows && row_bytes == 32 && ((uintptr_t)rows & 31))
         return smc_set_error(SMC_EINVAL, "smc_resample: 32-byte rows must be 32-byte aligned");
+    if (counts && ((uintptr_t)counts & 15))
+        return smc_set_error(SMC_EINVAL, "smc_resample: counts must be 16-byte aligned");
     if (!ws || ws_bytes < smc_resample_workspace_bytes(n))
         return smc_set_error(SMC_EWORKSPACE, "smc_resample: workspace too small");
     const int64_t nt = (n + TILE - 1) / TILE;
@@ -716,4 +827,11 @@ extern "C" int smc_gather_rows(void *dst, const void *src, int64_t row_bytes, co
     k_gather<<<grid_cap((n * (row_bytes / 8) + RT - 1) / RT), RT, 0, (cudaStream_t)stream>>>(
         (char *)dst, (const char *)src, row_bytes, parents, n);
     return smc_check_launch("smc_gather_rows");
+}
+
+extern "C" int smc_debug_set(int key, int value)
+{
+    if (key != SMC_DEBUG_FORCE_EXACT_F) return smc_set_error(SMC_EINVAL, "smc_debug_set: unknown key %d", key);
+    cudaError_t e = cudaMemcpyToSymbol(g_force_exact, &value, sizeof(int));
+    return e == cudaSuccess ? SMC_OK : smc_set_error(SMC_ECUDA, "smc_debug_set: %s", cudaGetErrorString(e));
 }

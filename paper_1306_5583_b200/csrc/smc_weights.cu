@@ -46,24 +46,53 @@ __global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restric
 
 constexpr int FB = 1024;
 
+// Two phases so every exp is independent (no dependent online-rescale chain):
+// M = max_b m_b, then s1 = sum_b s1_b e^{m_b - M}, s2 = sum_b s2_b e^{2(m_b - M)}.
+// Optional monitor partials (mon_parts[b] = sum_i W_i h(X_i) over block b) are
+// summed in the same fixed order into mon_out[0..1].
 __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ parts, int nparts,
-                                                      smc_wstate *st, int64_t n, int mode, int accumulate_nc)
+                                                      smc_wstate *st, int64_t n, int mode, int accumulate_nc,
+                                                      const double2 *__restrict__ mon_parts, double *mon_out)
 {
-    __shared__ LsePartial sm[FB / 32];
-    LsePartial acc{-INFINITY, 0.0, 0.0};
-    for (int b = threadIdx.x; b < nparts; b += FB) acc = lse_combine(acc, parts[b]);
-    // fixed-shape tree: xor shuffles, then warp partials in index order
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        LsePartial o_{__shfl_xor_sync(0xffffffffu, acc.m, o), __shfl_xor_sync(0xffffffffu, acc.s1, o),
-                      __shfl_xor_sync(0xffffffffu, acc.s2, o)};
-        acc = lse_combine(acc, o_);
-    }
-    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+    __shared__ double sm_a[FB / 32], sm_b[FB / 32], sm_c[FB / 32], sm_d[FB / 32];
+    __shared__ double s_M;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double m = -INFINITY;
+    for (int b = threadIdx.x; b < nparts; b += FB) m = fmax(m, parts[b].m);
+    m = warp_max(m);
+    if (lane == 0) sm_a[warp] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
-        LsePartial t = sm[0];
-        for (int w = 1; w < FB / 32; ++w) t = lse_combine(t, sm[w]);
+        double M = sm_a[0];
+        for (int w = 1; w < FB / 32; ++w) M = fmax(M, sm_a[w]);
+        s_M = M;
+    }
+    __syncthreads();
+    const double M = s_M;
+    double s1 = 0.0, s2 = 0.0, h0 = 0.0, h1 = 0.0;
+    if (M != -INFINITY) {
+        for (int b = threadIdx.x; b < nparts; b += FB) {
+            const LsePartial p = parts[b];
+            if (p.m != -INFINITY) {
+                const double f = exp(p.m - M);
+                s1 += p.s1 * f;
+                s2 += p.s2 * (f * f);
+            }
+            if (mon_parts) { h0 += mon_parts[b].x; h1 += mon_parts[b].y; }
+        }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    h0 = warp_sum(h0);
+    h1 = warp_sum(h1);
+    __syncthreads();
+    if (lane == 0) { sm_a[warp] = s1; sm_b[warp] = s2; sm_c[warp] = h0; sm_d[warp] = h1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LsePartial t{M, 0.0, 0.0};
+        double H0 = 0.0, H1 = 0.0;
+        for (int w = 0; w < FB / 32; ++w) { t.s1 += sm_a[w]; t.s2 += sm_b[w]; H0 += sm_c[w]; H1 += sm_d[w]; }
+        if (mon_parts && mon_out) { mon_out[0] = H0; mon_out[1] = H1; }
         if (t.m == -INFINITY || !(t.s1 > 0.0)) {
             raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
             return;
@@ -172,9 +201,9 @@ inline int reduce_blocks(int64_t n)
 }  // namespace
 
 void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
-                             int accumulate_nc, cudaStream_t s)
+                             int accumulate_nc, cudaStream_t s, const double2 *mon_parts, double *mon_out)
 {
-    k_lse_finalize<<<1, FB, 0, s>>>(parts, nparts, st, n, mode, accumulate_nc);
+    k_lse_finalize<<<1, FB, 0, s>>>(parts, nparts, st, n, mode, accumulate_nc, mon_parts, mon_out);
 }
 
 extern "C" size_t smc_weights_workspace_bytes(int64_t n)
@@ -198,7 +227,7 @@ extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values
     const int nb = (int)((n + WB - 1) / WB);
     LsePartial *parts = (LsePartial *)ws;
     k_weights_pass<<<nb, WB, 0, s>>>(mode, lw_raw, values, n, st, parts);
-    k_lse_finalize<<<1, FB, 0, s>>>(parts, nb, st, n, mode, accumulate_nc);
+    k_lse_finalize<<<1, FB, 0, s>>>(parts, nb, st, n, mode, accumulate_nc, nullptr, nullptr);
     return smc_check_launch("smc_weights_update");
 }
 

@@ -83,8 +83,10 @@ def _cv_move_kernel(iter_, system):
     n = system.size
     ws, nb = _ws(system, n)
     w = system.weight_set
+    # a pending fused "pos" monitor of the previous iteration is reduced by this launch
+    mon = system.take_pending_monitor("pos")
     _abi.call("smc_pf_move", _abi.ptr(v.data), _abi.ptr(w.lw_raw), n, system.rng_set.seed,
-              _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_), w.state_ptr, None, ws, nb, _abi.stream())
+              _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_), w.state_ptr, None, mon, ws, nb, _abi.stream())
     return None
 
 
@@ -94,8 +96,15 @@ def cv_move():
 
 
 def cv_monitor(dim=2):
-    """Monitor of (x_pos, y_pos) (dim=4 returns all columns)."""
-    return MonitorEval(lambda it, system: system.value.column_view(0, dim), dim)
+    """Monitor of (x_pos, y_pos) (dim=4 returns all columns).
+
+    With dim=2 it is fusable: the next cv_move reduces it from the state it
+    loads anyway (``fused_with="cv_move"``); the sampler falls back to the
+    standalone weighted reduction whenever the history is read first."""
+    ev = MonitorEval(lambda it, system: system.value.column_view(0, dim), dim)
+    if dim == 2:
+        ev.fused_with = "cv_move"
+    return ev
 
 
 def make_sampler(n, scheme=ResampleScheme.Systematic, threshold=0.5, seed=0, device="cuda", monitor_dim=2):

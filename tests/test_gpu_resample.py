@@ -139,6 +139,25 @@ def test_errors_surface():
         gpu_resample("stratified", [0.5, 0.5], u=[0.1])  # needs 2 uniforms
 
 
+@pytest.mark.parametrize("scheme", ["stratified", "systematic", "residual_stratified", "residual_systematic"])
+def test_fast_F_path_equals_exact_path(scheme):
+    """The fp64 guard-band path of F(X) and the exact 128-bit path give identical counts."""
+    from paper_1306_5583_b200 import _abi
+    for n in (3, 1000, 65537, 1 << 20):
+        for kind in ("skewed", "uniform", "equal"):
+            w = weights(n, kind)
+            u = np.random.default_rng(n + 1).random(n)
+            if kind == "equal":
+                u[:] = 1 - 2.0 ** -53  # stresses ties at stratum boundaries
+            fast, _ = gpu_resample(scheme, w, u=u)
+            _abi.call("smc_debug_set", 1, 1)
+            try:
+                exact, _ = gpu_resample(scheme, w, u=u)
+            finally:
+                _abi.call("smc_debug_set", 1, 0)
+            assert np.array_equal(fast, exact), (scheme, n, kind)
+
+
 def test_launch_configuration_invariance_sharded_tiles():
     """Counts for a prefix of tiles don't depend on the tail: integer CDF is associative."""
     n = 5 * 2048

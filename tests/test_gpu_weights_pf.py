@@ -63,7 +63,7 @@ def test_weights_vs_oracle(n):
     assert abs(ws.ess() - ess) <= 1e-12 * ess
     ws.add_log_weight(inc)
     st = ws.host_state()
-    assert abs(st.ess - ess2) <= 1e-12 * ess2
+    assert abs(st.ess - ess2) <= 1e-10 * ess2  # oracle: sequential sum over N; device: tree
     assert abs(st.nc_inc - nc) <= 1e-12 * max(1.0, abs(nc))
     np.testing.assert_allclose(ws.read_log_weight().cpu().numpy(), lw, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(ws.read_weight().cpu().numpy(), w, rtol=1e-11, atol=1e-300)
