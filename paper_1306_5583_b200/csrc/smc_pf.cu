@@ -131,7 +131,15 @@ PfConst pf_constants()
 
 extern "C" size_t smc_pf_workspace_bytes(int64_t n)
 {
-    return (size_t)((n + PB - 1) / PB + 1) * (sizeof(LsePartial) + sizeof(double2)) + 256;
+    return (size_t)((n + PB - 1) / PB + 1) * (sizeof(LsePartial) + sizeof(double2)) + smc_lse_scratch_bytes() + 512;
+}
+
+// workspace: [LsePartial nb+1][double2 nb+1][finalize scratch]
+static void *pf_scratch(void *ws, int nb)
+{
+    size_t o = ((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255;
+    o += ((size_t)(nb + 1) * sizeof(double2) + 255) & ~(size_t)255;
+    return (char *)ws + o;
 }
 
 static int pf_check(double *x, double *lw_raw, int64_t n, uint64_t *ctrs, const double *obs, smc_wstate *st,
@@ -152,9 +160,10 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, 
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
+    void *scratch = pf_scratch(ws, nb);
     k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
                                 pf_constants(), st, parts);
-    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s);
+    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s, scratch);
     return smc_check_launch("smc_pf_init");
 }
 
@@ -168,14 +177,15 @@ extern "C" int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, 
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
     double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
+    void *scratch = pf_scratch(ws, nb);
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
     if (monitor_prev) {
         k_pf_move<true><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts, mon);
-        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, mon, monitor_prev);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev);
     } else {
         k_pf_move<false><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts,
                                            nullptr);
-        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch);
     }
     return smc_check_launch("smc_pf_move");
 }

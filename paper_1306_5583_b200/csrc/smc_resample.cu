@@ -67,8 +67,9 @@ struct Layout {
     uint32_t *lb_status;
     uint4 *lb_agg, *lb_incl;
     int32_t *zpos, *sp_idx, *sp_start;
+    int32_t *tile_plo;  // per rank tile: index of the surplus parent covering its first rank
     uint64_t *qfull;
-    int32_t *cnt;
+    int32_t *cnt;       // multinomial histogram, then the counts when the caller passes none
     size_t bytes;
 };
 
@@ -92,6 +93,7 @@ Layout layout(void *ws, int64_t n)
     L.zpos = (int32_t *)take(sizeof(int32_t) * (n + 8));
     L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));  // P <= n even for invalid counts
     L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
+    L.tile_plo = (int32_t *)take(sizeof(int32_t) * (nt + 2));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
     L.bytes = o;
@@ -400,44 +402,26 @@ SMC_DEV uint32_t ld_status(const uint32_t *p) { return *(volatile const uint32_t
 // blocked smem index with one pad word per 16: conflict-free for 64-bit reads of t*8+j
 SMC_DEV int pad16(int i) { return i + (i >> 4); }
 
-// mode: 0 = counts from weights (sampler path), 1 = counts given (replication_to_parents)
-__global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src, const int32_t *__restrict__ cin,
-                                                  int64_t n, int64_t nt, double m_out, double rscale, Key key,
-                                                  uint64_t stream, const double *__restrict__ u,
-                                                  int32_t *__restrict__ counts, int32_t *__restrict__ parents,
-                                                  int32_t *status, Layout L)
+// Pass B1: counts per particle.  Embarrassingly parallel (no inter-tile wait);
+// the counts go to `counts` (the caller's or the workspace's).
+__global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t n, double m_out, double rscale,
+                                                  Key key, uint64_t stream, const double *__restrict__ u,
+                                                  int32_t *__restrict__ counts, Layout L)
 {
     RsHeader *h = L.hdr;
     if (!h->active) return;
     __shared__ uint64_t sm[RT / 32 + 1];
-    __shared__ uint32_t s_tile;
-    __shared__ uint4 s_excl;
     __shared__ uint64_t s_q[TILE + TILE / 16];
     __shared__ int32_t s_fb[TILE + TILE / 16];
     if (h->trivial) {  // N == 1: no-op resample
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            if (counts) counts[0] = (int32_t)m_out;
-            if (parents) parents[0] = 0;
-            h->Z_total = h->S_total = h->P_total = 0;
-            L.sp_start[0] = 0;
-        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)m_out;
         return;
     }
-    if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
-    __syncthreads();
-    const int64_t b = s_tile;
+    const int64_t b = blockIdx.x;
     const int64_t tbase = b * TILE;
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
     int32_t c[RI];
-    if (mode == 1) {
-        bool bad = false;
-#pragma unroll
-        for (int j = 0; j < RI; ++j) {
-            c[j] = base + j < n ? cin[base + j] : 1;
-            if (c[j] < 0) { bad = true; c[j] = 0; }
-        }
-        if (bad) raise_status(status, SMC_ECOUNTS);
-    } else {
+    {
         const bool residual = is_residual(scheme);
         const NormLw nl = src.norm();
         // stage: coalesced striped loads -> q (and f) -> shared memory -> blocked per thread
@@ -498,18 +482,57 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
             }
         }
     }
-    if (counts) {
-        if (base + RI <= n) {
-            reinterpret_cast<int4 *>(counts + base)[0] = make_int4(c[0], c[1], c[2], c[3]);
-            reinterpret_cast<int4 *>(counts + base)[1] = make_int4(c[4], c[5], c[6], c[7]);
-        } else {
+    if (base + RI <= n) {
+        reinterpret_cast<int4 *>(counts + base)[0] = make_int4(c[0], c[1], c[2], c[3]);
+        reinterpret_cast<int4 *>(counts + base)[1] = make_int4(c[4], c[5], c[6], c[7]);
+    } else {
 #pragma unroll
-            for (int j = 0; j < RI; ++j)
-                if (base + j < n) counts[base + j] = c[j];
-        }
+        for (int j = 0; j < RI; ++j)
+            if (base + j < n) counts[base + j] = c[j];
     }
-    if (!parents) return;
-    // ---- parent map: decoupled lookback over (Z, S, P) ----
+}
+
+// Pass B2: replication_to_parents' rank scan.  A cheap tile
+// (8 counts per thread) publishes its (zero slots, surplus children, surplus
+// parents) aggregate at once, then a DECOUPLED LOOKBACK finds its exclusive
+// prefix; it emits the survivor half of the parent map, the compacted
+// zero-slot list, the compacted surplus-parent list and, for pass C, the
+// surplus parent covering each rank tile's first rank.
+__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt,
+                                                 int32_t *__restrict__ parents, int32_t *status, Layout L)
+{
+    RsHeader *h = L.hdr;
+    if (!h->active) return;
+    __shared__ uint64_t sm[RT / 32 + 1];
+    __shared__ uint32_t s_tile;
+    __shared__ uint4 s_excl;
+    if (h->trivial) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            parents[0] = 0;
+            h->Z_total = h->S_total = h->P_total = 0;
+            L.sp_start[0] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
+    __syncthreads();
+    const int64_t b = s_tile;
+    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;
+    int32_t c[RI];
+    if (base + RI <= n) {
+        const int4 a0 = __ldcg(reinterpret_cast<const int4 *>(cin + base));
+        const int4 a1 = __ldcg(reinterpret_cast<const int4 *>(cin + base) + 1);
+        c[0] = a0.x; c[1] = a0.y; c[2] = a0.z; c[3] = a0.w;
+        c[4] = a1.x; c[5] = a1.y; c[6] = a1.z; c[7] = a1.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < RI; ++j) c[j] = base + j < n ? __ldcg(cin + base + j) : 1;  // padding: not zero, no surplus
+    }
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < RI; ++j)
+        if (c[j] < 0) { bad = true; c[j] = 0; }
+    if (bad) raise_status(status, SMC_ECOUNTS);
     uint32_t tz = 0, tp = 0;
     uint64_t ts = 0;
 #pragma unroll
@@ -586,8 +609,11 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int mode, int scheme, WSrc src
             if (c[j] >= 2) {
                 L.sp_idx[pr] = (int32_t)i;
                 L.sp_start[pr] = (int32_t)sr;
+                const uint32_t se = sr + (uint32_t)(c[j] - 1);
+                // rank tiles whose first rank this parent's surplus children cover
+                for (uint32_t m = (sr + TILE - 1) / TILE * TILE; m < se; m += TILE) L.tile_plo[m / TILE] = (int32_t)pr;
                 ++pr;
-                sr += (uint32_t)(c[j] - 1);
+                sr = se;
             }
         } else {
             L.zpos[zr++] = (int32_t)i;
@@ -631,24 +657,12 @@ __global__ void __launch_bounds__(RT) k_rs_assign(int32_t *__restrict__ parents,
     const uint32_t r0 = blockIdx.x * (uint32_t)TILE;
     if (r0 >= Z) return;
     const uint32_t r1 = r0 + TILE < Z ? r0 + TILE : Z;
-    __shared__ int32_t s_start[TILE + 1], s_idx[TILE + 1];
-    __shared__ uint32_t s_lo, s_cnt;
-    if (threadIdx.x == 0) {
-        // last p with sp_start[p] <= r  (sp_start strictly increasing, sentinel at P)
-        auto ub = [&](uint32_t r) {
-            uint32_t lo = 0, hi = P;  // first index with sp_start > r, in [0, P]
-            while (lo < hi) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if ((uint32_t)__ldcg(&L.sp_start[mid]) > r) hi = mid; else lo = mid + 1;
-            }
-            return lo;
-        };
-        const uint32_t plo = ub(r0) - 1, phi = ub(r1 - 1) - 1;
-        s_lo = plo;
-        s_cnt = phi - plo + 1;
-    }
-    __syncthreads();
-    const uint32_t plo = s_lo, cnt = s_cnt;  // cnt <= r1 - r0: every surplus parent covers >= 1 rank
+    __shared__ int32_t s_start[TILE + 2], s_idx[TILE + 2];
+    // merge-path boundaries from pass B2: the surplus parents covering r0 and r1 (or the last one);
+    // every surplus parent covers >= 1 rank, so at most TILE + 1 of them touch [r0, r1]
+    const uint32_t plo = (uint32_t)__ldcg(&L.tile_plo[blockIdx.x]);
+    const uint32_t phi = r1 < Z ? (uint32_t)__ldcg(&L.tile_plo[blockIdx.x + 1]) : P - 1;
+    const uint32_t cnt = phi - plo + 1;
     for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
         s_start[k] = __ldcg(&L.sp_start[plo + k]);
         s_idx[k] = __ldcg(&L.sp_idx[plo + k]);
@@ -694,7 +708,9 @@ __global__ void __launch_bounds__(RT) k_rs_assign(int32_t *__restrict__ parents,
             for (int j = 0; j < RI; ++j)
                 if (j < nr) st256((double *)(rows + (int64_t)dst[j] * 32), v[j]);
         } else {
-            for (int j = 0; j < nr; ++j) copy_row(rows, row_bytes, dst[j], par[j]);
+#pragma unroll
+            for (int j = 0; j < RI; ++j)
+                if (j < nr) copy_row(rows, row_bytes, dst[j], par[j]);
         }
     }
 }
@@ -760,6 +776,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (!u && !ctr) return smc_set_error(SMC_EINVAL, "smc_resample: need uniforms or a stream counter");
     if ((parents || rows) && m_out != n)
         return smc_set_error(SMC_EINVAL, "smc_resample: parent map / copy need m_out == n");
+    if (rows && !parents) return smc_set_error(SMC_EINVAL, "smc_resample: the row copy needs a parents buffer");
     if (rows && (row_bytes < 8 || (row_bytes & 7)))
         return smc_set_error(SMC_EINVAL, "smc_resample: row_bytes must be a positive multiple of 8");
     if (rows && row_bytes == 32 && ((uintptr_t)rows & 31))
@@ -783,10 +800,12 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
         k_rs_multinomial<<<grid_cap((m_out + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
     }
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(0, scheme, src, nullptr, n, nt, mo, rscale, key, stream_index, u,
-                                            counts, parents, status, L);
-    if (parents || rows)
+    int32_t *cout = counts ? counts : L.cnt;
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
+    if (parents) {
+        k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, nt, parents, status, L);
         k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, (char *)rows, row_bytes, L);
+    }
     return smc_check_launch("smc_resample");
 }
 
@@ -800,10 +819,9 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
         return smc_set_error(SMC_EWORKSPACE, "smc_replication_to_parents: workspace too small");
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
-    WSrc src{nullptr, nullptr, nullptr, n};
+    if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(1, 0, src, counts, n, nt, 0.0, 0.0, Key{0, 0}, 0, nullptr, nullptr,
-                                            parents, status, L);
+    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(counts, n, nt, parents, status, L);
     k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, nullptr, 0, L);
     return smc_check_launch("smc_replication_to_parents");
 }

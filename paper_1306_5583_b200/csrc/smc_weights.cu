@@ -44,21 +44,23 @@ __global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restric
     if (threadIdx.x == 0) parts[blockIdx.x] = p;
 }
 
-constexpr int FB = 1024;
+constexpr int FB = 256;   // threads per finalize block
+constexpr int FG = 148;   // level-1 finalize blocks (one per SM)
 
-// Two phases so every exp is independent (no dependent online-rescale chain):
-// M = max_b m_b, then s1 = sum_b s1_b e^{m_b - M}, s2 = sum_b s2_b e^{2(m_b - M)}.
-// Optional monitor partials (mon_parts[b] = sum_i W_i h(X_i) over block b) are
-// summed in the same fixed order into mon_out[0..1].
-__global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ parts, int nparts,
-                                                      smc_wstate *st, int64_t n, int mode, int accumulate_nc,
-                                                      const double2 *__restrict__ mon_parts, double *mon_out)
+// Finalize = two small launches so the ~N/256 block partials are read by the
+// whole GPU, not one SM: level 1 (FG blocks) reduces a contiguous slice each,
+// level 2 (one block) combines the FG results in index order (deterministic).
+// Each level is two-phase so every exp is independent: M = max m_b, then
+// s1 = sum s1_b e^{m_b - M}, s2 = sum s2_b e^{2(m_b - M)}.  Optional monitor
+// partials (mon_parts[b] = sum_i W_i h(X_i) over block b) ride along.
+SMC_DEV void lse_slice(const LsePartial *__restrict__ parts, const double2 *__restrict__ mon, int b0, int b1,
+                       LsePartial *out, double2 *out_mon)
 {
     __shared__ double sm_a[FB / 32], sm_b[FB / 32], sm_c[FB / 32], sm_d[FB / 32];
     __shared__ double s_M;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double m = -INFINITY;
-    for (int b = threadIdx.x; b < nparts; b += FB) m = fmax(m, parts[b].m);
+    for (int b = b0 + threadIdx.x; b < b1; b += FB) m = fmax(m, parts[b].m);
     m = warp_max(m);
     if (lane == 0) sm_a[warp] = m;
     __syncthreads();
@@ -70,16 +72,14 @@ __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restric
     __syncthreads();
     const double M = s_M;
     double s1 = 0.0, s2 = 0.0, h0 = 0.0, h1 = 0.0;
-    if (M != -INFINITY) {
-        for (int b = threadIdx.x; b < nparts; b += FB) {
-            const LsePartial p = parts[b];
-            if (p.m != -INFINITY) {
-                const double f = exp(p.m - M);
-                s1 += p.s1 * f;
-                s2 += p.s2 * (f * f);
-            }
-            if (mon_parts) { h0 += mon_parts[b].x; h1 += mon_parts[b].y; }
+    for (int b = b0 + threadIdx.x; b < b1; b += FB) {
+        const LsePartial p = parts[b];
+        if (p.m != -INFINITY) {
+            const double f = exp(p.m - M);
+            s1 += p.s1 * f;
+            s2 += p.s2 * (f * f);
         }
+        if (mon) { h0 += mon[b].x; h1 += mon[b].y; }
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
@@ -92,7 +92,29 @@ __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restric
         LsePartial t{M, 0.0, 0.0};
         double H0 = 0.0, H1 = 0.0;
         for (int w = 0; w < FB / 32; ++w) { t.s1 += sm_a[w]; t.s2 += sm_b[w]; H0 += sm_c[w]; H1 += sm_d[w]; }
-        if (mon_parts && mon_out) { mon_out[0] = H0; mon_out[1] = H1; }
+        *out = t;
+        *out_mon = make_double2(H0, H1);
+    }
+}
+
+__global__ void __launch_bounds__(FB) k_lse_level1(const LsePartial *__restrict__ parts, int nparts,
+                                                    const double2 *__restrict__ mon, LsePartial *l2, double2 *l2mon)
+{
+    const int per = (nparts + FG - 1) / FG;
+    const int b0 = min(nparts, (int)blockIdx.x * per), b1 = min(nparts, b0 + per);
+    lse_slice(parts, mon, b0, b1, l2 + blockIdx.x, l2mon + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ l2, const double2 *__restrict__ l2mon,
+                                                      int has_mon, smc_wstate *st, int64_t n, int mode,
+                                                      int accumulate_nc, double *mon_out)
+{
+    __shared__ LsePartial s_t;
+    __shared__ double2 s_h;
+    lse_slice(l2, has_mon ? l2mon : nullptr, 0, FG, &s_t, &s_h);
+    if (threadIdx.x == 0) {
+        const LsePartial t = s_t;
+        if (has_mon && mon_out) { mon_out[0] = s_h.x; mon_out[1] = s_h.y; }
         if (t.m == -INFINITY || !(t.s1 > 0.0)) {
             raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
             return;
@@ -200,15 +222,21 @@ inline int reduce_blocks(int64_t n)
 
 }  // namespace
 
+size_t smc_lse_scratch_bytes() { return FG * (sizeof(LsePartial) + sizeof(double2)); }
+
 void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
-                             int accumulate_nc, cudaStream_t s, const double2 *mon_parts, double *mon_out)
+                             int accumulate_nc, cudaStream_t s, void *scratch, const double2 *mon_parts,
+                             double *mon_out)
 {
-    k_lse_finalize<<<1, FB, 0, s>>>(parts, nparts, st, n, mode, accumulate_nc, mon_parts, mon_out);
+    LsePartial *l2 = (LsePartial *)scratch;
+    double2 *l2mon = (double2 *)(l2 + FG);
+    k_lse_level1<<<FG, FB, 0, s>>>(parts, nparts, mon_parts, l2, l2mon);
+    k_lse_finalize<<<1, FB, 0, s>>>(l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out);
 }
 
 extern "C" size_t smc_weights_workspace_bytes(int64_t n)
 {
-    return (size_t)((n + WB - 1) / WB + 1) * sizeof(LsePartial);
+    return (size_t)((n + WB - 1) / WB + 1) * sizeof(LsePartial) + smc_lse_scratch_bytes() + 256;
 }
 
 extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values, int64_t n, smc_wstate *st,
@@ -227,7 +255,8 @@ extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values
     const int nb = (int)((n + WB - 1) / WB);
     LsePartial *parts = (LsePartial *)ws;
     k_weights_pass<<<nb, WB, 0, s>>>(mode, lw_raw, values, n, st, parts);
-    k_lse_finalize<<<1, FB, 0, s>>>(parts, nb, st, n, mode, accumulate_nc, nullptr, nullptr);
+    void *scratch = (char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255);
+    smc_launch_lse_finalize(parts, nb, st, n, mode, accumulate_nc, s, scratch);
     return smc_check_launch("smc_weights_update");
 }
 

@@ -53,6 +53,8 @@ SMC_DEV LsePartial lse_combine(LsePartial a, LsePartial b)
 
 // Finalize over block partials (one block, fixed combine order => deterministic).
 // mode: SMC_W_* of the update (ADD_LOG sets nc_inc and optionally log_zconst).
+// `scratch` needs smc_lse_scratch_bytes() bytes of device memory.
+size_t smc_lse_scratch_bytes();
 void smc_launch_lse_finalize(const smc::LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
-                             int accumulate_nc, cudaStream_t s, const double2 *mon_parts = nullptr,
+                             int accumulate_nc, cudaStream_t s, void *scratch, const double2 *mon_parts = nullptr,
                              double *mon_out = nullptr);
