@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
             sq += qq.q;
             sqr += qq.qr;
             sf += qq.f;
+            L.qfull[i] = residual ? qq.qr : qq.q;  // the searched quantity, for passes M and B1
             if (is_multinomial(scheme)) L.cnt[i] = 0;
         }
     }
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     u128 tq = 0;
     uint64_t tqr = 0;
     int64_t tf = 0;
+#pragma unroll 8
     for (int64_t b = b0; b < b1; ++b) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -281,6 +283,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     if (!s_ok) return;
     // exclusive prefix of the searched per-tile totals (all < 2^64 once T is validated)
     uint64_t mine = 0;
+#pragma unroll 8
     for (int64_t b = b0; b < b1; ++b) mine += residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b];
     uint64_t tot;
     uint64_t run = block_exclusive_sum<SB, uint64_t>(mine, sm64, &tot);
@@ -297,20 +300,12 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
 {
     if (!L.hdr->active || L.hdr->trivial || L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
-    const bool residual = is_residual(scheme);
-    const NormLw nl = src.norm();
     const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * RI;  // blocked
     uint64_t v[RI];
     uint64_t loc = 0;
-    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < RI; ++j) {
-        const int64_t i = base + j;
-        v[j] = 0;
-        if (i < n) {
-            const Quant qq = quantize(src.weight(src.raw(i, nl), nl), residual, m_out, rscale, bad);
-            v[j] = residual ? qq.qr : qq.q;
-        }
+    for (int j = 0; j < RI; ++j) {  // q (or q') from pass A, scanned in place into Q
+        v[j] = base + j < n ? L.qfull[base + j] : 0;
         loc += v[j];
     }
     uint64_t tot;
@@ -390,12 +385,17 @@ SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
     return s + (d > 0.0 ? 1 : 0);
 }
 
-// pack (zero slots, surplus parents) in the top, surplus children in the low
-// 40 bits -- tile-local sums never carry across fields (<= 2048, < 2^31).
-SMC_DEV uint64_t pack_zsp(uint32_t z, uint32_t p, uint64_t s) { return ((uint64_t)z << 52) | ((uint64_t)p << 40) | s; }
-SMC_DEV uint32_t unz(uint64_t v) { return (uint32_t)(v >> 52); }
-SMC_DEV uint32_t unp(uint64_t v) { return (uint32_t)((v >> 40) & 0xFFF); }
-SMC_DEV uint64_t uns(uint64_t v) { return v & ((1ull << 40) - 1); }
+// Pass B2 tiles are larger than pass A/B1/C tiles: the lookback cost is per
+// tile, and these tiles are cheap (8 KiB of counts), so fewer of them win.
+constexpr int RI2 = 32;
+constexpr int TILE2 = RT * RI2;  // 8192 counts per rank-scan tile
+
+// pack (zero slots, surplus parents) in the top 2 x 14 bits, surplus children in
+// the low 36 -- tile-local sums never carry across fields (<= 8192, < 2^31).
+SMC_DEV uint64_t pack_zsp(uint32_t z, uint32_t p, uint64_t s) { return ((uint64_t)z << 50) | ((uint64_t)p << 36) | s; }
+SMC_DEV uint32_t unz(uint64_t v) { return (uint32_t)(v >> 50); }
+SMC_DEV uint32_t unp(uint64_t v) { return (uint32_t)((v >> 36) & 0x3FFF); }
+SMC_DEV uint64_t uns(uint64_t v) { return v & ((1ull << 36) - 1); }
 
 SMC_DEV uint32_t ld_status(const uint32_t *p) { return *(volatile const uint32_t *)p; }
 
@@ -423,33 +423,55 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
     int32_t c[RI];
     {
         const bool residual = is_residual(scheme);
-        const NormLw nl = src.norm();
-        // stage: coalesced striped loads -> q (and f) -> shared memory -> blocked per thread
-        double r[RI];
-#pragma unroll
-        for (int j = 0; j < RI; ++j) {
-            const int64_t i = tbase + j * RT + threadIdx.x;
-            r[j] = i < n ? src.raw(i, nl) : 0.0;
-        }
-        bool bad = false;
-#pragma unroll
-        for (int j = 0; j < RI; ++j) {
-            const int li = j * RT + threadIdx.x;
-            const int64_t i = tbase + li;
-            Quant qq{0, 0, 0};
-            if (i < n) qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
-            s_q[pad16(li)] = residual ? qq.qr : qq.q;
-            s_fb[pad16(li)] = (int32_t)qq.f;
-        }
-        __syncthreads();
         uint64_t q[RI];
         int32_t f[RI];
         uint64_t loc = 0;
+        if (!residual) {
+            // q_i was materialized by pass A: no exp / quantization here, 64 contiguous bytes per thread
+            if (!is_multinomial(scheme)) {
+                if (base + RI <= n) {
 #pragma unroll
-        for (int j = 0; j < RI; ++j) {
-            q[j] = s_q[pad16(threadIdx.x * RI + j)];
-            f[j] = s_fb[pad16(threadIdx.x * RI + j)];
-            loc += q[j];
+                    for (int v = 0; v < RI / 2; ++v) {
+                        const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2 *>(L.qfull + base) + v);
+                        q[2 * v] = a.x;
+                        q[2 * v + 1] = a.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RI; ++j) q[j] = base + j < n ? __ldcg(L.qfull + base + j) : 0;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < RI; ++j) q[j] = 0;  // multinomial: counts come from the histogram
+            }
+#pragma unroll
+            for (int j = 0; j < RI; ++j) { f[j] = 0; loc += q[j]; }
+        } else {
+            const NormLw nl = src.norm();
+            // stage: coalesced striped loads -> q' and f -> shared memory -> blocked per thread
+            double r[RI];
+#pragma unroll
+            for (int j = 0; j < RI; ++j) {
+                const int64_t i = tbase + j * RT + threadIdx.x;
+                r[j] = i < n ? src.raw(i, nl) : 0.0;
+            }
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < RI; ++j) {
+                const int li = j * RT + threadIdx.x;
+                const int64_t i = tbase + li;
+                Quant qq{0, 0, 0};
+                if (i < n) qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
+                s_q[pad16(li)] = qq.qr;
+                s_fb[pad16(li)] = (int32_t)qq.f;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < RI; ++j) {
+                q[j] = s_q[pad16(threadIdx.x * RI + j)];
+                f[j] = s_fb[pad16(threadIdx.x * RI + j)];
+                loc += q[j];
+            }
         }
         if (is_multinomial(scheme)) {
 #pragma unroll
@@ -517,26 +539,27 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
     __syncthreads();
     const int64_t b = s_tile;
-    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;
-    int32_t c[RI];
-    if (base + RI <= n) {
-        const int4 a0 = __ldcg(reinterpret_cast<const int4 *>(cin + base));
-        const int4 a1 = __ldcg(reinterpret_cast<const int4 *>(cin + base) + 1);
-        c[0] = a0.x; c[1] = a0.y; c[2] = a0.z; c[3] = a0.w;
-        c[4] = a1.x; c[5] = a1.y; c[6] = a1.z; c[7] = a1.w;
+    const int64_t base = b * TILE2 + (int64_t)threadIdx.x * RI2;
+    int32_t c[RI2];
+    if (base + RI2 <= n) {
+#pragma unroll
+        for (int v = 0; v < RI2 / 4; ++v) {
+            const int4 a = __ldcg(reinterpret_cast<const int4 *>(cin + base) + v);
+            c[4 * v] = a.x; c[4 * v + 1] = a.y; c[4 * v + 2] = a.z; c[4 * v + 3] = a.w;
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < RI; ++j) c[j] = base + j < n ? __ldcg(cin + base + j) : 1;  // padding: not zero, no surplus
+        for (int j = 0; j < RI2; ++j) c[j] = base + j < n ? __ldcg(cin + base + j) : 1;  // padding: not zero, no surplus
     }
     bool bad = false;
 #pragma unroll
-    for (int j = 0; j < RI; ++j)
+    for (int j = 0; j < RI2; ++j)
         if (c[j] < 0) { bad = true; c[j] = 0; }
     if (bad) raise_status(status, SMC_ECOUNTS);
     uint32_t tz = 0, tp = 0;
     uint64_t ts = 0;
 #pragma unroll
-    for (int j = 0; j < RI; ++j) {
+    for (int j = 0; j < RI2; ++j) {
         tz += (c[j] == 0);
         tp += (c[j] >= 2);
         ts += c[j] >= 2 ? (uint64_t)(c[j] - 1) : 0;
@@ -601,7 +624,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     uint32_t sr = s_excl.y + (uint32_t)uns(tex);
     uint32_t pr = s_excl.z + unp(tex);
 #pragma unroll
-    for (int j = 0; j < RI; ++j) {
+    for (int j = 0; j < RI2; ++j) {
         const int64_t i = base + j;
         if (i >= n) break;
         if (c[j] >= 1) {
@@ -803,7 +826,8 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     int32_t *cout = counts ? counts : L.cnt;
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
     if (parents) {
-        k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, nt, parents, status, L);
+        const int64_t nt2 = (n + TILE2 - 1) / TILE2;
+        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, parents, status, L);
         k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, (char *)rows, row_bytes, L);
     }
     return smc_check_launch("smc_resample");
@@ -821,7 +845,8 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     Layout L = layout(ws, n);
     if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
-    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(counts, n, nt, parents, status, L);
+    const int64_t nt2 = (n + TILE2 - 1) / TILE2;
+    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, parents, status, L);
     k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, nullptr, 0, L);
     return smc_check_launch("smc_replication_to_parents");
 }
