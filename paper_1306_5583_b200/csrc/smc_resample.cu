@@ -40,6 +40,7 @@ constexpr uint64_t T_LO = (1ull << 63) - (1ull << 43);
 constexpr uint64_t T_HI = (1ull << 63) + (1ull << 43);
 constexpr double TWO53 = 9007199254740992.0;
 constexpr double INV53 = 1.0 / 9007199254740992.0;
+constexpr int ANCHOR = 64;  // rank granularity of the surplus-parent anchors (pass B2 -> C)
 
 __device__ int g_force_exact = 0;  // test hook: always take the exact 128-bit F path
 
@@ -66,8 +67,8 @@ struct Layout {
     uint64_t *tile_pre;
     uint32_t *lb_status;
     uint4 *lb_agg, *lb_incl;
-    int32_t *zpos, *sp_idx, *sp_start;
-    int32_t *tile_plo;  // per rank tile: index of the surplus parent covering its first rank
+    int32_t *anchor, *sp_idx, *sp_start;  // anchor[k]: surplus parent covering rank k*ANCHOR
+    int32_t *tile_z0;   // per slot tile: its first zero rank (and Z at index nt)
     uint64_t *qfull;
     int32_t *cnt;       // multinomial histogram, then the counts when the caller passes none
     size_t bytes;
@@ -90,10 +91,10 @@ Layout layout(void *ws, int64_t n)
     L.lb_status = (uint32_t *)take(sizeof(uint32_t) * nt);
     L.lb_agg = (uint4 *)take(sizeof(uint4) * nt);
     L.lb_incl = (uint4 *)take(sizeof(uint4) * nt);
-    L.zpos = (int32_t *)take(sizeof(int32_t) * (n + 8));
+    L.anchor = (int32_t *)take(sizeof(int32_t) * (n / ANCHOR + 2));
     L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));  // P <= n even for invalid counts
     L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
-    L.tile_plo = (int32_t *)take(sizeof(int32_t) * (nt + 2));
+    L.tile_z0 = (int32_t *)take(sizeof(int32_t) * (nt + 2));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
     L.bytes = o;
@@ -515,27 +516,19 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
 }
 
 // Pass B2: replication_to_parents' rank scan.  A cheap tile
-// (8 counts per thread) publishes its (zero slots, surplus children, surplus
+// (32 counts per thread) publishes its (zero slots, surplus children, surplus
 // parents) aggregate at once, then a DECOUPLED LOOKBACK finds its exclusive
-// prefix; it emits the survivor half of the parent map, the compacted
-// zero-slot list, the compacted surplus-parent list and, for pass C, the
-// surplus parent covering each rank tile's first rank.
-__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt,
-                                                 int32_t *__restrict__ parents, int32_t *status, Layout L)
+// prefix.  It emits the compacted surplus-parent list (index, first surplus
+// rank), rank anchors every ANCHOR ranks, and each slot tile's first zero rank.
+// Writes are per-thread contiguous runs; no 4-byte scatter.
+__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt2,
+                                                 int32_t *status, Layout L)
 {
     RsHeader *h = L.hdr;
-    if (!h->active) return;
+    if (!h->active || h->trivial) return;
     __shared__ uint64_t sm[RT / 32 + 1];
     __shared__ uint32_t s_tile;
     __shared__ uint4 s_excl;
-    if (h->trivial) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            parents[0] = 0;
-            h->Z_total = h->S_total = h->P_total = 0;
-            L.sp_start[0] = 0;
-        }
-        return;
-    }
     if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
     __syncthreads();
     const int64_t b = s_tile;
@@ -543,13 +536,15 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     int32_t c[RI2];
     if (base + RI2 <= n) {
 #pragma unroll
-        for (int v = 0; v < RI2 / 4; ++v) {
-            const int4 a = __ldcg(reinterpret_cast<const int4 *>(cin + base) + v);
-            c[4 * v] = a.x; c[4 * v + 1] = a.y; c[4 * v + 2] = a.z; c[4 * v + 3] = a.w;
+        for (int v = 0; v < RI2 / 8; ++v) {
+            const int4 *p = reinterpret_cast<const int4 *>(cin + base) + 2 * v;
+            const int4 a = p[0], d = p[1];
+            c[8 * v] = a.x; c[8 * v + 1] = a.y; c[8 * v + 2] = a.z; c[8 * v + 3] = a.w;
+            c[8 * v + 4] = d.x; c[8 * v + 5] = d.y; c[8 * v + 6] = d.z; c[8 * v + 7] = d.w;
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < RI2; ++j) c[j] = base + j < n ? __ldcg(cin + base + j) : 1;  // padding: not zero, no surplus
+        for (int j = 0; j < RI2; ++j) c[j] = base + j < n ? cin[base + j] : 1;  // padding: not zero, no surplus
     }
     bool bad = false;
 #pragma unroll
@@ -609,12 +604,13 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
         }
         if (lane == 0) {
             s_excl = ex;
-            if (b == nt - 1) {
+            if (b == nt2 - 1) {
                 const uint32_t Z = ex.x + a4.x, S = ex.y + a4.y, P = ex.z + a4.z;
                 h->Z_total = Z;
                 h->S_total = S;
                 h->P_total = P;
                 L.sp_start[P] = (int32_t)S;  // sentinel
+                L.tile_z0[(n + TILE - 1) / TILE] = (int32_t)Z;
                 if (Z != S) raise_status(status, SMC_ECOUNTS);  // sum(counts) != N
             }
         }
@@ -627,19 +623,16 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     for (int j = 0; j < RI2; ++j) {
         const int64_t i = base + j;
         if (i >= n) break;
-        if (c[j] >= 1) {
-            parents[i] = (int32_t)i;  // survivors keep their slot
-            if (c[j] >= 2) {
-                L.sp_idx[pr] = (int32_t)i;
-                L.sp_start[pr] = (int32_t)sr;
-                const uint32_t se = sr + (uint32_t)(c[j] - 1);
-                // rank tiles whose first rank this parent's surplus children cover
-                for (uint32_t m = (sr + TILE - 1) / TILE * TILE; m < se; m += TILE) L.tile_plo[m / TILE] = (int32_t)pr;
-                ++pr;
-                sr = se;
-            }
-        } else {
-            L.zpos[zr++] = (int32_t)i;
+        if ((i & (TILE - 1)) == 0) L.tile_z0[i / TILE] = (int32_t)zr;  // first zero rank of slot tile i / TILE
+        zr += (c[j] == 0);
+        if (c[j] >= 2) {
+            L.sp_idx[pr] = (int32_t)i;
+            L.sp_start[pr] = (int32_t)sr;
+            const uint32_t se = sr + (uint32_t)(c[j] - 1);
+            for (uint32_t m = (sr + ANCHOR - 1) / ANCHOR * ANCHOR; m < se; m += ANCHOR)
+                L.anchor[m / ANCHOR] = (int32_t)pr;  // the surplus parent covering rank m
+            ++pr;
+            sr = se;
         }
     }
 }
@@ -671,69 +664,98 @@ SMC_DEV void copy_row(char *rows, int64_t row_bytes, int64_t dst, int64_t srcr)
     }
 }
 
-__global__ void __launch_bounds__(RT) k_rs_assign(int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
+// Pass C, per SLOT tile (2048 particles): survivors map to themselves, the
+// tile's zero slots (ranks z0..z1-1) take the surplus children of the parents
+// staged from the anchored slice of the surplus-parent list (merge walk), the
+// full parent vector is written with one 32-byte store per thread, and every
+// zero-slot row is overwritten by its parent's row in place (sources count >= 2
+// and destinations count 0 are disjoint).
+constexpr int CSTAGE = TILE + 2 * ANCHOR + 2;
+
+__global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
+                                                  int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
                                                   Layout L)
 {
     const RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
+    if (!h->active) return;
+    if (h->trivial) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) parents[0] = 0;
+        return;
+    }
+    __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
+    __shared__ uint32_t sm32[RT / 32 + 1];
+    const int64_t t = blockIdx.x;
+    const int64_t base = t * TILE + (int64_t)threadIdx.x * RI;
+    const uint32_t z0 = (uint32_t)__ldcg(&L.tile_z0[t]), z1 = (uint32_t)__ldcg(&L.tile_z0[t + 1]);
     const uint32_t Z = h->Z_total, P = h->P_total;
-    const uint32_t r0 = blockIdx.x * (uint32_t)TILE;
-    if (r0 >= Z) return;
-    const uint32_t r1 = r0 + TILE < Z ? r0 + TILE : Z;
-    __shared__ int32_t s_start[TILE + 2], s_idx[TILE + 2];
-    // merge-path boundaries from pass B2: the surplus parents covering r0 and r1 (or the last one);
-    // every surplus parent covers >= 1 rank, so at most TILE + 1 of them touch [r0, r1]
-    const uint32_t plo = (uint32_t)__ldcg(&L.tile_plo[blockIdx.x]);
-    const uint32_t phi = r1 < Z ? (uint32_t)__ldcg(&L.tile_plo[blockIdx.x + 1]) : P - 1;
-    const uint32_t cnt = phi - plo + 1;
-    for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
-        s_start[k] = __ldcg(&L.sp_start[plo + k]);
-        s_idx[k] = __ldcg(&L.sp_idx[plo + k]);
-    }
-    __syncthreads();
-    // blocked ranks: thread owns RI consecutive ranks; one binary search, then a merge walk
-    const uint32_t ra = r0 + threadIdx.x * RI;
-    if (ra >= r1) return;
-    uint32_t lo = 0, hi = cnt;
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if ((uint32_t)s_start[mid] <= ra) lo = mid; else hi = mid;
-    }
-    int32_t dst[RI], par[RI];
-    const int nr = (int)(r1 - ra < (uint32_t)RI ? r1 - ra : RI);
-    if (nr == RI) {
-        const int4 z0 = __ldcg(reinterpret_cast<const int4 *>(L.zpos + ra));
-        const int4 z1 = __ldcg(reinterpret_cast<const int4 *>(L.zpos + ra) + 1);
-        dst[0] = z0.x; dst[1] = z0.y; dst[2] = z0.z; dst[3] = z0.w;
-        dst[4] = z1.x; dst[5] = z1.y; dst[6] = z1.z; dst[7] = z1.w;
+    int32_t c[RI];
+    if (base + RI <= n) {
+        const int4 *p = reinterpret_cast<const int4 *>(cin + base);
+        const int4 a = p[0], d = p[1];
+        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = d.x; c[5] = d.y; c[6] = d.z; c[7] = d.w;
     } else {
 #pragma unroll
-        for (int j = 0; j < RI; ++j) dst[j] = j < nr ? __ldcg(L.zpos + ra + j) : 0;
+        for (int j = 0; j < RI; ++j) c[j] = base + j < n ? cin[base + j] : 1;
     }
+    uint32_t nz = 0;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) nz += (c[j] == 0);
+    uint32_t tot;
+    const uint32_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first zero rank of this thread
+    uint32_t cnt = 0;
+    if (z1 > z0) {
+        // surplus parents covering ranks [z0, z1): between the anchors around z0 and z1-1
+        const uint32_t a0 = (uint32_t)__ldcg(&L.anchor[z0 / ANCHOR]);
+        const uint32_t ka = (z1 - 1) / ANCHOR + 1;
+        const uint32_t a1 = (uint64_t)ka * ANCHOR < Z ? (uint32_t)__ldcg(&L.anchor[ka]) : P - 1;
+        cnt = a1 - a0 + 1;
+        for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
+            s_start[k] = __ldcg(&L.sp_start[a0 + k]);
+            s_idx[k] = __ldcg(&L.sp_idx[a0 + k]);
+        }
+    }
+    __syncthreads();
+    int32_t par[RI];
+    uint32_t lo = 0;
+    if (nz) {  // last k with s_start[k] <= zr, then a forward merge walk
+        uint32_t hi = cnt;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint32_t)s_start[mid] <= zr) lo = mid; else hi = mid;
+        }
+    }
+    uint32_t r = zr;
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
-        const uint32_t r = ra + j;
-        while (lo + 1 < cnt && (uint32_t)s_start[lo + 1] <= r) ++lo;
-        par[j] = s_idx[lo];
+        par[j] = (int32_t)(base + j);  // survivors keep their slot
+        if (c[j] == 0) {
+            while (lo + 1 < cnt && (uint32_t)s_start[lo + 1] <= r) ++lo;
+            par[j] = s_idx[lo];
+            ++r;
+        }
     }
-    if (parents) {
+    if (base + RI <= n) {
+        int4 *p = reinterpret_cast<int4 *>(parents + base);
+        p[0] = make_int4(par[0], par[1], par[2], par[3]);
+        p[1] = make_int4(par[4], par[5], par[6], par[7]);
+    } else {
 #pragma unroll
         for (int j = 0; j < RI; ++j)
-            if (j < nr) parents[dst[j]] = par[j];
+            if (base + j < n) parents[base + j] = par[j];
     }
-    if (rows) {
+    if (rows && nz) {
         if (row_bytes == 32) {
             double4 v[RI];
 #pragma unroll
             for (int j = 0; j < RI; ++j)
-                if (j < nr) ld256((const double *)(rows + (int64_t)par[j] * 32), v[j]);  // 8 loads in flight
+                if (c[j] == 0 && base + j < n) ld256((const double *)(rows + (int64_t)par[j] * 32), v[j]);  // in flight
 #pragma unroll
             for (int j = 0; j < RI; ++j)
-                if (j < nr) st256((double *)(rows + (int64_t)dst[j] * 32), v[j]);
+                if (c[j] == 0 && base + j < n) st256((double *)(rows + (base + j) * 32), v[j]);
         } else {
 #pragma unroll
             for (int j = 0; j < RI; ++j)
-                if (j < nr) copy_row(rows, row_bytes, dst[j], par[j]);
+                if (c[j] == 0 && base + j < n) copy_row(rows, row_bytes, base + j, par[j]);
         }
     }
 }
@@ -827,8 +849,8 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
     if (parents) {
         const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, parents, status, L);
-        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, (char *)rows, row_bytes, L);
+        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
+        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, (char *)rows, row_bytes, L);
     }
     return smc_check_launch("smc_resample");
 }
@@ -846,8 +868,8 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
     const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, parents, status, L);
-    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(parents, nullptr, 0, L);
+    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, status, L);
+    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, nullptr, 0, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
