@@ -190,9 +190,14 @@ int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *c
 /* cv_move on every particle + incw = llh(t) -> add_log_weight(incw) fused in
  * one pass over the state; log_zconst += log sum W_{t-1} exp(incw).
  * incw_out may be NULL. */
-int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                smc_wstate *ws_state, double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes,
-                void *stream);
+int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
+                int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t, smc_wstate *ws_state,
+                double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes, void *stream);
+/* x_in / parents / gate fold the previous resample's copy into the move: row i
+ * is read from x_in[parents[i]] (x_in[i] when parents is NULL or *gate == 0)
+ * and written to x[i] -- copy_particles' simultaneous semantics
+ * by double buffering, so the resample never copies rows.  x_in == NULL means
+ * x_in = x (in place, parents must then be NULL). */
 /* monitor_prev (device, 2 doubles, may be NULL): receives the "pos" monitor
  * sum_i W_i (x_i, y_i) of the state the move CONSUMES -- the previous
  * iteration's estimate -- reduced from registers the move

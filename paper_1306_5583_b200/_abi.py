@@ -76,7 +76,7 @@ _SIGS = {
     "smc_copy_rows_inplace": ([_vp, _i64, _vp, _i64, _vp, _vp], C.c_int),
     "smc_pf_workspace_bytes": ([_i64], _sz),
     "smc_pf_init": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
-    "smc_pf_move": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -49,7 +49,46 @@ class StateMatrix:
         self.size, self.dim, self.order = int(size), int(dim), order
         self.device = torch.device(device)
         shape = (self.size, self.dim) if order == ROW_MAJOR else (self.dim, self.size)
-        self.data = torch.zeros(shape, dtype=torch.float64, device=self.device)
+        self._bufs = [torch.zeros(shape, dtype=torch.float64, device=self.device), None]
+        self._cur = 0
+        # A resample's copy may be deferred: (parents, gate) that the next gathering
+        # kernel (or materialize()) applies "as simultaneous".
+        self.pending = None
+
+    # -- storage --------------------------------------------------------------
+    @property
+    def data(self):
+        """The state (any deferred resample copy applied first)."""
+        self.materialize()
+        return self._bufs[self._cur]
+
+    @data.setter
+    def data(self, t):
+        self.pending = None
+        self._bufs[self._cur] = t
+
+    @property
+    def raw(self):
+        """Current buffer WITHOUT applying a pending copy (for gathering kernels)."""
+        return self._bufs[self._cur]
+
+    def alt(self):
+        """The second buffer of the double-buffered state (allocated on first use)."""
+        o = 1 - self._cur
+        if self._bufs[o] is None or self._bufs[o].shape != self._bufs[self._cur].shape:
+            self._bufs[o] = torch.empty_like(self._bufs[self._cur])
+        return self._bufs[o]
+
+    def swap(self):
+        self._cur = 1 - self._cur
+
+    def materialize(self):
+        """Apply a deferred resample copy in place (sources and destinations are disjoint)."""
+        if self.pending is None:
+            return
+        parents, gate = self.pending
+        self.pending = None
+        self.copy_inplace(parents, gate)
 
     # element / column access (SPEC.md:342)
     def _check(self, i, pos):
@@ -109,14 +148,19 @@ class StateMatrix:
             return ctypes.c_void_p(self.data.data_ptr()), 8 * self.dim
         return None
 
+    # A value collection whose next move kernel gathers x_in[parents[i]] (double
+    # buffering) sets this: the sampler then only produces the parent map.
+    defer_copy = False
+
     def copy_inplace(self, parents, gate=None):
         """In-place copy for a ParentVector (sources and destinations are disjoint)."""
+        buf = self.raw
         if self.order == ROW_MAJOR:
-            _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(self.data.data_ptr()), 8 * self.dim,
+            _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(buf.data_ptr()), 8 * self.dim,
                       _abi.ptr(parents), self.size, gate, _abi.stream())
         else:
             for c in range(self.dim):
-                _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(self.data[c].data_ptr()), 8, _abi.ptr(parents),
+                _abi.call("smc_copy_rows_inplace", ctypes.c_void_p(buf[c].data_ptr()), 8, _abi.ptr(parents),
                           self.size, gate, _abi.stream())
 
 
@@ -299,6 +343,8 @@ class Sampler:
             raise RuntimeError("initialize: no init operation set")
         self._layout()
         self.system.pending_monitors.clear()
+        if hasattr(self.system.value, "pending"):
+            self.system.value.pending = None
         self._hist = None
         self._rows = 0
         self._path_grid = []
@@ -337,14 +383,24 @@ class Sampler:
         self._mark("resample", 0)
         if sysm.threshold > 0.0:
             gate = ws.field_ptr("resample")
-            rows = getattr(sysm.value, "resample_rows", lambda: None)()
-            sysm.resampler(sysm.resample_scheme, weight_set=ws, rng=sysm.rng_set, stream_index=n,
-                           parents=sysm.parents, rows=rows[0] if rows else None,
-                           row_bytes=rows[1] if rows else 0, gate=gate, status=ws.field_ptr("status"))
-            if not rows:
-                sysm.value.copy_inplace(sysm.parents, gate)
+            value = sysm.value
+            if getattr(value, "defer_copy", False):
+                # parent map only; the next (gathering) move applies the copy
+                value.materialize()
+                sysm.resampler(sysm.resample_scheme, weight_set=ws, rng=sysm.rng_set, stream_index=n,
+                               parents=sysm.parents, gate=gate, status=ws.field_ptr("status"))
+                value.pending = (sysm.parents, gate)
+            else:
+                rows = getattr(value, "resample_rows", lambda: None)()
+                sysm.resampler(sysm.resample_scheme, weight_set=ws, rng=sysm.rng_set, stream_index=n,
+                               parents=sysm.parents, rows=rows[0] if rows else None,
+                               row_bytes=rows[1] if rows else 0, gate=gate, status=ws.field_ptr("status"))
+                if not rows:
+                    value.copy_inplace(sysm.parents, gate)
             ws.set_equal_weight_if(gate)
         self._mark("resample", 1)
+        if self.mcmc_queue and hasattr(sysm.value, "materialize"):
+            sysm.value.materialize()  # mcmc kernels update the state in place
         for op in self.mcmc_queue:
             accs.append(apply_move(op, sysm, t))
         for k, a in enumerate(accs):

@@ -67,8 +67,13 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // MON: also reduce the "pos" monitor of the INCOMING state, sum_i W_{t-1,i} (x_i, y_i) -- the
 // previous iteration's estimate (evaluated after its resample) --
 // from the registers the move already holds: the monitor costs no extra HBM pass.
+// GATHER: the previous resample's copy is folded in -- row i is read from
+// x_in[parents[i]] (when the device gate says the resample ran) and written to
+// x_out[i], a second buffer: the "simultaneous" copy of SPEC.md:343 for free.
 template <bool MON>
-__global__ void __launch_bounds__(PB, 4) k_pf_move(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
+__global__ void __launch_bounds__(PB, 4) k_pf_move(const double *x_in, double *x_out,
+                                                   const int32_t *__restrict__ parents, const int32_t *gate,
+                                                   double *__restrict__ lw_raw, int64_t n,
                                                    Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
@@ -79,8 +84,9 @@ __global__ void __launch_bounds__(PB, 4) k_pf_move(double *__restrict__ x, doubl
     if (i < n) {
         const NormLw nl = norm_of(st);
         const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
+        const int64_t src = (parents && (gate == nullptr || *gate != 0)) ? (int64_t)__ldg(parents + i) : i;
         double x0, x1, x2, x3;
-        ld_row(x + 4 * i, x0, x1, x2, x3);
+        ld_row(x_in + 4 * src, x0, x1, x2, x3);
         if (MON) {
             const double w = nl.eq ? 1.0 / (double)n : exp(prev);
             h0 = w * x0;
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(PB, 4) k_pf_move(double *__restrict__ x, doubl
         x2 = x2 + (0.0 + k.sd_vel * normal_at(c + 4, si, key));
         x3 = x3 + (0.0 + k.sd_vel * normal_at(c + 6, si, key));
         ctrs[i] = c + 8;
-        st_row(x + 4 * i, x0, x1, x2, x3);
+        st_row(x_out + 4 * i, x0, x1, x2, x3);
         const double incw = cv_llh(x0, x1, obs[0], obs[1]);
         if (incw_out) incw_out[i] = incw;
         v = prev + incw;  // add_log_weight(incw)
@@ -167,12 +173,16 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, 
     return smc_check_launch("smc_pf_init");
 }
 
-extern "C" int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                           smc_wstate *st, double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes,
-                           void *stream)
+extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
+                           int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t, smc_wstate *st,
+                           double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes, void *stream)
 {
     int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_move");
     if (rc) return rc;
+    if (!x_in) x_in = x;
+    if ((uintptr_t)x_in & 31) return smc_set_error(SMC_EINVAL, "smc_pf_move: x_in must be 32-byte aligned");
+    if (parents && x_in == x)
+        return smc_set_error(SMC_EINVAL, "smc_pf_move: a gathering move needs distinct in/out state buffers");
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
@@ -180,11 +190,12 @@ extern "C" int smc_pf_move(double *x, double *lw_raw, int64_t n, uint64_t seed, 
     void *scratch = pf_scratch(ws, nb);
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
     if (monitor_prev) {
-        k_pf_move<true><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts, mon);
+        k_pf_move<true><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, key, ctrs, obs_t, pf_constants(), st,
+                                          incw_out, parts, mon);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev);
     } else {
-        k_pf_move<false><<<nb, PB, 0, s>>>(x, lw_raw, n, key, ctrs, obs_t, pf_constants(), st, incw_out, parts,
-                                           nullptr);
+        k_pf_move<false><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, key, ctrs, obs_t, pf_constants(), st,
+                                           incw_out, parts, nullptr);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch);
     }
     return smc_check_launch("smc_pf_move");

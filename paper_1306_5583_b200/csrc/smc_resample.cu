@@ -760,6 +760,29 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     }
 }
 
+// In-place copy of every zero-count row from its parent.
+// Sources (count >= 2) and destinations (count 0) are disjoint, so
+// no snapshot is needed.  One slot per thread keeps occupancy (and so the
+// number of 32-byte row loads in flight) at the maximum.
+constexpr int CB = 512;
+template <int RB>
+__global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
+                                                int64_t n, Layout L)
+{
+    if (!L.hdr->active || L.hdr->trivial) return;
+    const int64_t j = (int64_t)blockIdx.x * CB + threadIdx.x;
+    if (j >= n) return;
+    const int32_t p = __ldg(parents + j);
+    if (p == j) return;
+    if (RB == 32) {
+        double4 v;
+        ld256((const double *)(rows + (int64_t)p * 32), v);
+        st256((double *)(rows + j * 32), v);
+    } else {
+        copy_row(rows, row_bytes, j, p);
+    }
+}
+
 __global__ void k_rs_reset(int64_t n, int64_t nt, Layout L)
 {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nt; b += (int64_t)gridDim.x * blockDim.x)
@@ -850,7 +873,13 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (parents) {
         const int64_t nt2 = (n + TILE2 - 1) / TILE2;
         k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
-        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, (char *)rows, row_bytes, L);
+        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, nullptr, 0, L);
+        if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
+            if (row_bytes == 32)
+                k_rs_copy<32><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, 32, n, L);
+            else
+                k_rs_copy<0><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, row_bytes, n, L);
+        }
     }
     return smc_check_launch("smc_resample");
 }

@@ -37,6 +37,10 @@ DATA_NUM = 100
 class CVState(StateMatrix):
     """StateMatrix<RowMajor, 4, double> + the observations."""
 
+    # cv_move gathers x_in[parents[i]] into the second buffer, so a resample only
+    # builds the parent map and never copies rows itself (see smc_pf_move).
+    defer_copy = True
+
     def __init__(self, size, device="cuda"):
         super().__init__(size, 4, ROW_MAJOR, device)
         self.obs = None  # (T, 2) float64 on the device
@@ -73,7 +77,8 @@ def cv_init(system, param=None):
     n = system.size
     ws, nb = _ws(system, n)
     w = system.weight_set
-    _abi.call("smc_pf_init", _abi.ptr(v.data), _abi.ptr(w.lw_raw), n, system.rng_set.seed,
+    v.pending = None  # the prior draw overwrites every row
+    _abi.call("smc_pf_init", _abi.ptr(v.raw), _abi.ptr(w.lw_raw), n, system.rng_set.seed,
               _abi.ptr(system.rng_set.counters), v.obs_ptr(0), w.state_ptr, ws, nb, _abi.stream())
     return None  # acceptance "bares no meaning"
 
@@ -85,8 +90,15 @@ def _cv_move_kernel(iter_, system):
     w = system.weight_set
     # a pending fused "pos" monitor of the previous iteration is reduced by this launch
     mon = system.take_pending_monitor("pos")
-    _abi.call("smc_pf_move", _abi.ptr(v.data), _abi.ptr(w.lw_raw), n, system.rng_set.seed,
-              _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_), w.state_ptr, None, mon, ws, nb, _abi.stream())
+    common = (_abi.ptr(w.lw_raw), n, system.rng_set.seed, _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_),
+              w.state_ptr, None, mon, ws, nb, _abi.stream())
+    if v.pending is not None:  # fold the last resample's copy into this move (double buffer)
+        parents, gate = v.pending
+        v.pending = None
+        _abi.call("smc_pf_move", _abi.ptr(v.raw), _abi.ptr(v.alt()), _abi.ptr(parents), gate, *common)
+        v.swap()
+    else:
+        _abi.call("smc_pf_move", None, _abi.ptr(v.raw), None, None, *common)
     return None
 
 

@@ -124,8 +124,11 @@ def test_pf_full_run_matches_oracle(scheme):
     s.initialize(obs)
     s.iterate(99)
     h = s.history()
-    ref = O.pf_run(n, 1306, scheme, 0.5, obs)
+    ref, xref, lwref = O.pf_run(n, 1306, scheme, 0.5, obs, want_state=True)
     assert np.array_equal(h["resampled"], ref[:, 1])
+    # final state (the deferred resample copy is materialized on read) and log-weights
+    np.testing.assert_allclose(s.system.value.data.cpu().numpy(), xref, rtol=1e-8, atol=1e-9)
+    np.testing.assert_allclose(s.system.weight_set.read_log_weight().cpu().numpy(), lwref, rtol=1e-8, atol=1e-9)
     np.testing.assert_allclose(h["ess_over_n"], ref[:, 0], rtol=RTOL)
     np.testing.assert_allclose(h["pos.0"], ref[:, 2], rtol=RTOL, atol=1e-9)
     np.testing.assert_allclose(h["pos.1"], ref[:, 3], rtol=RTOL, atol=1e-9)
