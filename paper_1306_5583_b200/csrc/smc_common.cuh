@@ -167,6 +167,43 @@ SMC_DEV T block_exclusive_sum(T v, T *sm, T *total)
     return ex;
 }
 
+// Coalesced tile I/O.  Lanes of a warp touch contiguous addresses (one 128-byte
+// line per 32 x 4 B); the tile is transposed through shared memory so each
+// thread owns ITEMS consecutive items ("blocked" order, what scans need).  One
+// pad word per 128 B of shared memory keeps both phases bank-conflict free.
+template <typename T>
+SMC_DEV int tpad(int i) { return i + i / (128 / (int)sizeof(T)); }
+template <typename T, int NT, int ITEMS>
+constexpr int tile_smem_elems() { return NT * ITEMS + NT * ITEMS / (128 / (int)sizeof(T)) + 1; }
+
+template <int NT, int ITEMS, typename T>
+SMC_DEV void load_blocked(const T *__restrict__ g, int64_t base, int64_t n, T (&v)[ITEMS], T *sm, T pad)
+{
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const int li = j * NT + threadIdx.x;
+        sm[tpad<T>(li)] = base + li < n ? g[base + li] : pad;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) v[j] = sm[tpad<T>(threadIdx.x * ITEMS + j)];
+    __syncthreads();
+}
+
+template <int NT, int ITEMS, typename T>
+SMC_DEV void store_blocked(T *__restrict__ g, int64_t base, int64_t n, const T (&v)[ITEMS], T *sm)
+{
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) sm[tpad<T>(threadIdx.x * ITEMS + j)] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+        const int li = j * NT + threadIdx.x;
+        if (base + li < n) g[base + li] = sm[tpad<T>(li)];
+    }
+    __syncthreads();
+}
+
 // u128 has no shuffle; split in halves.
 SMC_DEV u128 shfl_xor_u128(u128 v, int o)
 {

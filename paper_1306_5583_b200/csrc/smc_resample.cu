@@ -224,15 +224,11 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         return;
     }
     const bool residual = is_residual(scheme);
-    // each thread a contiguous chunk of tiles (deterministic), then a shuffle tree
-    const int64_t per = (nt + SB - 1) / SB;
-    const int64_t b0 = threadIdx.x * per < nt ? threadIdx.x * per : nt;
-    const int64_t b1 = b0 + per < nt ? b0 + per : nt;
+    // totals: striped, so every warp load is coalesced (integer sums are order independent)
     u128 tq = 0;
     uint64_t tqr = 0;
     int64_t tf = 0;
-#pragma unroll 8
-    for (int64_t b = b0; b < b1; ++b) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
+    for (int64_t b = threadIdx.x; b < nt; b += SB) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         tq += shfl_xor_u128(tq, o);
@@ -282,15 +278,31 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     }
     __syncthreads();
     if (!s_ok) return;
-    // exclusive prefix of the searched per-tile totals (all < 2^64 once T is validated)
-    uint64_t mine = 0;
-#pragma unroll 8
-    for (int64_t b = b0; b < b1; ++b) mine += residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b];
-    uint64_t tot;
-    uint64_t run = block_exclusive_sum<SB, uint64_t>(mine, sm64, &tot);
-    for (int64_t b = b0; b < b1; ++b) {
-        L.tile_pre[b] = run;
-        run += residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b];
+    // exclusive prefix of the searched per-tile totals (all < 2^64 once T is validated):
+    // warp w owns a contiguous chunk; its lanes read consecutive tiles (coalesced) and
+    // scan them 32 at a time with a running carry, offset by the warps before it.
+    constexpr int NW = SB / 32;
+    const int64_t C = (nt + NW - 1) / NW;
+    const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
+    auto val = [&](int64_t b) { return residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b]; };
+    uint64_t wsum = 0;
+    for (int64_t b = w0 + lane; b < w1; b += 32) wsum += val(b);
+    wsum = warp_sum(wsum);
+    if (lane == 0) sm64[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t x = sm64[lane];
+        const uint64_t inc = warp_inclusive_sum(x);
+        sm64[lane] = inc - x;
+    }
+    __syncthreads();
+    uint64_t carry = sm64[warp];
+    for (int64_t b0 = w0; b0 < w1; b0 += 32) {
+        const int64_t b = b0 + lane;
+        const uint64_t v = b < w1 ? val(b) : 0;
+        const uint64_t inc = warp_inclusive_sum(v);
+        if (b < w1) L.tile_pre[b] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
 }
 
@@ -412,8 +424,8 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
     RsHeader *h = L.hdr;
     if (!h->active) return;
     __shared__ uint64_t sm[RT / 32 + 1];
-    __shared__ uint64_t s_q[TILE + TILE / 16];
-    __shared__ int32_t s_fb[TILE + TILE / 16];
+    __shared__ uint64_t s_q[tile_smem_elems<uint64_t, RT, RI>()];
+    __shared__ int32_t s_fb[tile_smem_elems<uint64_t, RT, RI>()];
     if (h->trivial) {  // N == 1: no-op resample
         if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)m_out;
         return;
@@ -430,17 +442,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
         if (!residual) {
             // q_i was materialized by pass A: no exp / quantization here, 64 contiguous bytes per thread
             if (!is_multinomial(scheme)) {
-                if (base + RI <= n) {
-#pragma unroll
-                    for (int v = 0; v < RI / 2; ++v) {
-                        const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2 *>(L.qfull + base) + v);
-                        q[2 * v] = a.x;
-                        q[2 * v + 1] = a.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < RI; ++j) q[j] = base + j < n ? __ldcg(L.qfull + base + j) : 0;
-                }
+                load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, q, s_q, 0ull);  // coalesced
             } else {
 #pragma unroll
                 for (int j = 0; j < RI; ++j) q[j] = 0;  // multinomial: counts come from the histogram
@@ -505,14 +507,8 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
             }
         }
     }
-    if (base + RI <= n) {
-        reinterpret_cast<int4 *>(counts + base)[0] = make_int4(c[0], c[1], c[2], c[3]);
-        reinterpret_cast<int4 *>(counts + base)[1] = make_int4(c[4], c[5], c[6], c[7]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < RI; ++j)
-            if (base + j < n) counts[base + j] = c[j];
-    }
+    __syncthreads();  // s_fb may still be read by the residual staging path
+    store_blocked<RT, RI, int32_t>(counts, tbase, n, c, s_fb);  // coalesced
 }
 
 // Pass B2: replication_to_parents' rank scan.  A cheap tile
@@ -534,17 +530,9 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     const int64_t b = s_tile;
     const int64_t base = b * TILE2 + (int64_t)threadIdx.x * RI2;
     int32_t c[RI2];
-    if (base + RI2 <= n) {
-#pragma unroll
-        for (int v = 0; v < RI2 / 8; ++v) {
-            const int4 *p = reinterpret_cast<const int4 *>(cin + base) + 2 * v;
-            const int4 a = p[0], d = p[1];
-            c[8 * v] = a.x; c[8 * v + 1] = a.y; c[8 * v + 2] = a.z; c[8 * v + 3] = a.w;
-            c[8 * v + 4] = d.x; c[8 * v + 5] = d.y; c[8 * v + 6] = d.z; c[8 * v + 7] = d.w;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < RI2; ++j) c[j] = base + j < n ? cin[base + j] : 1;  // padding: not zero, no surplus
+    {
+        __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI2>()];
+        load_blocked<RT, RI2, int32_t>(cin, b * TILE2, n, c, s_c, 1);  // coalesced; pad: not zero, no surplus
     }
     bool bad = false;
 #pragma unroll
@@ -673,8 +661,7 @@ SMC_DEV void copy_row(char *rows, int64_t row_bytes, int64_t dst, int64_t srcr)
 constexpr int CSTAGE = TILE + 2 * ANCHOR + 2;
 
 __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
-                                                  int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
-                                                  Layout L)
+                                                  int32_t *__restrict__ parents, Layout L)
 {
     const RsHeader *h = L.hdr;
     if (!h->active) return;
@@ -683,25 +670,18 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
         return;
     }
     __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
+    __shared__ int32_t s_io[tile_smem_elems<int32_t, RT, RI>()];
     __shared__ uint32_t sm32[RT / 32 + 1];
     const int64_t t = blockIdx.x;
-    const int64_t base = t * TILE + (int64_t)threadIdx.x * RI;
+    const int64_t tbase = t * TILE;
+    const int64_t base = tbase + (int64_t)threadIdx.x * RI;
     const uint32_t z0 = (uint32_t)__ldcg(&L.tile_z0[t]), z1 = (uint32_t)__ldcg(&L.tile_z0[t + 1]);
     const uint32_t Z = h->Z_total, P = h->P_total;
     int32_t c[RI];
-    if (base + RI <= n) {
-        const int4 *p = reinterpret_cast<const int4 *>(cin + base);
-        const int4 a = p[0], d = p[1];
-        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = d.x; c[5] = d.y; c[6] = d.z; c[7] = d.w;
-    } else {
-#pragma unroll
-        for (int j = 0; j < RI; ++j) c[j] = base + j < n ? cin[base + j] : 1;
-    }
+    load_blocked<RT, RI, int32_t>(cin, tbase, n, c, s_io, 1);  // coalesced
     uint32_t nz = 0;
 #pragma unroll
     for (int j = 0; j < RI; ++j) nz += (c[j] == 0);
-    uint32_t tot;
-    const uint32_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first zero rank of this thread
     uint32_t cnt = 0;
     if (z1 > z0) {
         // surplus parents covering ranks [z0, z1): between the anchors around z0 and z1-1
@@ -714,7 +694,8 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
             s_idx[k] = __ldcg(&L.sp_idx[a0 + k]);
         }
     }
-    __syncthreads();
+    uint32_t tot;
+    const uint32_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first zero rank of this thread
     int32_t par[RI];
     uint32_t lo = 0;
     if (nz) {  // last k with s_start[k] <= zr, then a forward merge walk
@@ -734,30 +715,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
             ++r;
         }
     }
-    if (base + RI <= n) {
-        int4 *p = reinterpret_cast<int4 *>(parents + base);
-        p[0] = make_int4(par[0], par[1], par[2], par[3]);
-        p[1] = make_int4(par[4], par[5], par[6], par[7]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < RI; ++j)
-            if (base + j < n) parents[base + j] = par[j];
-    }
-    if (rows && nz) {
-        if (row_bytes == 32) {
-            double4 v[RI];
-#pragma unroll
-            for (int j = 0; j < RI; ++j)
-                if (c[j] == 0 && base + j < n) ld256((const double *)(rows + (int64_t)par[j] * 32), v[j]);  // in flight
-#pragma unroll
-            for (int j = 0; j < RI; ++j)
-                if (c[j] == 0 && base + j < n) st256((double *)(rows + (base + j) * 32), v[j]);
-        } else {
-#pragma unroll
-            for (int j = 0; j < RI; ++j)
-                if (c[j] == 0 && base + j < n) copy_row(rows, row_bytes, base + j, par[j]);
-        }
-    }
+    store_blocked<RT, RI, int32_t>(parents, tbase, n, par, s_io);  // coalesced
 }
 
 // In-place copy of every zero-count row from its parent.
@@ -873,7 +831,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (parents) {
         const int64_t nt2 = (n + TILE2 - 1) / TILE2;
         k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
-        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, nullptr, 0, L);
+        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
                 k_rs_copy<32><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, 32, n, L);
@@ -898,7 +856,7 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
     const int64_t nt2 = (n + TILE2 - 1) / TILE2;
     k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, status, L);
-    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, nullptr, 0, L);
+    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
