@@ -90,6 +90,7 @@ typedef struct smc_wstate {
     double log_zconst; /* running NormalizingConstant         */
     double max_raw;    /* max_i lw_raw_i                                        */
     double log_sum;    /* log sum_i exp(lw_raw_i - max_raw); lse = max + this   */
+    double w_equal;    /* 1/N after set_equal_weight (N global when sharded)    */
     int32_t equal;     /* 1 after set_equal_weight                              */
     int32_t status;    /* sticky device error (SMC_E*), 0 when healthy          */
     int32_t resample;  /* decision of the last smc_ess_decide     */
@@ -112,6 +113,13 @@ int smc_weights_update(int mode, double *lw_raw, const double *values, int64_t n
 /* set_equal_weight gated by a device flag (skipped when
  * gate != NULL and *gate == 0): the post-resample reset of the sampler loop. */
 int smc_weights_set_equal(smc_wstate *ws_state, int64_t n, const int32_t *gate, void *stream);
+/* Multi-GPU normalization: combine G shard partials (SMC_PARTIAL_STRIDE
+ * doubles each: max, sum e, sum e^2, monitor0, monitor1, pad) in rank order, so
+ * every rank holds bit-identical global weight state; n_total is the global
+ * particle count; monitor_out (2 doubles, may be NULL) gets the summed monitor. */
+#define SMC_PARTIAL_STRIDE 8
+int smc_weights_combine(const double *partials, int G, smc_wstate *ws_state, int64_t n_total, int mode,
+                        int accumulate_nc, double *monitor_out, void *stream);
 /* read_log_weight / read_weight: the normalized log-weight or its exp */
 int smc_weights_read(int what, const double *lw_raw, const smc_wstate *ws_state, int64_t n, double *out,
                      void *stream);
@@ -164,6 +172,39 @@ int smc_resample(int scheme, const double *w, const double *lw_raw, const smc_ws
 #define SMC_DEBUG_FORCE_EXACT_F 1
 int smc_debug_set(int key, int value);
 
+/* Sharded resampling over G GPUs (this shard holds particles [base, base+n)
+ * of n_total; weights normalized globally, e.g. by smc_weights_combine).  The
+ * counts and the global parent pairing are bit-identical to one GPU:
+ *  1. smc_resample_shard_totals -> totals_out[4] = {T lo, T hi, sum f, T'};
+ *     the host allgathers them into totals_all[G*4];
+ *  2. smc_resample_shard_counts -> counts of the local particles (global CDF
+ *     offset = exact integer prefix of the shards before), the local rank scan,
+ *     zsp_out[4] = {zero slots Z, surplus children S, surplus parents P, active};
+ *     the host allgathers zsp and plans the exchange: global zero rank r pairs
+ *     with global surplus rank r; shard g owns zero ranks [Zoff_g, Zoff_g+Z_g)
+ *     and surplus ranks [Soff_g, Soff_g+S_g);
+ *  3. smc_resample_shard_pack -> rows of the local surplus children with local
+ *     surplus ranks [ranges[2r], ranges[2r] + ranges[2r+1]) (host array, K <= 64),
+ *     back to back, for ncclSend;
+ *  4. smc_resample_shard_assign -> the local parent map; zero slots paired
+ *     with a remote surplus child copy their row from `recv` (rows ordered by
+ *     global rank, the shard's own range [soff, soff+s_self) excluded) and
+ *     keep parents[j] = j; local pairs get the local parent index. */
+int smc_resample_shard_totals(int scheme, const double *w, const double *lw_raw, const smc_wstate *ws_state,
+                              int64_t n, int64_t n_total, int64_t m_total, const double *u, int64_t n_u,
+                              const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes, uint64_t *totals_out,
+                              void *stream);
+int smc_resample_shard_counts(int scheme, const double *w, const double *lw_raw, const smc_wstate *ws_state,
+                              int64_t n, int64_t n_total, int64_t m_total, int G, int rank,
+                              const uint64_t *totals_all, uint64_t seed, uint64_t stream_index, uint64_t *ctr,
+                              const double *u, int64_t n_u, int32_t *counts, const int32_t *gate, int32_t *status,
+                              void *ws, size_t ws_bytes, uint32_t *zsp_out, void *stream);
+int smc_resample_shard_pack(const void *rows, int64_t row_bytes, const int64_t *ranges, int K, void *sendbuf, void *ws,
+                            size_t ws_bytes, void *stream);
+int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64_t zoff, int64_t soff, int64_t s_self,
+                              const void *recv, void *rows, int64_t row_bytes, int32_t *parents, void *ws,
+                              size_t ws_bytes, void *stream);
+
 /* replication_to_parents(counts) from a device counts vector. */
 int smc_replication_to_parents(const int32_t *counts, int64_t n, int32_t *parents, int32_t *status, void *ws,
                                size_t ws_bytes, void *stream);
@@ -185,14 +226,21 @@ size_t smc_pf_workspace_bytes(int64_t n);
 /* X (n x 4 row-major f64) ~ prior from streams 0..n-1 (draw order x,y,vx,vy),
  * llh at obs_t = (x_obs, y_obs) (device, 2 doubles) -> set_log_weight; the
  * state's log_zconst restarts at log (1/N) sum exp(llh). */
-int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                smc_wstate *ws_state, void *ws, size_t ws_bytes, void *stream);
+int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+                const double *obs_t, smc_wstate *ws_state, double *partial_out, void *ws, size_t ws_bytes,
+                void *stream);
+/* Sharded systems (particles [stream_base, stream_base + n) of N_total on
+ * this GPU): the Philox stream of local particle i is stream_base + i, and
+ * with partial_out != NULL the normalization is NOT applied locally -- the
+ * shard's {max, sum e, sum e^2, mon0, mon1} (SMC_PARTIAL_STRIDE doubles) is
+ * written there for the ranks to allgather and smc_weights_combine. */
 /* cv_move on every particle + incw = llh(t) -> add_log_weight(incw) fused in
  * one pass over the state; log_zconst += log sum W_{t-1} exp(incw).
  * incw_out may be NULL. */
 int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
-                int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t, smc_wstate *ws_state,
-                double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes, void *stream);
+                int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed, uint64_t *ctrs,
+                const double *obs_t, smc_wstate *ws_state, double *incw_out, double *monitor_prev,
+                double *partial_out, void *ws, size_t ws_bytes, void *stream);
 /* x_in / parents / gate fold the previous resample's copy into the move: row i
  * is read from x_in[parents[i]] (x_in[i] when parents is NULL or *gate == 0)
  * and written to x[i] -- copy_particles' simultaneous semantics

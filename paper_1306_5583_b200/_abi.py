@@ -44,7 +44,8 @@ class SmcWState(C.Structure):
 
     _fields_ = [
         ("lse", C.c_double), ("ess", C.c_double), ("ess_over_n", C.c_double), ("nc_inc", C.c_double),
-        ("log_zconst", C.c_double), ("max_raw", C.c_double), ("log_sum", C.c_double), ("equal", C.c_int32), ("status", C.c_int32),
+        ("log_zconst", C.c_double), ("max_raw", C.c_double), ("log_sum", C.c_double), ("w_equal", C.c_double),
+        ("equal", C.c_int32), ("status", C.c_int32),
         ("resample", C.c_int32), ("iter", C.c_int32),
     ]
 
@@ -71,12 +72,20 @@ _SIGS = {
     "smc_resample": ([_i32, _vp, _vp, _vp, _i64, _i64, _u64, _u64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
                       _vp, _vp, _sz, _vp], C.c_int),
     "smc_debug_set": ([C.c_int, C.c_int], C.c_int),
+    "smc_weights_combine": ([_vp, _i32, _vp, _i64, _i32, _i32, _vp, _vp], C.c_int),
+    "smc_resample_shard_totals": ([_i32, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp],
+                                  C.c_int),
+    "smc_resample_shard_counts": ([_i32, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp, _u64, _u64, _vp, _vp,
+                                   _i64, _vp, _vp, _vp, _vp, _sz, _vp, _vp], C.c_int),
+    "smc_resample_shard_pack": ([_vp, _i64, _vp, _i32, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_resample_shard_assign": ([_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp], C.c_int),
     "smc_replication_to_parents": ([_vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gather_rows": ([_vp, _vp, _i64, _vp, _i64, _vp], C.c_int),
     "smc_copy_rows_inplace": ([_vp, _i64, _vp, _i64, _vp, _vp], C.c_int),
     "smc_pf_workspace_bytes": ([_i64], _sz),
-    "smc_pf_init": ([_vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
-    "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_pf_init": ([_vp, _vp, _i64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
+                    C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 

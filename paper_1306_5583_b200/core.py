@@ -167,9 +167,14 @@ class StateMatrix:
 class ParticleSystem:
     """value + WeightSet + RngStreamSet(N + 1) + resampling policy."""
 
-    def __init__(self, value, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, device="cuda"):
+    def __init__(self, value, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, device="cuda",
+                 shard=None):
         self.value = value
         self.size = int(size)
+        # shard: dist.Shard when this system is one rank's slice of a multi-GPU system
+        self.shard = shard
+        self.n_total = shard.n_total if shard is not None else self.size
+        self.stream_base = shard.base if shard is not None else 0
         self.device = torch.device(device)
         self.weight_set = WeightSet(self.size, self.device, check=False)
         self.rng_set = RngStreamSet(self.size + 1, seed, self.device)
@@ -246,7 +251,8 @@ class Sampler:
     value collection defaults to an N x 1 StateMatrix.
     """
 
-    def __init__(self, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, value=None, device="cuda"):
+    def __init__(self, size, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0, value=None, device="cuda",
+                 shard=None):
         size = int(size)
         if size < 1:
             raise ValueError("sampler needs N >= 1")  # SPEC.md:292
@@ -254,7 +260,9 @@ class Sampler:
         self.device = torch.device(device)
         if value is None:
             value = StateMatrix(size, 1, device=self.device)
-        self.system = ParticleSystem(value, size, scheme, threshold, seed, self.device)
+        if shard is not None and not getattr(value, "defer_copy", False):
+            raise ValueError("a sharded sampler needs a value collection whose move gathers (defer_copy)")
+        self.system = ParticleSystem(value, size, scheme, threshold, seed, self.device, shard)
         self.init_op = None
         self.move_queue = []
         self.mcmc_queue = []
@@ -349,7 +357,7 @@ class Sampler:
         self._rows = 0
         self._path_grid = []
         sysm = self.system
-        sysm.weight_set.set_equal_weight()
+        sysm.weight_set.set_equal_weight_if(None, sysm.n_total)
         row = self._row(0)
         acc = self.init_op(sysm, param) if not isinstance(self.init_op, ParticleKernelOp) \
             else apply_move(self.init_op, sysm, 0)
@@ -379,12 +387,20 @@ class Sampler:
         n = sysm.size
         hist_ptr = ctypes.c_void_p(row.data_ptr())
         # ESS trigger (F11: also after init)
-        _abi.call("smc_ess_decide", ws.state_ptr, n, sysm.threshold, hist_ptr, _abi.stream())
+        _abi.call("smc_ess_decide", ws.state_ptr, sysm.n_total, sysm.threshold, hist_ptr, _abi.stream())
         self._mark("resample", 0)
         if sysm.threshold > 0.0:
             gate = ws.field_ptr("resample")
             value = sysm.value
-            if getattr(value, "defer_copy", False):
+            if sysm.shard is not None:
+                # global resample across the ranks: counts bit-identical to one GPU,
+                # cross-rank surplus rows arrive in place, local pairs gathered by the next move
+                value.materialize()
+                rows = ctypes.c_void_p(value.raw.data_ptr())
+                sysm.shard.resample(sysm, sysm.resample_scheme, gate, ws.field_ptr("status"), rows,
+                                    8 * value.dim)
+                value.pending = (sysm.parents, gate)
+            elif getattr(value, "defer_copy", False):
                 # parent map only; the next (gathering) move applies the copy
                 value.materialize()
                 sysm.resampler(sysm.resample_scheme, weight_set=ws, rng=sysm.rng_set, stream_index=n,
@@ -397,7 +413,7 @@ class Sampler:
                                row_bytes=rows[1] if rows else 0, gate=gate, status=ws.field_ptr("status"))
                 if not rows:
                     value.copy_inplace(sysm.parents, gate)
-            ws.set_equal_weight_if(gate)
+            ws.set_equal_weight_if(gate, sysm.n_total)
         self._mark("resample", 1)
         if self.mcmc_queue and hasattr(sysm.value, "materialize"):
             sysm.value.materialize()  # mcmc kernels update the state in place
@@ -454,9 +470,21 @@ class Sampler:
         ws = self.system.weight_set
         n = self.system.size
         buf, nb = self._ws.get(_abi.lib().smc_weighted_reduce_workspace_bytes(n, m))
-        out = ctypes.c_void_p(row.data_ptr() + 8 * col)
-        _abi.call("smc_weighted_reduce", _abi.ptr(vals), ld, m, _abi.ptr(ws.lw_raw), ws.state_ptr, n, out, buf, nb,
-                  _abi.stream())
+        shard = self.system.shard
+        if shard is None:
+            out = ctypes.c_void_p(row.data_ptr() + 8 * col)
+            _abi.call("smc_weighted_reduce", _abi.ptr(vals), ld, m, _abi.ptr(ws.lw_raw), ws.state_ptr, n, out, buf,
+                      nb, _abi.stream())
+            return
+        # shard: local weighted sums, allgathered and added in rank order (deterministic)
+        loc = torch.empty(m, dtype=torch.float64, device=self.device)
+        _abi.call("smc_weighted_reduce", _abi.ptr(vals), ld, m, _abi.ptr(ws.lw_raw), ws.state_ptr, n,
+                  _abi.ptr(loc), buf, nb, _abi.stream())
+        allp = shard.comm.allgather(loc)
+        acc = allp[0].clone()
+        for g in range(1, shard.world):
+            acc += allp[g]
+        row[col:col + m].copy_(acc)
 
     def check(self):
         """Synchronize and raise any device-side failure (SPEC.md:315 'propagates')."""

@@ -101,10 +101,14 @@ SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, Key key, double shape)
 struct NormLw {
     double m, ls;
     bool eq;
+    double weq;  // the equal weight 1/N (valid when eq)
     SMC_DEV double operator()(double raw) const { return eq ? -ls : (raw - m) - ls; }
     SMC_DEV bool needs_raw() const { return !eq; }
 };
-SMC_DEV NormLw norm_of(const smc_wstate *st) { return NormLw{st->max_raw, st->log_sum, st->equal != 0}; }
+SMC_DEV NormLw norm_of(const smc_wstate *st)
+{
+    return NormLw{st->max_raw, st->log_sum, st->equal != 0, st->w_equal};
+}
 
 // ---------------------------------------------------------------------------
 // Device status: first error wins ("first failing ... reported").

@@ -42,13 +42,14 @@ SMC_DEV void st_row(double *p, double a, double b, double c, double d)
 }
 
 __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
-                                                Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                uint64_t sbase, Key key, uint64_t *__restrict__ ctrs,
+                                                const double *__restrict__ obs,
                                                 PfConst k, smc_wstate *st, LsePartial *__restrict__ parts)
 {
     const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
     double v = -INFINITY;
     if (i < n) {
-        const uint64_t c = ctrs[i], si = (uint64_t)i;
+        const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;  // global stream index of a sharded system
         // draw order x_pos, y_pos, x_vel, y_vel; normal = mean + sd*z (rng.py:201)
         const double r0 = 0.0 + k.sd_pos0 * normal_at(c + 0, si, key);
         const double r1 = 0.0 + k.sd_pos0 * normal_at(c + 2, si, key);
@@ -73,8 +74,8 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 template <bool MON>
 __global__ void __launch_bounds__(PB, 4) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
-                                                   double *__restrict__ lw_raw, int64_t n,
-                                                   Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                   double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
+                                                   double w_equal, Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
@@ -88,11 +89,11 @@ __global__ void __launch_bounds__(PB, 4) k_pf_move(const double *x_in, double *x
         double x0, x1, x2, x3;
         ld_row(x_in + 4 * src, x0, x1, x2, x3);
         if (MON) {
-            const double w = nl.eq ? 1.0 / (double)n : exp(prev);
+            const double w = nl.eq ? w_equal : exp(prev);  // 1 / N_total after a resample
             h0 = w * x0;
             h1 = w * x1;
         }
-        const uint64_t c = ctrs[i], si = (uint64_t)i;
+        const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;
         // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
         x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
         x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
@@ -158,8 +159,9 @@ static int pf_check(double *x, double *lw_raw, int64_t n, uint64_t *ctrs, const 
     return SMC_OK;
 }
 
-extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t,
-                           smc_wstate *st, void *ws, size_t ws_bytes, void *stream)
+extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+                           const double *obs_t, smc_wstate *st, double *partial_out, void *ws, size_t ws_bytes,
+                           void *stream)
 {
     int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_init");
     if (rc) return rc;
@@ -167,15 +169,16 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t seed, 
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
     void *scratch = pf_scratch(ws, nb);
-    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
+    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, stream_base, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
                                 pf_constants(), st, parts);
-    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s, scratch);
+    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     return smc_check_launch("smc_pf_init");
 }
 
 extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
-                           int64_t n, uint64_t seed, uint64_t *ctrs, const double *obs_t, smc_wstate *st,
-                           double *incw_out, double *monitor_prev, void *ws, size_t ws_bytes, void *stream)
+                           int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed, uint64_t *ctrs,
+                           const double *obs_t, smc_wstate *st, double *incw_out, double *monitor_prev,
+                           double *partial_out, void *ws, size_t ws_bytes, void *stream)
 {
     int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_move");
     if (rc) return rc;
@@ -189,14 +192,15 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
     void *scratch = pf_scratch(ws, nb);
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
     if (monitor_prev) {
-        k_pf_move<true><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, key, ctrs, obs_t, pf_constants(), st,
-                                          incw_out, parts, mon);
-        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev);
+        k_pf_move<true><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
+                                          pf_constants(), st, incw_out, parts, mon);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev, partial_out);
     } else {
-        k_pf_move<false><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, key, ctrs, obs_t, pf_constants(), st,
-                                           incw_out, parts, nullptr);
-        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch);
+        k_pf_move<false><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
+                                           pf_constants(), st, incw_out, parts, nullptr);
+        smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     }
     return smc_check_launch("smc_pf_move");
 }

@@ -57,6 +57,7 @@ struct RsHeader {
     int32_t trivial;  // N == 1
     uint32_t tile_ctr;
     uint32_t Z_total, S_total, P_total;
+    uint64_t qoff;    // this shard's CDF offset (0 on one GPU)
 };
 
 struct Layout {
@@ -107,7 +108,7 @@ struct WSrc {
     const double *lw;  // raw log weights (w == null)
     const smc_wstate *st;
     int64_t n;
-    SMC_DEV NormLw norm() const { return w ? NormLw{0.0, 0.0, false} : norm_of(st); }
+    SMC_DEV NormLw norm() const { return w ? NormLw{0.0, 0.0, false, 0.0} : norm_of(st); }
     SMC_DEV double raw(int64_t i, const NormLw &nl) const  // the load (coalescable)
     {
         if (w) return __ldg(w + i);
@@ -116,7 +117,7 @@ struct WSrc {
     SMC_DEV double weight(double r, const NormLw &nl) const  // the math
     {
         if (w) return r;
-        return nl.eq ? 1.0 / (double)n : exp(nl(r));
+        return nl.eq ? nl.weq : exp(nl(r));
     }
 };
 
@@ -209,10 +210,50 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
 // ------------------------------------------------------------------ pass S --
 constexpr int SB = 1024;
 
+// A shard's totals {T lo, T hi, sum f, T'} for the allgather of a G-GPU resample.
+__global__ void __launch_bounds__(SB) k_rs_local_totals(int64_t nt, const int32_t *gate, Layout L, uint64_t *out)
+{
+    __shared__ u128 s_q[SB / 32];
+    __shared__ uint64_t s_qr[SB / 32];
+    __shared__ int64_t s_f[SB / 32];
+    if (gate && *gate == 0) {
+        if (threadIdx.x == 0) { out[0] = out[1] = out[2] = out[3] = 0; }
+        return;
+    }
+    u128 tq = 0;
+    uint64_t tqr = 0;
+    int64_t tf = 0;
+    for (int64_t b = threadIdx.x; b < nt; b += SB) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tq += shfl_xor_u128(tq, o);
+        tqr += __shfl_xor_sync(0xffffffffu, tqr, o);
+        tf += __shfl_xor_sync(0xffffffffu, tf, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_q[warp] = tq; s_qr[warp] = tqr; s_f[warp] = tf; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u128 T = 0;
+        uint64_t Tr = 0;
+        int64_t F = 0;
+        for (int w = 0; w < SB / 32; ++w) { T += s_q[w]; Tr += s_qr[w]; F += s_f[w]; }
+        out[0] = (uint64_t)T;
+        out[1] = (uint64_t)(T >> 64);
+        out[2] = (uint64_t)F;
+        out[3] = Tr;
+    }
+}
+
+// totals_all != NULL: a shard of a G-GPU system -- the global T / sum f / T'
+// come from the allgathered per-shard totals (4 u64 each: T lo, T hi, sum f, T'),
+// and this shard's CDF starts at the exact integer offset of the shards before it.
 __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t nt, uint64_t m_out, Key key,
                                                 uint64_t stream, uint64_t *ctr, const double *__restrict__ u,
-                                                int64_t n_u, const int32_t *gate, int32_t *status, Layout L)
+                                                int64_t n_u, const int32_t *gate, int32_t *status, Layout L,
+                                                const uint64_t *totals_all, int G, int rank, int64_t n_total)
 {
+    __shared__ uint64_t s_off;
     __shared__ uint64_t sm64[SB / 32 + 1];
     __shared__ u128 s_q[SB / 32];
     __shared__ uint64_t s_qr[SB / 32];
@@ -243,18 +284,32 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         uint64_t Tr = 0;
         int64_t F = 0;
         for (int w = 0; w < SB / 32; ++w) { T += s_q[w]; Tr += s_qr[w]; F += s_f[w]; }
+        uint64_t off = 0;
+        if (totals_all) {
+            T = 0; Tr = 0; F = 0;
+            for (int g = 0; g < G; ++g) {
+                const uint64_t *t4 = totals_all + 4 * g;
+                const u128 Tg = ((u128)t4[1] << 64) | t4[0];
+                if (g < rank) off += residual ? t4[3] : t4[0];
+                T += Tg;
+                F += (int64_t)t4[2];
+                Tr += t4[3];
+            }
+        }
+        s_off = off;
+        h->qoff = off;
         int ok = (status == nullptr || *status == 0);
         if (T < (u128)T_LO || T > (u128)T_HI) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
         int64_t M = (int64_t)m_out;
         uint64_t Tm = (uint64_t)T;
-        if (ok && residual && n > 1) {
+        if (ok && residual && n_total > 1) {
             M = (int64_t)m_out - F;
             if (M < 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
             if (M > 0 && Tr == 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
             Tm = Tr;
         }
         int64_t draws = 0;
-        if (n > 1 && M > 0) draws = is_systematic(scheme) ? 1 : M;
+        if (n_total > 1 && M > 0) draws = is_systematic(scheme) ? 1 : M;
         if (ok && u && n_u < draws) { raise_status(status, SMC_EUNIFORMS); ok = 0; }
         h->T = (uint64_t)T;
         h->Tm = Tm;
@@ -263,7 +318,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         // |fl(X) fl(M/Tm) - X M/Tm| <= 3.4e-16 * M; flag anything within 2^-47 M of a decision boundary
         h->guard = (double)(M > 0 ? M : 1) * 7.105427357601002e-15;
         h->draws = draws;
-        h->trivial = (n == 1);
+        h->trivial = (n_total == 1);
         h->tile_ctr = 0;
         h->Z_total = h->S_total = h->P_total = 0;
         if (ok) {
@@ -296,7 +351,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         sm64[lane] = inc - x;
     }
     __syncthreads();
-    uint64_t carry = sm64[warp];
+    uint64_t carry = sm64[warp] + s_off;
     for (int64_t b0 = w0; b0 < w1; b0 += 32) {
         const int64_t b = b0 + lane;
         const uint64_t v = b < w1 ? val(b) : 0;
@@ -340,7 +395,8 @@ __global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const doub
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c0 + k, stream, key);
         const uint64_t P = (uint64_t)(((u128)m * Tm) >> 53);
-        int64_t lo = 0, hi = n - 1;  // P < Tm = Q_{n-1} so the answer exists
+        if (P < h->qoff || P >= __ldg(&L.qfull[n - 1])) continue;  // position on another shard
+        int64_t lo = 0, hi = n - 1;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
             if (__ldg(&L.qfull[mid]) > P) hi = mid; else lo = mid + 1;
@@ -660,8 +716,19 @@ SMC_DEV void copy_row(char *rows, int64_t row_bytes, int64_t dst, int64_t srcr)
 // and destinations count 0 are disjoint).
 constexpr int CSTAGE = TILE + 2 * ANCHOR + 2;
 
+// Shard geometry of pass C: this shard's zero slots have global zero ranks
+// zoff + local rank; global surplus ranks [soff, soff + s_self) are this
+// shard's own surplus children (local pairs, gathered by the next move); the
+// rest arrive as rows in `recv`, ordered by global rank.
+struct ShardC {
+    int64_t zoff, soff, s_self;  // s_self < 0: single GPU (all pairs local)
+    const char *recv;
+    char *rows;
+    int64_t row_bytes;
+};
+
 __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
-                                                  int32_t *__restrict__ parents, Layout L)
+                                                  int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
     const RsHeader *h = L.hdr;
     if (!h->active) return;
@@ -675,19 +742,24 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     const int64_t t = blockIdx.x;
     const int64_t tbase = t * TILE;
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;
-    const uint32_t z0 = (uint32_t)__ldcg(&L.tile_z0[t]), z1 = (uint32_t)__ldcg(&L.tile_z0[t + 1]);
-    const uint32_t Z = h->Z_total, P = h->P_total;
+    const int64_t z0 = __ldcg(&L.tile_z0[t]), z1 = __ldcg(&L.tile_z0[t + 1]);  // local zero ranks
+    const int64_t Zl = h->Z_total, Sl = h->S_total, P = h->P_total;
+    const int64_t s_self = sc.s_self < 0 ? Sl : sc.s_self;
+    const int64_t soff = sc.soff, zoff = sc.zoff;
+    // length of this shard's local piece [soff, soff+s_self) ∩ [zoff, zoff+Zl) in global ranks
+    const int64_t piece = max((int64_t)0, min(zoff + Zl, soff + s_self) - max(zoff, soff));
     int32_t c[RI];
     load_blocked<RT, RI, int32_t>(cin, tbase, n, c, s_io, 1);  // coalesced
     uint32_t nz = 0;
 #pragma unroll
     for (int j = 0; j < RI; ++j) nz += (c[j] == 0);
+    // local surplus ranks this tile needs: [lo_s, hi_s)
+    const int64_t lo_s = max(zoff + z0, soff) - soff, hi_s = min(zoff + z1, soff + s_self) - soff;
     uint32_t cnt = 0;
-    if (z1 > z0) {
-        // surplus parents covering ranks [z0, z1): between the anchors around z0 and z1-1
-        const uint32_t a0 = (uint32_t)__ldcg(&L.anchor[z0 / ANCHOR]);
-        const uint32_t ka = (z1 - 1) / ANCHOR + 1;
-        const uint32_t a1 = (uint64_t)ka * ANCHOR < Z ? (uint32_t)__ldcg(&L.anchor[ka]) : P - 1;
+    if (hi_s > lo_s) {
+        const uint32_t a0 = (uint32_t)__ldcg(&L.anchor[lo_s / ANCHOR]);
+        const int64_t ka = (hi_s - 1) / ANCHOR + 1;
+        const uint32_t a1 = ka * ANCHOR < Sl ? (uint32_t)__ldcg(&L.anchor[ka]) : (uint32_t)(P - 1);
         cnt = a1 - a0 + 1;
         for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
             s_start[k] = __ldcg(&L.sp_start[a0 + k]);
@@ -695,27 +767,62 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
         }
     }
     uint32_t tot;
-    const uint32_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first zero rank of this thread
+    const int64_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first local zero rank
     int32_t par[RI];
     uint32_t lo = 0;
-    if (nz) {  // last k with s_start[k] <= zr, then a forward merge walk
+    int64_t g = zoff + zr;  // global zero rank of this thread's next zero slot
+    if (nz && cnt) {  // last k with s_start[k] <= first local surplus rank, then a forward merge walk
+        const int64_t s0 = max(g, soff) - soff;
         uint32_t hi = cnt;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if ((uint32_t)s_start[mid] <= zr) lo = mid; else hi = mid;
+            if ((int64_t)s_start[mid] <= s0) lo = mid; else hi = mid;
         }
     }
-    uint32_t r = zr;
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         par[j] = (int32_t)(base + j);  // survivors keep their slot
         if (c[j] == 0) {
-            while (lo + 1 < cnt && (uint32_t)s_start[lo + 1] <= r) ++lo;
-            par[j] = s_idx[lo];
-            ++r;
+            if (g >= soff && g < soff + s_self) {
+                const int64_t s = g - soff;
+                while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
+                par[j] = s_idx[lo];
+            } else if (sc.recv) {  // surplus child on another shard: its row arrived in recv
+                const int64_t k = g < soff ? g - zoff : g - zoff - piece;
+                const char *src = sc.recv + k * sc.row_bytes;
+                char *dst = sc.rows + (base + j) * sc.row_bytes;
+                for (int64_t b = 0; b < sc.row_bytes; b += 8)
+                    *(int64_t *)(dst + b) = __ldcg((const long long *)(src + b));
+            }
+            ++g;
         }
     }
     store_blocked<RT, RI, int32_t>(parents, tbase, n, par, s_io);  // coalesced
+}
+
+// Sender side of the cross-shard exchange: rows of this shard's surplus children
+// with local surplus ranks [lo_r, lo_r + cnt_r), destination ranges back to back.
+struct PackRanges {
+    int64_t lo[64], cnt[64], off[64];
+    int K;
+    int64_t total;
+};
+
+__global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, PackRanges pr, char *__restrict__ out,
+                          Layout L)
+{
+    const int64_t Sl = L.hdr->S_total, P = L.hdr->P_total;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pr.total; k += (int64_t)gridDim.x * blockDim.x) {
+        int r = 0;
+        while (r + 1 < pr.K && k >= pr.off[r + 1]) ++r;
+        const int64_t s = pr.lo[r] + (k - pr.off[r]);  // local surplus rank
+        if (s >= Sl) continue;
+        int64_t p = __ldcg(&L.anchor[s / ANCHOR]);
+        while (p + 1 < P && (int64_t)__ldcg(&L.sp_start[p + 1]) <= s) ++p;  // <= ANCHOR steps
+        const int64_t src = __ldcg(&L.sp_idx[p]);
+        for (int64_t b = 0; b < row_bytes; b += 8)
+            *(int64_t *)(out + k * row_bytes + b) = __ldg((const long long *)(rows + src * row_bytes + b));
+    }
 }
 
 // In-place copy of every zero-count row from its parent.
@@ -739,6 +846,16 @@ __global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ pare
     } else {
         copy_row(rows, row_bytes, j, p);
     }
+}
+
+__global__ void k_rs_export_zsp(Layout L, uint32_t *out)
+{
+    const RsHeader *h = L.hdr;
+    const bool on = h->active && !h->trivial;
+    out[0] = on ? h->Z_total : 0;
+    out[1] = on ? h->S_total : 0;
+    out[2] = on ? h->P_total : 0;
+    out[3] = h->active;
 }
 
 __global__ void k_rs_reset(int64_t n, int64_t nt, Layout L)
@@ -821,7 +938,8 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     const double mo = (double)m_out;
 
     k_rs_tiles<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, u, n_u, gate, status, L);
-    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L);
+    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
+                               nullptr, 1, 0, n);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
         k_rs_multinomial<<<grid_cap((m_out + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
@@ -831,7 +949,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (parents) {
         const int64_t nt2 = (n + TILE2 - 1) / TILE2;
         k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
-        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, L);
+        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
                 k_rs_copy<32><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, 32, n, L);
@@ -856,7 +974,7 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
     const int64_t nt2 = (n + TILE2 - 1) / TILE2;
     k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, status, L);
-    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, L);
+    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
@@ -886,4 +1004,114 @@ extern "C" int smc_debug_set(int key, int value)
     if (key != SMC_DEBUG_FORCE_EXACT_F) return smc_set_error(SMC_EINVAL, "smc_debug_set: unknown key %d", key);
     cudaError_t e = cudaMemcpyToSymbol(g_force_exact, &value, sizeof(int));
     return e == cudaSuccess ? SMC_OK : smc_set_error(SMC_ECUDA, "smc_debug_set: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Sharded (multi-GPU) resampling: the same kernels with global offsets; the
+// host allgathers two tiny vectors between the phases.
+// ---------------------------------------------------------------------------
+static int shard_common(int scheme, const double *w, const double *lw_raw, const smc_wstate *st, int64_t n,
+                        int64_t n_total, int64_t m_total, void *ws, size_t ws_bytes, const char *who)
+{
+    if (scheme < 0 || scheme > 5 || n < 1 || n >= ((int64_t)1 << 31) - TILE || n_total < n ||
+        n_total >= ((int64_t)1 << 31) || m_total != n_total)
+        return smc_set_error(SMC_EINVAL, "%s: bad sizes", who);
+    if (!w && (!lw_raw || !st)) return smc_set_error(SMC_EINVAL, "%s: need w or (lw_raw, state)", who);
+    if (!ws || ws_bytes < smc_resample_workspace_bytes(n)) return smc_set_error(SMC_EWORKSPACE, "%s: workspace", who);
+    return SMC_OK;
+}
+
+static double shard_rscale(int64_t n_total)
+{
+    int L2 = 0;
+    while (((int64_t)1 << L2) < n_total) ++L2;
+    return ldexp(1.0, 63 - L2);
+}
+
+extern "C" int smc_resample_shard_totals(int scheme, const double *w, const double *lw_raw, const smc_wstate *st,
+                                         int64_t n, int64_t n_total, int64_t m_total, const double *u, int64_t n_u,
+                                         const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes,
+                                         uint64_t *totals_out, void *stream)
+{
+    int rc = shard_common(scheme, w, lw_raw, st, n, n_total, m_total, ws, ws_bytes, "smc_resample_shard_totals");
+    if (rc) return rc;
+    if (!totals_out) return smc_set_error(SMC_EINVAL, "smc_resample_shard_totals: totals_out");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nt = (n + TILE - 1) / TILE;
+    Layout L = layout(ws, n);
+    WSrc src{w, lw_raw, st, n_total};  // equal weights are 1 / N_total
+    k_rs_tiles<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, (double)m_total, shard_rscale(n_total), u, n_u, gate,
+                                           status, L);
+    k_rs_local_totals<<<1, SB, 0, s>>>(nt, gate, L, totals_out);
+    return smc_check_launch("smc_resample_shard_totals");
+}
+
+extern "C" int smc_resample_shard_counts(int scheme, const double *w, const double *lw_raw, const smc_wstate *st,
+                                         int64_t n, int64_t n_total, int64_t m_total, int G, int rank,
+                                         const uint64_t *totals_all, uint64_t seed, uint64_t stream_index,
+                                         uint64_t *ctr, const double *u, int64_t n_u, int32_t *counts,
+                                         const int32_t *gate, int32_t *status, void *ws, size_t ws_bytes,
+                                         uint32_t *zsp_out, void *stream)
+{
+    int rc = shard_common(scheme, w, lw_raw, st, n, n_total, m_total, ws, ws_bytes, "smc_resample_shard_counts");
+    if (rc) return rc;
+    if (G < 1 || rank < 0 || rank >= G || !totals_all || !zsp_out || (!u && !ctr))
+        return smc_set_error(SMC_EINVAL, "smc_resample_shard_counts: bad shard args");
+    if (counts && ((uintptr_t)counts & 15)) return smc_set_error(SMC_EINVAL, "smc_resample_shard_counts: counts");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nt = (n + TILE - 1) / TILE, nt2 = (n + TILE2 - 1) / TILE2;
+    Layout L = layout(ws, n);
+    WSrc src{w, lw_raw, st, n_total};
+    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const double rscale = shard_rscale(n_total), mo = (double)m_total;
+    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_total, key, stream_index, ctr, u, n_u, gate, status, L,
+                               totals_all, G, rank, n_total);
+    if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
+        k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
+        k_rs_multinomial<<<grid_cap((m_total + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
+    }
+    int32_t *cout = counts ? counts : L.cnt;
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
+    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
+    k_rs_export_zsp<<<1, 1, 0, s>>>(L, zsp_out);
+    return smc_check_launch("smc_resample_shard_counts");
+}
+
+extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, const int64_t *ranges, int K,
+                                       void *sendbuf, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!rows || row_bytes < 8 || (row_bytes & 7) || K < 0 || K > 64 || (K && (!ranges || !sendbuf)) || !ws)
+        return smc_set_error(SMC_EINVAL, "smc_resample_shard_pack: bad args");
+    PackRanges pr{};
+    pr.K = K;
+    int64_t off = 0;
+    for (int r = 0; r < K; ++r) {
+        pr.lo[r] = ranges[2 * r];
+        pr.cnt[r] = ranges[2 * r + 1];
+        pr.off[r] = off;
+        off += pr.cnt[r];
+    }
+    pr.total = off;
+    if (!off) return SMC_OK;
+    Layout L = layout(ws, 1);  // only the header / surplus list pointers are used
+    (void)ws_bytes;
+    const int bs = 256;
+    k_rs_pack<<<grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>((const char *)rows, row_bytes, pr,
+                                                                              (char *)sendbuf, L);
+    return smc_check_launch("smc_resample_shard_pack");
+}
+
+extern "C" int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64_t zoff, int64_t soff, int64_t s_self,
+                                         const void *recv, void *rows, int64_t row_bytes, int32_t *parents, void *ws,
+                                         size_t ws_bytes, void *stream)
+{
+    if (n < 1 || !parents || !ws || ws_bytes < smc_resample_workspace_bytes(n) || zoff < 0 || soff < 0 ||
+        (recv && (!rows || row_bytes < 8 || (row_bytes & 7))))
+        return smc_set_error(SMC_EINVAL, "smc_resample_shard_assign: bad args");
+    const int64_t nt = (n + TILE - 1) / TILE;
+    Layout L = layout(ws, n);
+    const int32_t *cin = counts ? counts : L.cnt;
+    k_rs_assign<<<(unsigned)nt, RT, 0, (cudaStream_t)stream>>>(
+        cin, n, parents, ShardC{zoff, soff, s_self, (const char *)recv, (char *)rows, row_bytes}, L);
+    return smc_check_launch("smc_resample_shard_assign");
 }

@@ -105,38 +105,78 @@ __global__ void __launch_bounds__(FB) k_lse_level1(const LsePartial *__restrict_
     lse_slice(parts, mon, b0, b1, l2 + blockIdx.x, l2mon + blockIdx.x);
 }
 
+// The state update shared by the single-GPU finalize and the multi-GPU combine.
+SMC_DEV void apply_lse(smc_wstate *st, LsePartial t, int64_t n, int mode, int accumulate_nc)
+{
+    if (t.m == -INFINITY || !(t.s1 > 0.0)) {
+        raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
+        return;
+    }
+    const double ls = log(t.s1);
+    const double lse = t.m + ls;
+    st->lse = lse;
+    st->max_raw = t.m;
+    st->log_sum = ls;
+    st->ess = (t.s1 * t.s1) / t.s2;  // 1 / sum W^2 with W = e / s1
+    st->ess_over_n = st->ess / (double)n;
+    st->equal = 0;
+    if (mode == SMC_W_ADD_LOG) {
+        // previous lw was normalized => log sum_i W_{t-1,i} exp(incw_i) = lse
+        st->nc_inc = lse;
+        if (accumulate_nc) st->log_zconst += lse;
+    } else if (mode == SMC_W_SET_LOG && accumulate_nc) {
+        // first weighting from the equal-weight prior sample: log (1/N) sum_i exp(v_i)
+        st->nc_inc = lse - log((double)n);
+        st->log_zconst = st->nc_inc;
+    }
+}
+
+// partial_out != NULL (a shard of a multi-GPU system): export {max, sum e,
+// sum e^2, monitor0, monitor1} instead of updating the state; the ranks then
+// allgather and smc_weights_combine them in rank order.
 __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ l2, const double2 *__restrict__ l2mon,
                                                       int has_mon, smc_wstate *st, int64_t n, int mode,
-                                                      int accumulate_nc, double *mon_out)
+                                                      int accumulate_nc, double *mon_out, double *partial_out)
 {
     __shared__ LsePartial s_t;
     __shared__ double2 s_h;
     lse_slice(l2, has_mon ? l2mon : nullptr, 0, FG, &s_t, &s_h);
     if (threadIdx.x == 0) {
         const LsePartial t = s_t;
-        if (has_mon && mon_out) { mon_out[0] = s_h.x; mon_out[1] = s_h.y; }
-        if (t.m == -INFINITY || !(t.s1 > 0.0)) {
-            raise_status(&st->status, SMC_ENORMALIZE);  // SPEC.md:45 all -inf
+        if (partial_out) {
+            partial_out[0] = t.m;
+            partial_out[1] = t.s1;
+            partial_out[2] = t.s2;
+            partial_out[3] = has_mon ? s_h.x : 0.0;
+            partial_out[4] = has_mon ? s_h.y : 0.0;
             return;
         }
-        const double ls = log(t.s1);
-        const double lse = t.m + ls;
-        st->lse = lse;
-        st->max_raw = t.m;
-        st->log_sum = ls;
-        st->ess = (t.s1 * t.s1) / t.s2;  // 1 / sum W^2 with W = e / s1
-        st->ess_over_n = st->ess / (double)n;
-        st->equal = 0;
-        if (mode == SMC_W_ADD_LOG) {
-            // previous lw was normalized => log sum_i W_{t-1,i} exp(incw_i) = lse
-            st->nc_inc = lse;
-            if (accumulate_nc) st->log_zconst += lse;
-        } else if (mode == SMC_W_SET_LOG && accumulate_nc) {
-            // first weighting from the equal-weight prior sample: log (1/N) sum_i exp(v_i)
-            st->nc_inc = lse - log((double)n);
-            st->log_zconst = st->nc_inc;
-        }
+        if (has_mon && mon_out) { mon_out[0] = s_h.x; mon_out[1] = s_h.y; }
+        apply_lse(st, t, n, mode, accumulate_nc);
     }
+}
+
+// Multi-GPU: combine G exported shard partials (stride SMC_PARTIAL_STRIDE) in
+// rank order -- every rank computes bit-identical state (unlike an allreduce).
+__global__ void k_lse_combine(const double *__restrict__ parts, int G, smc_wstate *st, int64_t n_total, int mode,
+                              int accumulate_nc, double *mon_out)
+{
+    double M = -INFINITY;
+    for (int g = 0; g < G; ++g) M = fmax(M, parts[g * SMC_PARTIAL_STRIDE]);
+    LsePartial t{M, 0.0, 0.0};
+    double h0 = 0.0, h1 = 0.0;
+    for (int g = 0; g < G; ++g) {
+        const double *p = parts + g * SMC_PARTIAL_STRIDE;
+        if (p[0] != -INFINITY) {
+            const double f = exp(p[0] - M);
+            t.s1 += p[1] * f;
+            t.s2 += p[2] * (f * f);
+        }
+        h0 += p[3];
+        h1 += p[4];
+    }
+    if (mon_out) { mon_out[0] = h0; mon_out[1] = h1; }
+    apply_lse(st, t, n_total, mode, accumulate_nc);
 }
 
 __global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
@@ -146,6 +186,7 @@ __global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
     st->lse = log((double)n);  // consistent with lw_raw == 0 everywhere
     st->max_raw = 0.0;
     st->log_sum = log((double)n);
+    st->w_equal = 1.0 / (double)n;
     st->ess = (double)n;
     st->ess_over_n = 1.0;
 }
@@ -157,7 +198,8 @@ __global__ void k_weights_read(int what, const double *__restrict__ lw_raw, cons
     if (i >= n) return;
     const NormLw nl = norm_of(st);
     const double l = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
-    out[i] = what == SMC_READ_WEIGHT ? (nl.eq ? 1.0 / (double)n : exp(l)) : l;
+    // equal weights are exp(-log N): N is the GLOBAL count of a sharded system
+    out[i] = what == SMC_READ_WEIGHT ? (nl.eq ? nl.weq : exp(l)) : l;
 }
 
 // SPEC.md:266 / SURVEY R8: threshold >= 1 always, <= 0 never, else ess/N < threshold.
@@ -183,9 +225,9 @@ __global__ void __launch_bounds__(RB) k_wsum_pass(const double *__restrict__ val
 #pragma unroll
     for (int j = 0; j < RMAX; ++j) acc[j] = 0.0;
     const NormLw nl = norm_of(st);
-    const double inv_n = 1.0 / (double)n;
+    const double w_eq = nl.weq;  // 1 / N_total after set_equal_weight
     for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        const double w = nl.eq ? inv_n : exp(nl(lw_raw[i]));
+        const double w = nl.eq ? w_eq : exp(nl(lw_raw[i]));
 #pragma unroll
         for (int j = 0; j < RMAX; ++j)
             if (j < mc) acc[j] += w * vals[i * ld + m0 + j];
@@ -226,12 +268,22 @@ size_t smc_lse_scratch_bytes() { return FG * (sizeof(LsePartial) + sizeof(double
 
 void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
                              int accumulate_nc, cudaStream_t s, void *scratch, const double2 *mon_parts,
-                             double *mon_out)
+                             double *mon_out, double *partial_out)
 {
     LsePartial *l2 = (LsePartial *)scratch;
     double2 *l2mon = (double2 *)(l2 + FG);
     k_lse_level1<<<FG, FB, 0, s>>>(parts, nparts, mon_parts, l2, l2mon);
-    k_lse_finalize<<<1, FB, 0, s>>>(l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out);
+    k_lse_finalize<<<1, FB, 0, s>>>(l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out,
+                                    partial_out);
+}
+
+extern "C" int smc_weights_combine(const double *partials, int G, smc_wstate *st, int64_t n_total, int mode,
+                                   int accumulate_nc, double *monitor_out, void *stream)
+{
+    if (!partials || G < 1 || !st || n_total < 1)
+        return smc_set_error(SMC_EINVAL, "smc_weights_combine: bad args");
+    k_lse_combine<<<1, 1, 0, (cudaStream_t)stream>>>(partials, G, st, n_total, mode, accumulate_nc, monitor_out);
+    return smc_check_launch("smc_weights_combine");
 }
 
 extern "C" size_t smc_weights_workspace_bytes(int64_t n)

@@ -57,4 +57,4 @@ SMC_DEV LsePartial lse_combine(LsePartial a, LsePartial b)
 size_t smc_lse_scratch_bytes();
 void smc_launch_lse_finalize(const smc::LsePartial *parts, int nparts, smc_wstate *st, int64_t n, int mode,
                              int accumulate_nc, cudaStream_t s, void *scratch, const double2 *mon_parts = nullptr,
-                             double *mon_out = nullptr);
+                             double *mon_out = nullptr, double *partial_out = nullptr);

@@ -78,8 +78,12 @@ def cv_init(system, param=None):
     ws, nb = _ws(system, n)
     w = system.weight_set
     v.pending = None  # the prior draw overwrites every row
-    _abi.call("smc_pf_init", _abi.ptr(v.raw), _abi.ptr(w.lw_raw), n, system.rng_set.seed,
-              _abi.ptr(system.rng_set.counters), v.obs_ptr(0), w.state_ptr, ws, nb, _abi.stream())
+    shard = system.shard
+    _abi.call("smc_pf_init", _abi.ptr(v.raw), _abi.ptr(w.lw_raw), n, system.stream_base, system.rng_set.seed,
+              _abi.ptr(system.rng_set.counters), v.obs_ptr(0), w.state_ptr,
+              None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
+    if shard is not None:  # global normalization: allgather the shard partials, combine in rank order
+        shard.combine(w, 0, True)  # SMC_W_SET_LOG
     return None  # acceptance "bares no meaning"
 
 
@@ -90,8 +94,10 @@ def _cv_move_kernel(iter_, system):
     w = system.weight_set
     # a pending fused "pos" monitor of the previous iteration is reduced by this launch
     mon = system.take_pending_monitor("pos")
-    common = (_abi.ptr(w.lw_raw), n, system.rng_set.seed, _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_),
-              w.state_ptr, None, mon, ws, nb, _abi.stream())
+    shard = system.shard
+    common = (_abi.ptr(w.lw_raw), n, system.stream_base, system.n_total, system.rng_set.seed,
+              _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_), w.state_ptr, None, mon,
+              None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
     if v.pending is not None:  # fold the last resample's copy into this move (double buffer)
         parents, gate = v.pending
         v.pending = None
@@ -99,6 +105,8 @@ def _cv_move_kernel(iter_, system):
         v.swap()
     else:
         _abi.call("smc_pf_move", None, _abi.ptr(v.raw), None, None, *common)
+    if shard is not None:  # global add_log_weight + the fused monitor of the previous iteration
+        shard.combine(w, 1, True, mon)  # SMC_W_ADD_LOG
     return None
 
 
@@ -119,9 +127,11 @@ def cv_monitor(dim=2):
     return ev
 
 
-def make_sampler(n, scheme=ResampleScheme.Systematic, threshold=0.5, seed=0, device="cuda", monitor_dim=2):
-    """The paper's main(): sampler, init, move, 'pos' monitor."""
-    s = Sampler(n, scheme, threshold, seed, value=CVState(n, device), device=device)
+def make_sampler(n, scheme=ResampleScheme.Systematic, threshold=0.5, seed=0, device="cuda", monitor_dim=2,
+                 shard=None):
+    """The paper's main(): sampler, init, move, 'pos' monitor.
+    shard: a dist.Shard to run this as one rank of a multi-GPU filter (n particles per rank)."""
+    s = Sampler(n, scheme, threshold, seed, value=CVState(n, device), device=device, shard=shard)
     s.set_init(cv_init)
     s.add_move(cv_move(), False)
     s.set_monitor("pos", monitor_dim, cv_monitor(monitor_dim))

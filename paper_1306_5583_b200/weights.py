@@ -78,9 +78,10 @@ class WeightSet:
         """weight = 1/N, ess = N (SPEC.md:31-39)."""
         self._update(EQUAL, None, check=False)
 
-    def set_equal_weight_if(self, gate_ptr):
-        """Device-gated set_equal_weight (the post-resample reset; no host sync)."""
-        _abi.call("smc_weights_set_equal", self.state_ptr, self.size, gate_ptr, _abi.stream())
+    def set_equal_weight_if(self, gate_ptr, n_total=None):
+        """Device-gated set_equal_weight (the post-resample reset; no host sync).
+        n_total: the global particle count of a sharded system (equal weight 1/n_total)."""
+        _abi.call("smc_weights_set_equal", self.state_ptr, int(n_total or self.size), gate_ptr, _abi.stream())
 
     def set_log_weight(self, values, check=None):
         """Normalize values by max-shift + log-sum-exp."""

@@ -55,5 +55,5 @@ def test_argument_validation_without_gpu():
 
 
 def test_wstate_layout_matches_header():
-    assert _abi.WSTATE_BYTES == 72
-    assert _abi.WSTATE_OFF["status"] == 60 and _abi.WSTATE_OFF["resample"] == 64
+    assert _abi.WSTATE_BYTES == 80
+    assert _abi.WSTATE_OFF["status"] == 68 and _abi.WSTATE_OFF["resample"] == 72
