@@ -183,7 +183,11 @@ def run_b200(args):
     # synthetic observations of the paper's shape: a smooth track + noise (T x 2)
     obs = np.cumsum(rs.normal(0, 0.15, (max(100, T), 2)), 0)
 
-    s = P.pf.make_sampler(n, args.scheme, 0.5, seed=1306 + rank)
+    shard = None
+    if world > 1:  # one rank's slice of a G-GPU filter: global streams, NCCL allgathers + row exchange
+        from paper_1306_5583_b200.dist import Shard, TorchComm
+        shard = Shard(n, TorchComm())
+    s = P.pf.make_sampler(n, args.scheme, 0.5, seed=1306, shard=shard)
     s.initialize(obs)
     s.timing = None
     for _ in range(args.warmup):

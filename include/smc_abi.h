@@ -199,8 +199,8 @@ int smc_resample_shard_counts(int scheme, const double *w, const double *lw_raw,
                               const uint64_t *totals_all, uint64_t seed, uint64_t stream_index, uint64_t *ctr,
                               const double *u, int64_t n_u, int32_t *counts, const int32_t *gate, int32_t *status,
                               void *ws, size_t ws_bytes, uint32_t *zsp_out, void *stream);
-int smc_resample_shard_pack(const void *rows, int64_t row_bytes, const int64_t *ranges, int K, void *sendbuf, void *ws,
-                            size_t ws_bytes, void *stream);
+int smc_resample_shard_pack(const void *rows, int64_t row_bytes, int64_t n, const int64_t *ranges, int K,
+                            void *sendbuf, void *ws, size_t ws_bytes, void *stream);
 int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64_t zoff, int64_t soff, int64_t s_self,
                               const void *recv, void *rows, int64_t row_bytes, int32_t *parents, void *ws,
                               size_t ws_bytes, void *stream);

@@ -77,7 +77,7 @@ _SIGS = {
                                   C.c_int),
     "smc_resample_shard_counts": ([_i32, _vp, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _vp, _u64, _u64, _vp, _vp,
                                    _i64, _vp, _vp, _vp, _vp, _sz, _vp, _vp], C.c_int),
-    "smc_resample_shard_pack": ([_vp, _i64, _vp, _i32, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_resample_shard_pack": ([_vp, _i64, _i64, _vp, _i32, _vp, _vp, _sz, _vp], C.c_int),
     "smc_resample_shard_assign": ([_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp], C.c_int),
     "smc_replication_to_parents": ([_vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gather_rows": ([_vp, _vp, _i64, _vp, _i64, _vp], C.c_int),

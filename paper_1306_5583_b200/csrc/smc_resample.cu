@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
 // prefix.  It emits the compacted surplus-parent list (index, first surplus
 // rank), rank anchors every ANCHOR ranks, and each slot tile's first zero rank.
 // Writes are per-thread contiguous runs; no 4-byte scatter.
-__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt2,
+__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt2, int whole,
                                                  int32_t *status, Layout L)
 {
     RsHeader *h = L.hdr;
@@ -655,7 +655,8 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
                 h->P_total = P;
                 L.sp_start[P] = (int32_t)S;  // sentinel
                 L.tile_z0[(n + TILE - 1) / TILE] = (int32_t)Z;
-                if (Z != S) raise_status(status, SMC_ECOUNTS);  // sum(counts) != N
+                // sum(counts) != N; a shard's Z and S only balance globally (host check)
+                if (whole && Z != S) raise_status(status, SMC_ECOUNTS);
             }
         }
     }
@@ -948,7 +949,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
     if (parents) {
         const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
+        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, 1, status, L);
         k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
@@ -973,7 +974,7 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
     k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
     const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, status, L);
+    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, 1, status, L);
     k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
@@ -1072,15 +1073,16 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     }
     int32_t *cout = counts ? counts : L.cnt;
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
-    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, status, L);
+    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, 0, status, L);
     k_rs_export_zsp<<<1, 1, 0, s>>>(L, zsp_out);
     return smc_check_launch("smc_resample_shard_counts");
 }
 
-extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, const int64_t *ranges, int K,
+extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, int64_t n, const int64_t *ranges, int K,
                                        void *sendbuf, void *ws, size_t ws_bytes, void *stream)
 {
-    if (!rows || row_bytes < 8 || (row_bytes & 7) || K < 0 || K > 64 || (K && (!ranges || !sendbuf)) || !ws)
+    if (!rows || row_bytes < 8 || (row_bytes & 7) || K < 0 || K > 64 || (K && (!ranges || !sendbuf)) || !ws ||
+        n < 1 || ws_bytes < smc_resample_workspace_bytes(n))
         return smc_set_error(SMC_EINVAL, "smc_resample_shard_pack: bad args");
     PackRanges pr{};
     pr.K = K;
@@ -1093,8 +1095,7 @@ extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, cons
     }
     pr.total = off;
     if (!off) return SMC_OK;
-    Layout L = layout(ws, 1);  // only the header / surplus list pointers are used
-    (void)ws_bytes;
+    Layout L = layout(ws, n);
     const int bs = 256;
     k_rs_pack<<<grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>((const char *)rows, row_bytes, pr,
                                                                               (char *)sendbuf, L);

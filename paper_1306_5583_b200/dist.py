@@ -155,7 +155,7 @@ class Shard:
             sendbuf = torch.empty((nsend, row_bytes // 8), dtype=torch.float64, device=dev)
             ranges = (ctypes.c_int64 * (2 * len(plan["sends"])))(
                 *[v for _, lo, c in plan["sends"] for v in (lo, c)])
-            _abi.call("smc_resample_shard_pack", rows, row_bytes, ranges, len(plan["sends"]), _abi.ptr(sendbuf),
+            _abi.call("smc_resample_shard_pack", rows, row_bytes, n, ranges, len(plan["sends"]), _abi.ptr(sendbuf),
                       buf, nb, _abi.stream())
             o = 0
             for peer, _, c in plan["sends"]:

@@ -73,7 +73,8 @@ def test_sharded_resample_equals_single(scheme, G, n):
         buf = torch.empty((max(tot, 1), 4), dtype=torch.float64, device="cuda")
         if tot:
             ranges = (ctypes.c_int64 * (2 * len(sends)))(*[v for _, lo, c in sends for v in (lo, c)])
-            _abi.call("smc_resample_shard_pack", p(xg[g]), 32, ranges, len(sends), p(buf), p(ws[g]), ws[g].numel(), S)
+            _abi.call("smc_resample_shard_pack", p(xg[g]), 32, n, ranges, len(sends), p(buf), p(ws[g]), ws[g].numel(),
+                      S)
         o = 0
         for peer, _, c in sends:
             outbox[(g, peer)] = buf[o:o + c]
