@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include "../../include/smc_abi.h"
+#include "smc_fastmath.h"
 
 typedef unsigned __int128 u128;
 
@@ -61,12 +62,13 @@ SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, Key key)
 }
 
 // rng.py:85-91: Box-Muller cosine branch on 1 - u1, exactly two draws.
-// (All TUs build with --fmad=false, so no contraction changes the rounding.)
+// (All TUs build with --fmad=false, so no contraction changes the rounding;
+// log/cos are smc_fastmath.h's <= 0.55 / 1 ulp versions, sqrt is IEEE.)
 SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, Key key)
 {
     const double u1 = u01_at(ctr, stream, key);
     const double u2 = u01_at(ctr + 1, stream, key);
-    return sqrt(-2.0 * log(1.0 - u1)) * cos((2.0 * 3.141592653589793) * u2);
+    return sqrt(-2.0 * smc_fm::log(1.0 - u1)) * smc_fm::cos((2.0 * 3.141592653589793) * u2);
 }
 
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the
@@ -91,7 +93,7 @@ SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, Key key, double shape)
         const double v = t * t * t;
         const double u = 1.0 - u01_at(ctr, stream, key);
         ctr += 1;
-        if (log(u) < 0.5 * x * x + d - d * v + d * log(v)) return boost * d * v;
+        if (smc_fm::log(u) < 0.5 * x * x + d - d * v + d * smc_fm::log(v)) return boost * d * v;
     }
 }
 

