@@ -13,6 +13,9 @@ using namespace smc;
 namespace {
 
 constexpr int PB = 256;
+#ifndef PF_MIN_BLOCKS
+#define PF_MIN_BLOCKS 4
+#endif
 
 struct PfConst {
     double sd_pos0, sd_vel0;  // init: 2, 1
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // x_in[parents[i]] (when the device gate says the resample ran) and written to
 // x_out[i], a second buffer: the "simultaneous" copy of SPEC.md:343 for free.
 template <bool MON>
-__global__ void __launch_bounds__(PB, 4) k_pf_move(const double *x_in, double *x_out,
+__global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
                                                    double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
                                                    double w_equal, Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,

@@ -20,6 +20,8 @@ __global__ void k(double *out, int64_t n, Key key)
         if (F == 4) acc += (double)draw53((uint64_t)r + (uint64_t)(acc * 1e-300), (uint64_t)i, key);
         if (F == 5) acc += normal_at((uint64_t)r * 2 + (uint64_t)(acc * 1e-300), (uint64_t)i, key);
         if (F == 6) acc += x * 1.0000001 + acc * 1e-300;
+        if (F == 7) acc += smc_fm::log(x + acc * 1e-300);
+        if (F == 8) acc += smc_fm::cos(x * 6.283185307179586 + acc * 1e-300);
         x += 1e-3;
     }
     out[i] = acc;
@@ -32,8 +34,9 @@ int main()
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    const char *names[] = {"log", "cos", "sqrt", "exp", "philox+u53", "normal(2 philox+log+sqrt+cos)", "baseline"};
-    for (int f = 0; f < 7; ++f) {
+    const char *names[] = {"log", "cos", "sqrt", "exp", "philox+u53", "normal(2 philox+log+sqrt+cos)", "baseline",
+                           "smc_fm::log", "smc_fm::cos"};
+    for (int f = 0; f < 9; ++f) {
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(a);
             Key key{1306, 0};
@@ -45,6 +48,8 @@ int main()
             case 4: k<4><<<n / 256, 256>>>(d, n, key); break;
             case 5: k<5><<<n / 256, 256>>>(d, n, key); break;
             case 6: k<6><<<n / 256, 256>>>(d, n, key); break;
+            case 7: k<7><<<n / 256, 256>>>(d, n, key); break;
+            case 8: k<8><<<n / 256, 256>>>(d, n, key); break;
             }
             cudaEventRecord(b);
             cudaEventSynchronize(b);
