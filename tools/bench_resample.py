@@ -63,7 +63,7 @@ def main():
         for kind in kinds:
             w = weights(n, kind, g)
             for scheme in SCHEMES:
-                sid = int(P.resample.ResampleScheme[scheme.title().replace("_", "")])
+                sid = int(P.ResampleScheme[scheme.title().replace("_", "")])
 
                 def call():
                     _abi.call("smc_resample", sid, ctypes.c_void_p(w.data_ptr()), None, None, n, n, rng.seed, n,
