@@ -534,3 +534,187 @@ int orc_pf_run(int64_t n, uint64_t seed, int scheme, double threshold, const dou
     free(s.x); free(s.lw); free(s.w); free(s.incw); free(s.ctrs); free(s.counts); free(s.parents);
     return rc;
 }
+
+/* ------------------------------------------------------------------------- */
+/* example-gmm                         */
+/* state row: mu[4] lambda[4] omega[4] log_prior log_likelihood pad pad       */
+/* ------------------------------------------------------------------------- */
+
+static void gmm_hyper_derive(const double *h5, double *h)
+{
+    /* h: xi kappa nu chi rho | lgamma(nu) log(chi) log(kappa/2pi) dirichlet_const */
+    for (int k = 0; k < 5; ++k) h[k] = h5[k];
+    h[5] = lgamma(h[2]);
+    h[6] = log(h[3]);
+    h[7] = log(h[1] / (2.0 * 3.141592653589793));
+    h[8] = lgamma(ORC_GMM_R * h[4]) - ORC_GMM_R * lgamma(h[4]);
+}
+
+/* update_log_likelihood */
+double orc_gmm_llh(const double *row, const double *y, int nd)
+{
+    double ll = -0.5 * (double)nd * 1.8378770664093455;
+    double lj[ORC_GMM_R];
+    for (int j = 0; j < ORC_GMM_R; ++j) lj[j] = log(row[ORC_GMM_R + j]);
+    for (int k = 0; k < nd; ++k) {
+        double lli = 0;
+        for (int j = 0; j < ORC_GMM_R; ++j) {
+            double resid = y[k] - row[j];
+            lli += row[2 * ORC_GMM_R + j] * exp(0.5 * lj[j] - 0.5 * row[ORC_GMM_R + j] * resid * resid);
+        }
+        ll += log(lli);
+    }
+    return ll;
+}
+
+/* update_log_prior */
+double orc_gmm_lprior(const double *row, const double *h5)
+{
+    double h[9];
+    gmm_hyper_derive(h5, h);
+    double lp = 0;
+    for (int j = 0; j < ORC_GMM_R; ++j) {
+        double d = row[j] - h[0];
+        lp += h[7] * 0.5 - 0.5 * h[1] * d * d;
+        double lam = row[ORC_GMM_R + j];
+        lp += (h[2] - 1) * log(lam) - lam / h[3] - h[5] - h[2] * h[6];
+        if (h[4] != 1.0) lp += (h[4] - 1) * log(row[2 * ORC_GMM_R + j]);
+    }
+    return lp + h[8];
+}
+
+/* gmm_init::initialize_state for particles [0, n) */
+void orc_gmm_init(double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
+                  const double *h5, int nthreads)
+{
+    const double sd0 = 1.0 / sqrt(h5[1]);
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+        double *row = x + ORC_GMM_ROW * i;
+        double sum = 0;
+        for (int j = 0; j < ORC_GMM_R; ++j) {
+            row[j] = h5[0] + sd0 * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
+            row[ORC_GMM_R + j] = h5[3] * orc_std_gamma(ctrs, (uint64_t)i, k0, k1, h5[2]);
+            row[2 * ORC_GMM_R + j] = 1.0 * orc_std_gamma(ctrs, (uint64_t)i, k0, k1, 1.0);
+            sum += row[2 * ORC_GMM_R + j];
+        }
+        for (int j = 0; j < ORC_GMM_R; ++j) row[2 * ORC_GMM_R + j] /= sum;
+        row[12] = orc_gmm_lprior(row, h5);
+        row[13] = orc_gmm_llh(row, y, nd);
+        row[14] = row[15] = 0.0;
+    }
+    (void)nthreads;
+}
+
+/* gmm_move_{mu,lambda,weight}: returns #accepted */
+int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y,
+                   int nd, const double *h5, double alpha, double sd, int nthreads)
+{
+    int64_t acc = 0;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) reduction(+ : acc) num_threads(nthreads > 0 ? nthreads : 1)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+        double *row = x + ORC_GMM_ROW * i;
+        double p[ORC_GMM_ROW];
+        memcpy(p, row, sizeof(p));
+        double p_old = row[12] + alpha * row[13];
+        double jac = 0;
+        if (block == 0) {
+            for (int j = 0; j < ORC_GMM_R; ++j) p[j] += 0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
+        } else if (block == 1) {
+            for (int j = 0; j < ORC_GMM_R; ++j) {
+                double old = p[ORC_GMM_R + j];
+                p[ORC_GMM_R + j] = old * exp(0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1));
+                jac += log(p[ORC_GMM_R + j]) - log(old);
+            }
+        } else {
+            double g[ORC_GMM_R];
+            double *om = p + 2 * ORC_GMM_R;
+            for (int j = 0; j < ORC_GMM_R; ++j) jac -= log(om[j]);
+            for (int j = 0; j < ORC_GMM_R - 1; ++j)
+                g[j] = log(om[j] / om[ORC_GMM_R - 1]) + (0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1));
+            g[ORC_GMM_R - 1] = 0.0;
+            double gm = g[0];
+            for (int j = 1; j < ORC_GMM_R; ++j) gm = fmax(gm, g[j]);
+            double s = 0;
+            for (int j = 0; j < ORC_GMM_R; ++j) { om[j] = exp(g[j] - gm); s += om[j]; }
+            for (int j = 0; j < ORC_GMM_R; ++j) { om[j] /= s; jac += log(om[j]); }
+        }
+        double lp = orc_gmm_lprior(p, h5), ll = orc_gmm_llh(p, y, nd);
+        double dp = lp + alpha * ll - p_old + jac;
+        double u = log(orc_u01(ctrs, (uint64_t)i, k0, k1));
+        if (u < dp) {
+            p[12] = lp;
+            p[13] = ll;
+            memcpy(row, p, sizeof(p));
+            acc += 1;
+        }
+    }
+    (void)nthreads;
+    return acc;
+}
+
+/* The GMM sampler: prior annealing
+ * alpha_t = (t/T)^power, move_smc -> ESS rule -> resample -> mu, lambda, weight MH ->
+ * path (alpha_t, sum W llh).  hist rows (T+1) x 8: ess_over_n resampled acc_mu acc_lambda
+ * acc_weight alpha U_t log_zconst. */
+int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                const double *h5, int T, double power, double *hist, int nthreads)
+{
+    double *x = (double *)calloc((size_t)(ORC_GMM_ROW * n), sizeof(double));
+    double *lw = (double *)malloc(sizeof(double) * (size_t)n), *w = (double *)malloc(sizeof(double) * (size_t)n);
+    double *incw = (double *)malloc(sizeof(double) * (size_t)n);
+    uint64_t *ctrs = (uint64_t *)calloc((size_t)(n + 1), sizeof(uint64_t));
+    int32_t *counts = (int32_t *)malloc(sizeof(int32_t) * (size_t)n), *parents = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    double ess, alpha = 0.0, log_z = 0.0;
+    int rc = 0;
+    orc_gmm_init(x, n, ctrs, k0, k1, y, nd, h5, nthreads);
+    orc_weights_update(ORC_W_EQUAL, lw, w, NULL, n, &ess);
+    for (int t = 0; t <= T && !rc; ++t) {
+        double *hr = hist + 8 * t;
+        double acc[3] = {0, 0, 0};
+        if (t > 0) {
+            double a = pow((double)t / (double)T, power);
+            a = a < 1 ? a : 1;
+            a = a > 0 ? a : 0;
+            double dalpha = a - alpha;
+            alpha = a;
+            double ac = alpha < 0.02 ? 0.02 : alpha;
+            double sds[3] = {0.15 / ac, (1 + sqrt(1 / ac)) * 0.15, (1 + sqrt(1 / ac)) * 0.2};
+            for (int64_t i = 0; i < n; ++i) incw[i] = dalpha * x[ORC_GMM_ROW * i + 13];
+            log_z += orc_nc_increment(lw, incw, n);
+            rc = orc_weights_update(ORC_W_ADD_LOG, lw, w, incw, n, &ess);
+            if (rc) break;
+            double eon = ess / (double)n;
+            int rs = resample_rule(eon, threshold);
+            hr[0] = eon;
+            hr[1] = rs;
+            if (rs && n > 1) {
+                int64_t draws;
+                rc = orc_resample_counts(scheme, w, n, n, ctrs, (uint64_t)n, k0, k1, NULL, 0, counts, &draws);
+                if (!rc) rc = orc_replication_to_parents(counts, n, parents);
+                if (rc) break;
+                orc_copy_rows(x, n, ORC_GMM_ROW, parents);
+                orc_weights_update(ORC_W_EQUAL, lw, w, NULL, n, &ess);
+            }
+            for (int b = 0; b < 3; ++b) acc[b] = (double)orc_gmm_mh(b, x, n, ctrs, k0, k1, y, nd, h5, alpha, sds[b], nthreads);
+        } else {
+            hr[0] = ess / (double)n;
+            hr[1] = resample_rule(hr[0], threshold);
+        }
+        double u = 0;
+        for (int64_t i = 0; i < n; ++i) u += w[i] * x[ORC_GMM_ROW * i + 13];
+        hr[2] = acc[0];
+        hr[3] = acc[1];
+        hr[4] = acc[2];
+        hr[5] = alpha;
+        hr[6] = u;
+        hr[7] = log_z;
+    }
+    free(x); free(lw); free(w); free(incw); free(ctrs); free(counts); free(parents);
+    return rc;
+}

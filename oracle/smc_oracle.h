@@ -87,6 +87,18 @@ typedef struct orc_pf_sys {
 int orc_pf_step(orc_pf_sys *s, const double *obs_t, double *hist_row, int nthreads);
 int orc_pf_initialize(orc_pf_sys *s, const double *obs0, double *hist_row, int nthreads);
 
+/* ---- example-gmm ---- */
+#define ORC_GMM_R 4
+#define ORC_GMM_ROW 16
+double orc_gmm_llh(const double *row, const double *y, int nd);
+double orc_gmm_lprior(const double *row, const double *h5);
+void orc_gmm_init(double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
+                  const double *h5, int nthreads);
+int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y,
+                   int nd, const double *h5, double alpha, double sd, int nthreads);
+int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                const double *h5, int T, double power, double *hist, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -415,9 +415,10 @@ class Sampler:
                     value.copy_inplace(sysm.parents, gate)
             ws.set_equal_weight_if(gate, sysm.n_total)
         self._mark("resample", 1)
-        if self.mcmc_queue and hasattr(sysm.value, "materialize"):
+        mcmc = self.mcmc_queue if t > 0 else []  # initialize() runs no mcmc
+        if mcmc and hasattr(sysm.value, "materialize"):
             sysm.value.materialize()  # mcmc kernels update the state in place
-        for op in self.mcmc_queue:
+        for op in mcmc:
             accs.append(apply_move(op, sysm, t))
         for k, a in enumerate(accs):
             if isinstance(a, torch.Tensor):
@@ -426,10 +427,10 @@ class Sampler:
                 row[2 + k].fill_(float(a))
         self._mark("monitor", 0)
         if self.path is not None:
-            alpha, integrand = apply_path_eval(self.path, sysm, t)
+            alpha, integrand, ld = apply_path_eval(self.path, sysm, t)
             self._path_grid.append(alpha)
             row[self._col["path.grid"]].fill_(alpha)
-            self._reduce(integrand, 1, 1, row, self._col["path.integrand"])
+            self._reduce(integrand, ld, 1, row, self._col["path.integrand"])
         for name, rec in self.monitors.items():
             col = self._col[f"{name}.0"]
             fw = getattr(rec.eval, "fused_with", None)

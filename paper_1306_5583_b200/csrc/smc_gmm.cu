@@ -1,0 +1,301 @@
+// smc_gmm.cu -- the paper's Gaussian-mixture SMC sampler (
+// PAPER.md:1516-1981; config 3): tempered targets pi_alpha ∝ prior * lik^alpha,
+// three-block random-walk Metropolis moves, direct (NC) and path-sampling log Z.
+//
+// State: N x 16 f64 row-major (128 B = 4 sectors per particle):
+//   [0,4) mu, [4,8) lambda, [8,12) omega, 12 log_prior, 13 log_likelihood.
+// The data (n <= 4096 doubles) is staged once per block in shared memory; the
+// likelihood loop is the hot spot: per data point r exp + 1 log (FP64 bound).
+#include "smc_weights.cuh"
+
+using namespace smc;
+
+namespace {
+
+constexpr int GB = 128;  // threads per block (register-heavy per-particle loops)
+constexpr int R = 4;     // mixture components (the paper's 4-component model)
+constexpr int W = SMC_GMM_ROW;
+
+struct Hyper {
+    double xi, kappa, nu, chi, rho;
+    double lgamma_nu, log_chi, log_kappa_2pi, dir_const;
+};
+
+struct Param {
+    double mu[R], lam[R], om[R];
+};
+
+SMC_DEV void load_param(const double *row, Param &p)
+{
+#pragma unroll
+    for (int j = 0; j < R; ++j) { p.mu[j] = row[j]; p.lam[j] = row[R + j]; p.om[j] = row[2 * R + j]; }
+}
+
+// update_log_likelihood: -n/2 log 2pi + sum_k log sum_j w_j exp(.5 log l_j - .5 l_j r^2)
+SMC_DEV double log_likelihood(const Param &p, const double *__restrict__ y, int nd)
+{
+    double ll = -0.5 * (double)nd * 1.8378770664093455;
+    double ll_j[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) ll_j[j] = log(p.lam[j]);  // update_log_lambda
+    for (int k = 0; k < nd; ++k) {
+        const double yk = y[k];
+        double lli = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const double resid = yk - p.mu[j];
+            lli += p.om[j] * exp(0.5 * ll_j[j] - 0.5 * p.lam[j] * resid * resid);
+        }
+        ll += smc_fm::log(lli);
+    }
+    return ll;
+}
+
+// update_log_prior: Normal(xi, 1/kappa) per mu, Gamma(nu, chi) per
+// lambda, symmetric Dirichlet(rho) for omega.
+SMC_DEV double log_prior(const Param &p, const Hyper &h)
+{
+    double lp = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const double d = p.mu[j] - h.xi;
+        lp += h.log_kappa_2pi * 0.5 - 0.5 * h.kappa * d * d;
+        lp += (h.nu - 1) * log(p.lam[j]) - p.lam[j] / h.chi - h.lgamma_nu - h.nu * h.log_chi;
+        if (h.rho != 1.0) lp += (h.rho - 1) * log(p.om[j]);
+    }
+    return lp + h.dir_const;
+}
+
+SMC_DEV void stage_data(const double *__restrict__ data, int nd, double *s_y)
+{
+    for (int k = threadIdx.x; k < nd; k += blockDim.x) s_y[k] = data[k];
+    __syncthreads();
+}
+
+// gmm_init::initialize_state: per component, in order,
+// mu ~ N(mu0, sd0), lambda ~ Gamma(shape0, scale0), weight ~ Gamma(1, 1); normalize.
+__global__ void __launch_bounds__(GB) k_gmm_init(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
+                                                 uint64_t *__restrict__ ctrs, const double *__restrict__ data, int nd,
+                                                 Hyper h)
+{
+    extern __shared__ double s_y[];
+    stage_data(data, nd, s_y);
+    const int64_t i = (int64_t)blockIdx.x * GB + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t si = sbase + (uint64_t)i;
+    uint64_t c = ctrs[i];
+    Param p;
+    const double sd0 = 1.0 / sqrt(h.kappa);
+    double sum = 0;
+    for (int j = 0; j < R; ++j) {
+        p.mu[j] = h.xi + sd0 * normal_at(c, si, key);
+        c += 2;
+        p.lam[j] = h.chi * gamma_from(c, si, key, h.nu);
+        p.om[j] = 1.0 * gamma_from(c, si, key, 1.0);
+        sum += p.om[j];
+    }
+    for (int j = 0; j < R; ++j) p.om[j] /= sum;
+    ctrs[i] = c;
+    double *row = x + i * W;
+#pragma unroll
+    for (int j = 0; j < R; ++j) { row[j] = p.mu[j]; row[R + j] = p.lam[j]; row[2 * R + j] = p.om[j]; }
+    row[12] = log_prior(p, h);
+    row[13] = log_likelihood(p, s_y, nd);
+}
+
+// gmm_move_smc: incw = dalpha * llh; nc_add_log_weight then
+// add_log_weight -- fused with the one-pass lse partials.
+__global__ void __launch_bounds__(256) k_gmm_reweight(const double *__restrict__ x, double *__restrict__ lw_raw,
+                                                      int64_t n, double dalpha, smc_wstate *st,
+                                                      LsePartial *__restrict__ parts)
+{
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    double v = -INFINITY;
+    if (i < n) {
+        const NormLw nl = norm_of(st);
+        const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
+        v = prev + dalpha * x[i * W + 13];
+        if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+        lw_raw[i] = v;
+    }
+    LsePartial p = block_lse_partial<256>(v);
+    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+}
+
+// gmm_move_mu / _lambda / _weight: random walk,
+// recompute caches, accept iff log U < p_new - p_old (+ Jacobian).  Draws: the block's
+// normals in component order, then one uniform.
+template <int BLOCK>
+__global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
+                                               uint64_t *__restrict__ ctrs, const double *__restrict__ data, int nd,
+                                               Hyper h, double alpha, double sd,
+                                               unsigned long long *__restrict__ accepted)
+{
+    extern __shared__ double s_y[];
+    stage_data(data, nd, s_y);
+    const int64_t i = (int64_t)blockIdx.x * GB + threadIdx.x;
+    int acc = 0;
+    if (i < n) {
+        double *row = x + i * W;
+        Param p;
+        load_param(row, p);
+        const double lp_old = row[12], ll_old = row[13];
+        const double p_old = lp_old + alpha * ll_old;
+        const uint64_t si = sbase + (uint64_t)i;
+        uint64_t c = ctrs[i];
+        double jac = 0;
+        if (BLOCK == 0) {  // mu_j += N(0, mu_sd)
+#pragma unroll
+            for (int j = 0; j < R; ++j) { p.mu[j] += 0.0 + sd * normal_at(c, si, key); c += 2; }
+        } else if (BLOCK == 1) {  // log-scale walk on lambda, Jacobian sum(log l_new - log l_old)
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const double old = p.lam[j];
+                p.lam[j] = old * exp(0.0 + sd * normal_at(c, si, key));
+                c += 2;
+                jac += log(p.lam[j]) - log(old);
+            }
+        } else {  // logit walk on omega (omega_R reference), Jacobian sum_j (log w_new - log w_old)
+            double g[R];
+#pragma unroll
+            for (int j = 0; j < R; ++j) jac -= log(p.om[j]);
+#pragma unroll
+            for (int j = 0; j < R - 1; ++j) {
+                g[j] = log(p.om[j] / p.om[R - 1]) + (0.0 + sd * normal_at(c, si, key));
+                c += 2;
+            }
+            g[R - 1] = 0.0;
+            double gm = g[0];
+#pragma unroll
+            for (int j = 1; j < R; ++j) gm = fmax(gm, g[j]);
+            double s = 0;
+#pragma unroll
+            for (int j = 0; j < R; ++j) { p.om[j] = exp(g[j] - gm); s += p.om[j]; }
+#pragma unroll
+            for (int j = 0; j < R; ++j) { p.om[j] /= s; jac += log(p.om[j]); }
+        }
+        const double lp_new = log_prior(p, h);
+        const double ll_new = log_likelihood(p, s_y, nd);
+        const double dp = lp_new + alpha * ll_new - p_old + jac;
+        const double u = log(u01_at(c, si, key));
+        c += 1;
+        ctrs[i] = c;
+        if (u < dp) {  // accept (strict)
+#pragma unroll
+            for (int j = 0; j < R; ++j) { row[j] = p.mu[j]; row[R + j] = p.lam[j]; row[2 * R + j] = p.om[j]; }
+            row[12] = lp_new;
+            row[13] = ll_new;
+            acc = 1;
+        }
+    }
+    // acceptance count: block sum, one integer atomic (order-free, exact)
+    __shared__ int s_acc[GB / 32];
+    const int a = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < GB / 32; ++w) t += s_acc[w];
+        if (t) atomicAdd(accepted, (unsigned long long)t);
+    }
+}
+
+// log-prior / log-likelihood of given parameter rows (the cache-coherence hook).
+__global__ void __launch_bounds__(GB) k_gmm_eval(double *__restrict__ x, int64_t n, const double *__restrict__ data,
+                                                 int nd, Hyper h)
+{
+    extern __shared__ double s_y[];
+    stage_data(data, nd, s_y);
+    const int64_t i = (int64_t)blockIdx.x * GB + threadIdx.x;
+    if (i >= n) return;
+    double *row = x + i * W;
+    Param p;
+    load_param(row, p);
+    row[12] = log_prior(p, h);
+    row[13] = log_likelihood(p, s_y, nd);
+}
+
+Hyper make_hyper(const double *hyper5)
+{
+    Hyper h;
+    h.xi = hyper5[0];
+    h.kappa = hyper5[1];
+    h.nu = hyper5[2];
+    h.chi = hyper5[3];
+    h.rho = hyper5[4];
+    h.lgamma_nu = lgamma(h.nu);
+    h.log_chi = log(h.chi);
+    h.log_kappa_2pi = log(h.kappa / (2.0 * 3.141592653589793));
+    h.dir_const = lgamma(R * h.rho) - R * lgamma(h.rho);  // Dirichlet normalizer (ln (r-1)! at rho = 1)
+    return h;
+}
+
+int gmm_check(const double *x, int64_t n, const double *data, int nd, const double *hyper, const char *who)
+{
+    if (!x || n < 1 || n >= ((int64_t)1 << 31) || !data || nd < 1 || nd > SMC_GMM_MAX_DATA || !hyper)
+        return smc_set_error(SMC_EINVAL, "%s: bad args", who);
+    if (!(hyper[1] > 0 && hyper[2] > 0 && hyper[3] > 0 && hyper[4] > 0))
+        return smc_set_error(SMC_EINVAL, "%s: hyperparameters must be positive", who);
+    return SMC_OK;
+}
+
+}  // namespace
+
+extern "C" int smc_gmm_init(double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs, const double *data,
+                            int nd, const double *hyper, void *stream)
+{
+    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_init");
+    if (rc) return rc;
+    if (!ctrs) return smc_set_error(SMC_EINVAL, "smc_gmm_init: ctrs");
+    k_gmm_init<<<(unsigned)((n + GB - 1) / GB), GB, nd * sizeof(double), (cudaStream_t)stream>>>(
+        x, n, stream_base, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, data, nd, make_hyper(hyper));
+    return smc_check_launch("smc_gmm_init");
+}
+
+extern "C" int smc_gmm_eval(double *x, int64_t n, const double *data, int nd, const double *hyper, void *stream)
+{
+    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_eval");
+    if (rc) return rc;
+    k_gmm_eval<<<(unsigned)((n + GB - 1) / GB), GB, nd * sizeof(double), (cudaStream_t)stream>>>(x, n, data, nd,
+                                                                                               make_hyper(hyper));
+    return smc_check_launch("smc_gmm_eval");
+}
+
+extern "C" size_t smc_gmm_workspace_bytes(int64_t n)
+{
+    return (size_t)((n + 255) / 256 + 1) * sizeof(LsePartial) + smc_lse_scratch_bytes() + 512;
+}
+
+extern "C" int smc_gmm_reweight(const double *x, double *lw_raw, int64_t n, double dalpha, smc_wstate *st,
+                                double *partial_out, void *ws, size_t ws_bytes, void *stream)
+{
+    if (!x || !lw_raw || !st || n < 1 || n >= ((int64_t)1 << 31))
+        return smc_set_error(SMC_EINVAL, "smc_gmm_reweight: bad args");
+    if (!ws || ws_bytes < smc_gmm_workspace_bytes(n)) return smc_set_error(SMC_EWORKSPACE, "smc_gmm_reweight: ws");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nb = (int)((n + 255) / 256);
+    LsePartial *parts = (LsePartial *)ws;
+    void *scratch = (char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255);
+    k_gmm_reweight<<<nb, 256, 0, s>>>(x, lw_raw, n, dalpha, st, parts);
+    smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
+    return smc_check_launch("smc_gmm_reweight");
+}
+
+extern "C" int smc_gmm_mh(int block, double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+                          const double *data, int nd, const double *hyper, double alpha, double sd,
+                          unsigned long long *accepted, void *stream)
+{
+    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_mh");
+    if (rc) return rc;
+    if (!ctrs || !accepted || block < 0 || block > 2 || !(sd >= 0))
+        return smc_set_error(SMC_EINVAL, "smc_gmm_mh: bad args");
+    cudaStream_t s = (cudaStream_t)stream;
+    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const Hyper h = make_hyper(hyper);
+    const unsigned nb = (unsigned)((n + GB - 1) / GB);
+    const size_t sm = nd * sizeof(double);
+    if (block == 0) k_gmm_mh<0><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
+    else if (block == 1) k_gmm_mh<1><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
+    else k_gmm_mh<2><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
+    return smc_check_launch("smc_gmm_mh");
+}

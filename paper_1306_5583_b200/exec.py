@@ -100,5 +100,8 @@ class PathEval:
 
 
 def apply_path_eval(ev, system, iter_):
-    alpha, integrand = ev(iter_, system)
-    return float(alpha), integrand
+    """-> (alpha_t, vals, ld): integrand_i = vals[i * ld] (ld = 1 for a plain vector)."""
+    r = ev(iter_, system)
+    if len(r) == 3:
+        return float(r[0]), r[1], int(r[2])
+    return float(r[0]), r[1], 1

@@ -57,6 +57,11 @@ class WeightSet:
             self.clear_status()
             raise _abi.SmcError(code, "device-side weight failure")
 
+    def reset_log_zconst(self):
+        """NormalizingConstant::initialize (PAPER.md:1808): log Z accumulator back to 0."""
+        off = _abi.WSTATE_OFF["log_zconst"]
+        self.state[off:off + 8].zero_()
+
     def clear_status(self):
         off = _abi.WSTATE_OFF["status"]
         self.state[off:off + 4].zero_()
