@@ -21,9 +21,11 @@
 
 #ifdef __CUDACC__
 #define SMC_HD __host__ __device__ __forceinline__
+#define SMC_HDM __host__ __device__ __forceinline__
 #define SMC_TABLE __device__ const
 #else
 #define SMC_HD static inline
+#define SMC_HDM inline
 #define SMC_TABLE static const
 #endif
 
@@ -157,5 +159,69 @@ SMC_HD double cos(double x)
     }
     return res;
 }
+
+// exp(x) for the GMM likelihood (smc_gmm.cu).  x = (128 m + j) ln2/128 + r with
+// |r| <= ln2/256; exp(r) - 1 by a degree-5 Taylor polynomial (truncation
+// < 2^-60); 2^(j/128) as hi + lo from kExpTab.  Subnormal results are scaled in
+// two steps; overflow gives +inf; NaN propagates.  No libm call, no branch.  The table is passed in so the device can
+// stage it in shared memory (one LDS.128 per call instead of a global gather).
+struct ExpEntry {
+    double hi, lo;
+};
+
+SMC_TABLE ExpEntry kExpTab[128] = {
+#include "smc_exptab.inc"
+};
+
+SMC_HD double exp(double x, const ExpEntry *tab)
+{
+    // Branch-free so that independent calls interleave.  Outside [-746, ln DBL_MAX]
+    // the reduction below is garbage and the final selects return 0 / +inf; NaN
+    // fails both comparisons and propagates through the arithmetic.
+    const double XMAX = 0x1.62e42fefa39efp+9;  // 709.78271289338397 = ln(DBL_MAX) rounded down
+    const double SH = 0x1.8p52;
+    double kd = fma_(x, 0x1.71547652b82fep+7, SH);
+    const int64_t k = (int32_t)(uint32_t)bits(kd);  // round(x 128/ln2) from the shifter's low word
+    kd -= SH;
+    double r = fma_(-kd, 0x1.62e42fefc0000p-8, x);
+    r = fma_(-kd, -0x1.c610ca86c3899p-44, r);
+    double p = fma_(r, 1.0 / 120, 1.0 / 24);
+    p = fma_(r, p, 1.0 / 6);
+    p = fma_(r, p, 0.5);
+    p = fma_(r * r, p, r);
+    const ExpEntry t = tab[k & 127];
+    const double m = fma_(t.hi, p, t.lo) + t.hi;  // 2^(j/128) exp(r), in [1, 2)
+    const int64_t e = k >> 7;
+    // subnormal results are scaled in two steps so the only rounding is the final multiply
+    const bool tiny = e < -1020;
+    const double res = from_bits(bits(m) + ((uint64_t)(tiny ? e + 600 : e) << 52)) * (tiny ? 0x1p-600 : 1.0);
+    return x < -746.0 ? 0.0 : (x > XMAX ? INFINITY : res);  // exp(-746) rounds to +0
+}
+
+// sum_k log(v_k) as one log of a running product: the product's exponent is
+// peeled off after every factor (integer ops), so the mantissa stays in [1, 2);
+// zero, subnormal or non-finite products take one libm-class log each.
+struct LogProd {
+    double m = 1.0, acc = 0.0;
+    int64_t ex = 0;
+    SMC_HDM void add(double v)
+    {
+        m *= v;
+        const uint64_t b = bits(m);
+        const int64_t e = (int64_t)((b >> 52) & 0x7ff);
+        if (e == 0 || e == 0x7ff) {
+            acc += smc_fm::log(m);
+            m = 1.0;
+        } else {
+            ex += e - 1023;
+            m = from_bits((b & 0x800fffffffffffffull) | 0x3ff0000000000000ull);
+        }
+    }
+    SMC_HDM double result() const
+    {
+        const double e = (double)ex;  // e LN2_HI is exact for |e| < 2^11, rounded once beyond
+        return acc + (e * 0x1.62e42fefa3800p-1 + (smc_fm::log(m) + e * 0x1.ef35793c76730p-45));
+    }
+};
 
 }  // namespace smc_fm

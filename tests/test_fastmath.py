@@ -23,15 +23,22 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_cos):
+    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp):
         f.argtypes = [P, P, ctypes.c_long]
+    lib.fm_logprod.argtypes = [P, ctypes.c_long]
+    lib.fm_logprod.restype = ctypes.c_double
 
     def call(f, x):
         x = np.ascontiguousarray(x, np.float64)
         y = np.empty_like(x)
         f(x, y, x.size)
         return y
-    return lambda name, x: call(getattr(lib, name), x)
+    def run(name, x):
+        if name == "fm_logprod":
+            x = np.ascontiguousarray(x, np.float64)
+            return lib.fm_logprod(x, x.size)
+        return call(getattr(lib, name), x)
+    return run
 
 
 def ulp_err(got, exact_decimals):
@@ -92,3 +99,41 @@ def test_agrees_with_glibc_bulk(fm):
     a, b = fm("fm_cos", xc), np.cos(xc)
     assert np.max(np.abs(a - b) / np.spacing(np.maximum(np.abs(b), 2.0 ** -30))) <= 1.0
     assert np.mean(a == b) > 0.95
+
+
+def test_exp_exact_ulp(fm):
+    """smc_fm::exp (GMM likelihood): <= 0.52 ulp against 60-digit exp."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(4)
+    xs = np.concatenate([rng.uniform(-707.9, 707.9, 3000), rng.uniform(-1, 1, 3000), rng.uniform(-40, 0, 3000),
+                         rng.uniform(-1e-6, 1e-6, 500), [0.0, -0.0, 1.0, -1.0, 707.5, -707.5, 1e-300]])
+    got = fm("fm_exp", xs)
+    exact = [decimal.Decimal(float(x)).exp() for x in xs]
+    assert ulp_err(got, exact) <= 0.52
+    # overflow side (libm), subnormal results, underflow to 0, +-inf
+    edge = np.array([709.0, -708.5, -720.0, -730.3, -744.4, -745.0, -745.2, -746.0, -1e4, np.inf, -np.inf, 710.0])
+    with np.errstate(over="ignore"):
+        np.testing.assert_array_equal(fm("fm_exp", edge), np.exp(edge))
+    assert np.isnan(fm("fm_exp", np.array([np.nan])))[0]
+
+
+def test_exp_agrees_with_glibc_bulk(fm):
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-700, 700, 1_000_000), rng.uniform(-30, 3, 1_000_000)])
+    a, b = fm("fm_exp", x), np.exp(x)
+    assert np.max(np.abs(a - b) / np.spacing(b)) <= 1.0
+    # both are ~0.51-ulp functions (glibc's bound is 0.511): they differ only where the
+    # exact value lies within a few hundredths of an ulp of a rounding midpoint
+    assert np.mean(a == b) > 0.9
+
+
+def test_logprod_matches_sum_of_logs(fm):
+    """LogProd: one log of a renormalized running product == sum of logs (GMM llh)."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(6)
+    for v in (rng.uniform(1e-3, 2.0, 1000), np.exp(rng.uniform(-300, 5, 1000)), np.full(1000, 1e-200),
+              np.array([1e-310, 0.5, 3e-320, 2.0]), rng.uniform(0.9, 1.1, 4096)):
+        exact = sum(decimal.Decimal(float(t)).ln() for t in v)
+        got = fm("fm_logprod", v)
+        assert abs(decimal.Decimal(got) - exact) <= decimal.Decimal(1e-15) * max(1, abs(exact)), (got, exact)
+    assert fm("fm_logprod", np.array([0.5, 0.0, 2.0])) == -np.inf
