@@ -256,26 +256,30 @@ int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int
 /* lambda,weight} / gmm_path          */
 /* ------------------------------------------------------------------------ */
 /* State: n x SMC_GMM_ROW f64 row-major per particle: mu[4], lambda[4],
- * omega[4], log_prior, log_likelihood, 2 pad.  data: the observations (device,
- * nd <= SMC_GMM_MAX_DATA).  hyper (host, 5 doubles): xi, kappa, nu, chi, rho of
- * mu ~ N(xi, 1/kappa), lambda ~ Gamma(nu, scale chi), omega ~ Dirichlet(rho). */
+ * omega[4], log_prior, log_likelihood, 2 pad; components j < r (1 <= r <=
+ * SMC_GMM_MAX_R) are live, the rest stay 0.  data: the observations (device,
+ * nd <= SMC_GMM_MAX_DATA).  hyper (host, 6 doubles): xi, kappa, nu, chi, rho,
+ * lambda_known of mu ~ N(xi, 1/kappa), lambda ~ Gamma(nu, scale chi), omega ~
+ * Dirichlet(rho); lambda_known > 0 fixes every lambda_j at that precision (no
+ * Gamma term, no lambda move: the conjugate-oracle model of SPEC.md:586-587). */
 #define SMC_GMM_ROW 16
+#define SMC_GMM_MAX_R 4
 #define SMC_GMM_MAX_DATA 4096
-/* gmm_init: per component mu, lambda, Gamma(1,1) weight (in
- * that order, from stream stream_base + i); weights normalized; caches set. */
-int smc_gmm_init(double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs, const double *data,
-                 int nd, const double *hyper, void *stream);
+/* gmm_init: per component mu, lambda (unless known), Gamma(1,1)
+ * weight (in that order, from stream stream_base + i); weights normalized; caches set. */
+int smc_gmm_init(double *x, int64_t n, int r, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+                 const double *data, int nd, const double *hyper, void *stream);
 /* Recompute the log_prior / log_likelihood caches of every row. */
-int smc_gmm_eval(double *x, int64_t n, const double *data, int nd, const double *hyper, void *stream);
+int smc_gmm_eval(double *x, int64_t n, int r, const double *data, int nd, const double *hyper, void *stream);
 size_t smc_gmm_workspace_bytes(int64_t n);
 /* gmm_move_smc's weight update: incw_i = dalpha * llh_i,
  * log_zconst += log sum W_{t-1} exp(incw), add_log_weight(incw) -- fused. */
 int smc_gmm_reweight(const double *x, double *lw_raw, int64_t n, double dalpha, smc_wstate *ws_state,
                      double *partial_out, void *ws, size_t ws_bytes, void *stream);
-/* gmm_move_mu (block 0), _lambda (1, log scale), _weight (2, logits) random-walk
+/* gmm_move_mu (block 0), _lambda (1, log scale), _weight (2, r-1 logits) random-walk
  * Metropolis at temperature alpha with proposal scale sd:
  * accept iff log U < p_new - p_old (+ Jacobian); *accepted += #accepted. */
-int smc_gmm_mh(int block, double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+int smc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
                const double *data, int nd, const double *hyper, double alpha, double sd,
                unsigned long long *accepted, void *stream);
 

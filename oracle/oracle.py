@@ -232,50 +232,53 @@ def _gmm_sigs():
     if getattr(L, "_gmm_ok", False):
         return L
     L.orc_gmm_llh.restype = C.c_double
-    L.orc_gmm_llh.argtypes = [_f64, _f64, C.c_int]
+    L.orc_gmm_llh.argtypes = [_f64, C.c_int, _f64, C.c_int]
     L.orc_gmm_lprior.restype = C.c_double
-    L.orc_gmm_lprior.argtypes = [_f64, _f64]
-    L.orc_gmm_init.argtypes = [_f64, C.c_int64, _u64, C.c_uint32, C.c_uint32, _f64, C.c_int, _f64, C.c_int]
+    L.orc_gmm_lprior.argtypes = [_f64, C.c_int, _f64]
+    L.orc_gmm_init.argtypes = [_f64, C.c_int64, C.c_int, _u64, C.c_uint32, C.c_uint32, _f64, C.c_int, _f64, C.c_int]
     L.orc_gmm_mh.restype = C.c_int64
-    L.orc_gmm_mh.argtypes = [C.c_int, _f64, C.c_int64, _u64, C.c_uint32, C.c_uint32, _f64, C.c_int, _f64,
+    L.orc_gmm_mh.argtypes = [C.c_int, _f64, C.c_int64, C.c_int, _u64, C.c_uint32, C.c_uint32, _f64, C.c_int, _f64,
                              C.c_double, C.c_double, C.c_int]
-    L.orc_gmm_run.argtypes = [C.c_int64, C.c_uint64, C.c_int, C.c_double, _f64, C.c_int, _f64, C.c_int,
+    L.orc_gmm_run.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_double, _f64, C.c_int, _f64, C.c_int,
                               C.c_double, _f64, C.c_int]
     L._gmm_ok = True
     return L
 
 
-def gmm_llh(row, y):
-    return _gmm_sigs().orc_gmm_llh(np.ascontiguousarray(row, np.float64), np.ascontiguousarray(y, np.float64),
+def _h6(h):
+    h = list(h) + [0.0] * (6 - len(h))
+    return np.ascontiguousarray(h[:6], np.float64)
+
+
+def gmm_llh(row, y, r=4):
+    return _gmm_sigs().orc_gmm_llh(np.ascontiguousarray(row, np.float64), r, np.ascontiguousarray(y, np.float64),
                                    len(y))
 
 
-def gmm_lprior(row, h5):
-    return _gmm_sigs().orc_gmm_lprior(np.ascontiguousarray(row, np.float64), np.ascontiguousarray(h5, np.float64))
+def gmm_lprior(row, h, r=4):
+    return _gmm_sigs().orc_gmm_lprior(np.ascontiguousarray(row, np.float64), r, _h6(h))
 
 
-def gmm_init(n, streams, y, h5, nthreads=1):
+def gmm_init(n, streams, y, h, r=4, nthreads=1):
     x = np.zeros((n, 16), np.float64)
     y = np.ascontiguousarray(y, np.float64)
-    _gmm_sigs().orc_gmm_init(x, n, streams.counters, streams.k0, streams.k1, y, len(y),
-                             np.ascontiguousarray(h5, np.float64), nthreads)
+    _gmm_sigs().orc_gmm_init(x, n, r, streams.counters, streams.k0, streams.k1, y, len(y), _h6(h), nthreads)
     return x
 
 
-def gmm_mh(block, x, streams, y, h5, alpha, sd, nthreads=1):
+def gmm_mh(block, x, streams, y, h, alpha, sd, r=4, nthreads=1):
     y = np.ascontiguousarray(y, np.float64)
-    return _gmm_sigs().orc_gmm_mh(block, x, x.shape[0], streams.counters, streams.k0, streams.k1, y, len(y),
-                                  np.ascontiguousarray(h5, np.float64), alpha, sd, nthreads)
+    return _gmm_sigs().orc_gmm_mh(block, x, x.shape[0], r, streams.counters, streams.k0, streams.k1, y, len(y),
+                                  _h6(h), alpha, sd, nthreads)
 
 
-def gmm_run(n, seed, scheme, threshold, y, h5, T, power, nthreads=1):
+def gmm_run(n, seed, scheme, threshold, y, h, T, power, r=4, nthreads=1):
     """hist (T+1) x 8: ess_over_n resampled acc_mu acc_lambda acc_weight alpha U_t log_zconst."""
     if isinstance(scheme, str):
         scheme = SCHEMES[scheme]
     y = np.ascontiguousarray(y, np.float64)
     hist = np.zeros((T + 1, 8), np.float64)
-    rc = _gmm_sigs().orc_gmm_run(n, seed, scheme, threshold, y, len(y), np.ascontiguousarray(h5, np.float64), T,
-                                 power, hist, nthreads)
+    rc = _gmm_sigs().orc_gmm_run(n, r, seed, scheme, threshold, y, len(y), _h6(h), T, power, hist, nthreads)
     if rc:
         raise OracleError(f"gmm_run rc={rc}")
     return hist

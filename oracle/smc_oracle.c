@@ -540,25 +540,26 @@ int orc_pf_run(int64_t n, uint64_t seed, int scheme, double threshold, const dou
 /* state row: mu[4] lambda[4] omega[4] log_prior log_likelihood pad pad       */
 /* ------------------------------------------------------------------------- */
 
-static void gmm_hyper_derive(const double *h5, double *h)
+static void gmm_hyper_derive(const double *h6, int r, double *h)
 {
-    /* h: xi kappa nu chi rho | lgamma(nu) log(chi) log(kappa/2pi) dirichlet_const */
-    for (int k = 0; k < 5; ++k) h[k] = h5[k];
-    h[5] = lgamma(h[2]);
-    h[6] = log(h[3]);
-    h[7] = log(h[1] / (2.0 * 3.141592653589793));
-    h[8] = lgamma(ORC_GMM_R * h[4]) - ORC_GMM_R * lgamma(h[4]);
+    /* h: xi kappa nu chi rho lambda_known | lgamma(nu) log(chi) log(kappa/2pi) dirichlet_const */
+    for (int k = 0; k < 6; ++k) h[k] = h6[k];
+    h[6] = lgamma(h[2]);
+    h[7] = log(h[3]);
+    h[8] = log(h[1] / (2.0 * 3.141592653589793));
+    h[9] = lgamma(r * h[4]) - r * lgamma(h[4]);
 }
 
-/* update_log_likelihood */
-double orc_gmm_llh(const double *row, const double *y, int nd)
+/* update_log_likelihood:
+ * -n/2 log 2pi + sum_k log sum_{j<r} w_j exp(.5 log l_j - .5 l_j (y_k - mu_j)^2) */
+double orc_gmm_llh(const double *row, int r, const double *y, int nd)
 {
     double ll = -0.5 * (double)nd * 1.8378770664093455;
     double lj[ORC_GMM_R];
-    for (int j = 0; j < ORC_GMM_R; ++j) lj[j] = log(row[ORC_GMM_R + j]);
+    for (int j = 0; j < r; ++j) lj[j] = log(row[ORC_GMM_R + j]);
     for (int k = 0; k < nd; ++k) {
         double lli = 0;
-        for (int j = 0; j < ORC_GMM_R; ++j) {
+        for (int j = 0; j < r; ++j) {
             double resid = y[k] - row[j];
             lli += row[2 * ORC_GMM_R + j] * exp(0.5 * lj[j] - 0.5 * row[ORC_GMM_R + j] * resid * resid);
         }
@@ -567,50 +568,55 @@ double orc_gmm_llh(const double *row, const double *y, int nd)
     return ll;
 }
 
-/* update_log_prior */
-double orc_gmm_lprior(const double *row, const double *h5)
+/* update_log_prior: Normal(xi, 1/kappa) per mu, Gamma(nu, scale chi) per lambda
+ * (absent when lambda is known), symmetric Dirichlet(rho) on omega */
+double orc_gmm_lprior(const double *row, int r, const double *h6)
 {
-    double h[9];
-    gmm_hyper_derive(h5, h);
+    double h[10];
+    gmm_hyper_derive(h6, r, h);
     double lp = 0;
-    for (int j = 0; j < ORC_GMM_R; ++j) {
+    for (int j = 0; j < r; ++j) {
         double d = row[j] - h[0];
-        lp += h[7] * 0.5 - 0.5 * h[1] * d * d;
-        double lam = row[ORC_GMM_R + j];
-        lp += (h[2] - 1) * log(lam) - lam / h[3] - h[5] - h[2] * h[6];
+        lp += h[8] * 0.5 - 0.5 * h[1] * d * d;
+        if (!(h[5] > 0)) {
+            double lam = row[ORC_GMM_R + j];
+            lp += (h[2] - 1) * log(lam) - lam / h[3] - h[6] - h[2] * h[7];
+        }
         if (h[4] != 1.0) lp += (h[4] - 1) * log(row[2 * ORC_GMM_R + j]);
     }
-    return lp + h[8];
+    return lp + h[9];
 }
 
-/* gmm_init::initialize_state for particles [0, n) */
-void orc_gmm_init(double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
-                  const double *h5, int nthreads)
+/* gmm_init::initialize_state for particles [0, n): per component in
+ * order mu ~ N(xi, 1/kappa), lambda ~ Gamma(nu, chi) (unless known), omega ~ Gamma(1, 1);
+ * normalize omega */
+void orc_gmm_init(double *x, int64_t n, int r, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
+                  const double *h6, int nthreads)
 {
-    const double sd0 = 1.0 / sqrt(h5[1]);
+    const double sd0 = 1.0 / sqrt(h6[1]);
 #ifdef _OPENMP
 #pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
 #endif
     for (int64_t i = 0; i < n; ++i) {
         double *row = x + ORC_GMM_ROW * i;
         double sum = 0;
-        for (int j = 0; j < ORC_GMM_R; ++j) {
-            row[j] = h5[0] + sd0 * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
-            row[ORC_GMM_R + j] = h5[3] * orc_std_gamma(ctrs, (uint64_t)i, k0, k1, h5[2]);
+        memset(row, 0, sizeof(double) * ORC_GMM_ROW);
+        for (int j = 0; j < r; ++j) {
+            row[j] = h6[0] + sd0 * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
+            row[ORC_GMM_R + j] = h6[5] > 0 ? h6[5] : h6[3] * orc_std_gamma(ctrs, (uint64_t)i, k0, k1, h6[2]);
             row[2 * ORC_GMM_R + j] = 1.0 * orc_std_gamma(ctrs, (uint64_t)i, k0, k1, 1.0);
             sum += row[2 * ORC_GMM_R + j];
         }
-        for (int j = 0; j < ORC_GMM_R; ++j) row[2 * ORC_GMM_R + j] /= sum;
-        row[12] = orc_gmm_lprior(row, h5);
-        row[13] = orc_gmm_llh(row, y, nd);
-        row[14] = row[15] = 0.0;
+        for (int j = 0; j < r; ++j) row[2 * ORC_GMM_R + j] /= sum;
+        row[12] = orc_gmm_lprior(row, r, h6);
+        row[13] = orc_gmm_llh(row, r, y, nd);
     }
     (void)nthreads;
 }
 
 /* gmm_move_{mu,lambda,weight}: returns #accepted */
-int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y,
-                   int nd, const double *h5, double alpha, double sd, int nthreads)
+int64_t orc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t *ctrs, uint32_t k0, uint32_t k1,
+                   const double *y, int nd, const double *h6, double alpha, double sd, int nthreads)
 {
     int64_t acc = 0;
 #ifdef _OPENMP
@@ -623,9 +629,9 @@ int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0,
         double p_old = row[12] + alpha * row[13];
         double jac = 0;
         if (block == 0) {
-            for (int j = 0; j < ORC_GMM_R; ++j) p[j] += 0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
+            for (int j = 0; j < r; ++j) p[j] += 0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1);
         } else if (block == 1) {
-            for (int j = 0; j < ORC_GMM_R; ++j) {
+            for (int j = 0; j < r; ++j) {
                 double old = p[ORC_GMM_R + j];
                 p[ORC_GMM_R + j] = old * exp(0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1));
                 jac += log(p[ORC_GMM_R + j]) - log(old);
@@ -633,17 +639,17 @@ int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0,
         } else {
             double g[ORC_GMM_R];
             double *om = p + 2 * ORC_GMM_R;
-            for (int j = 0; j < ORC_GMM_R; ++j) jac -= log(om[j]);
-            for (int j = 0; j < ORC_GMM_R - 1; ++j)
-                g[j] = log(om[j] / om[ORC_GMM_R - 1]) + (0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1));
-            g[ORC_GMM_R - 1] = 0.0;
+            for (int j = 0; j < r; ++j) jac -= log(om[j]);
+            for (int j = 0; j < r - 1; ++j)
+                g[j] = log(om[j] / om[r - 1]) + (0.0 + sd * orc_std_normal(ctrs, (uint64_t)i, k0, k1));
+            g[r - 1] = 0.0;
             double gm = g[0];
-            for (int j = 1; j < ORC_GMM_R; ++j) gm = fmax(gm, g[j]);
+            for (int j = 1; j < r; ++j) gm = fmax(gm, g[j]);
             double s = 0;
-            for (int j = 0; j < ORC_GMM_R; ++j) { om[j] = exp(g[j] - gm); s += om[j]; }
-            for (int j = 0; j < ORC_GMM_R; ++j) { om[j] /= s; jac += log(om[j]); }
+            for (int j = 0; j < r; ++j) { om[j] = exp(g[j] - gm); s += om[j]; }
+            for (int j = 0; j < r; ++j) { om[j] /= s; jac += log(om[j]); }
         }
-        double lp = orc_gmm_lprior(p, h5), ll = orc_gmm_llh(p, y, nd);
+        double lp = orc_gmm_lprior(p, r, h6), ll = orc_gmm_llh(p, r, y, nd);
         double dp = lp + alpha * ll - p_old + jac;
         double u = log(orc_u01(ctrs, (uint64_t)i, k0, k1));
         if (u < dp) {
@@ -658,11 +664,11 @@ int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0,
 }
 
 /* The GMM sampler: prior annealing
- * alpha_t = (t/T)^power, move_smc -> ESS rule -> resample -> mu, lambda, weight MH ->
- * path (alpha_t, sum W llh).  hist rows (T+1) x 8: ess_over_n resampled acc_mu acc_lambda
- * acc_weight alpha U_t log_zconst. */
-int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const double *y, int nd,
-                const double *h5, int T, double power, double *hist, int nthreads)
+ * alpha_t = (t/T)^power, move_smc -> ESS rule -> resample -> mu, lambda (unless known),
+ * weight (r > 1) MH -> path (alpha_t, sum W llh).  hist rows (T+1) x 8: ess_over_n resampled
+ * acc_mu acc_lambda acc_weight alpha U_t log_zconst. */
+int orc_gmm_run(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                const double *h6, int T, double power, double *hist, int nthreads)
 {
     double *x = (double *)calloc((size_t)(ORC_GMM_ROW * n), sizeof(double));
     double *lw = (double *)malloc(sizeof(double) * (size_t)n), *w = (double *)malloc(sizeof(double) * (size_t)n);
@@ -672,7 +678,8 @@ int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const do
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     double ess, alpha = 0.0, log_z = 0.0;
     int rc = 0;
-    orc_gmm_init(x, n, ctrs, k0, k1, y, nd, h5, nthreads);
+    const int use[3] = {1, !(h6[5] > 0), r > 1};
+    orc_gmm_init(x, n, r, ctrs, k0, k1, y, nd, h6, nthreads);
     orc_weights_update(ORC_W_EQUAL, lw, w, NULL, n, &ess);
     for (int t = 0; t <= T && !rc; ++t) {
         double *hr = hist + 8 * t;
@@ -701,7 +708,8 @@ int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const do
                 orc_copy_rows(x, n, ORC_GMM_ROW, parents);
                 orc_weights_update(ORC_W_EQUAL, lw, w, NULL, n, &ess);
             }
-            for (int b = 0; b < 3; ++b) acc[b] = (double)orc_gmm_mh(b, x, n, ctrs, k0, k1, y, nd, h5, alpha, sds[b], nthreads);
+            for (int b = 0; b < 3; ++b)
+                if (use[b]) acc[b] = (double)orc_gmm_mh(b, x, n, r, ctrs, k0, k1, y, nd, h6, alpha, sds[b], nthreads);
         } else {
             hr[0] = ess / (double)n;
             hr[1] = resample_rule(hr[0], threshold);

@@ -88,16 +88,18 @@ int orc_pf_step(orc_pf_sys *s, const double *obs_t, double *hist_row, int nthrea
 int orc_pf_initialize(orc_pf_sys *s, const double *obs0, double *hist_row, int nthreads);
 
 /* ---- example-gmm ---- */
-#define ORC_GMM_R 4
+#define ORC_GMM_R 4   /* column stride: mu [0,4) lambda [4,8) omega [8,12); r <= 4 components used */
 #define ORC_GMM_ROW 16
-double orc_gmm_llh(const double *row, const double *y, int nd);
-double orc_gmm_lprior(const double *row, const double *h5);
-void orc_gmm_init(double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
-                  const double *h5, int nthreads);
-int64_t orc_gmm_mh(int block, double *x, int64_t n, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y,
-                   int nd, const double *h5, double alpha, double sd, int nthreads);
-int orc_gmm_run(int64_t n, uint64_t seed, int scheme, double threshold, const double *y, int nd,
-                const double *h5, int T, double power, double *hist, int nthreads);
+/* h6: xi kappa nu chi rho lambda_known (lambda_known > 0: every lambda_j fixed at that precision,
+ * no Gamma prior term and no lambda move -- the conjugate-oracle model) */
+double orc_gmm_llh(const double *row, int r, const double *y, int nd);
+double orc_gmm_lprior(const double *row, int r, const double *h6);
+void orc_gmm_init(double *x, int64_t n, int r, uint64_t *ctrs, uint32_t k0, uint32_t k1, const double *y, int nd,
+                  const double *h6, int nthreads);
+int64_t orc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t *ctrs, uint32_t k0, uint32_t k1,
+                   const double *y, int nd, const double *h6, double alpha, double sd, int nthreads);
+int orc_gmm_run(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                const double *h6, int T, double power, double *hist, int nthreads);
 
 #ifdef __cplusplus
 }

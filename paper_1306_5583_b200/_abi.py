@@ -82,11 +82,11 @@ _SIGS = {
     "smc_replication_to_parents": ([_vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gather_rows": ([_vp, _vp, _i64, _vp, _i64, _vp], C.c_int),
     "smc_copy_rows_inplace": ([_vp, _i64, _vp, _i64, _vp, _vp], C.c_int),
-    "smc_gmm_init": ([_vp, _i64, _u64, _u64, _vp, _vp, _i32, _vp, _vp], C.c_int),
-    "smc_gmm_eval": ([_vp, _i64, _vp, _i32, _vp, _vp], C.c_int),
+    "smc_gmm_init": ([_vp, _i64, _i32, _u64, _u64, _vp, _vp, _i32, _vp, _vp], C.c_int),
+    "smc_gmm_eval": ([_vp, _i64, _i32, _vp, _i32, _vp, _vp], C.c_int),
     "smc_gmm_workspace_bytes": ([_i64], _sz),
     "smc_gmm_reweight": ([_vp, _vp, _i64, _f64, _vp, _vp, _vp, _sz, _vp], C.c_int),
-    "smc_gmm_mh": ([_i32, _vp, _i64, _u64, _u64, _vp, _vp, _i32, _vp, _f64, _f64, _vp, _vp], C.c_int),
+    "smc_gmm_mh": ([_i32, _vp, _i64, _i32, _u64, _u64, _vp, _vp, _i32, _vp, _f64, _f64, _vp, _vp], C.c_int),
     "smc_pf_workspace_bytes": ([_i64], _sz),
     "smc_pf_init": ([_vp, _vp, _i64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],

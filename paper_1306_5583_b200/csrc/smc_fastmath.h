@@ -199,23 +199,24 @@ SMC_HD double exp(double x, const ExpEntry *tab)
 }
 
 // sum_k log(v_k) as one log of a running product: the product's exponent is
-// peeled off after every factor (integer ops), so the mantissa stays in [1, 2);
-// zero, subnormal or non-finite products take one libm-class log each.
+// peeled off after every factor (integer ops), so the mantissa m stays in [1, 2).
+// Factors outside [2^-999, 2^1000) (subnormal, zero, huge, non-finite, negative)
+// take their own libm-class log instead, so the product is never subnormal and
+// never rounds more than a normal multiply does.
 struct LogProd {
     double m = 1.0, acc = 0.0;
     int64_t ex = 0;
     SMC_HDM void add(double v)
     {
-        m *= v;
-        const uint64_t b = bits(m);
-        const int64_t e = (int64_t)((b >> 52) & 0x7ff);
-        if (e == 0 || e == 0x7ff) {
-            acc += smc_fm::log(m);
-            m = 1.0;
-        } else {
-            ex += e - 1023;
-            m = from_bits((b & 0x800fffffffffffffull) | 0x3ff0000000000000ull);
+        const uint64_t ev = bits(v) >> 52;  // biased exponent (sign bit -> >= 2048)
+        if (ev - 24u >= 2000u) {
+            acc += smc_fm::log(v);
+            return;
         }
+        m *= v;  // in [2^-999, 2^1001): normal
+        const uint64_t b = bits(m);
+        ex += (int64_t)(b >> 52) - 1023;
+        m = from_bits((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
     }
     SMC_HDM double result() const
     {

@@ -13,22 +13,31 @@ using namespace smc;
 namespace {
 
 constexpr int GB = 128;  // threads per block (register-heavy per-particle loops)
-constexpr int R = 4;     // mixture components (the paper's 4-component model)
+constexpr int RS = 4;    // column stride of mu / lambda / omega in a row (SMC_GMM_MAX_R)
 constexpr int W = SMC_GMM_ROW;
 
 struct Hyper {
-    double xi, kappa, nu, chi, rho;
+    double xi, kappa, nu, chi, rho, lambda_known;
     double lgamma_nu, log_chi, log_kappa_2pi, dir_const;
 };
 
+template <int R>
 struct Param {
     double mu[R], lam[R], om[R];
 };
 
-SMC_DEV void load_param(const double *row, Param &p)
+template <int R>
+SMC_DEV void load_param(const double *row, Param<R> &p)
 {
 #pragma unroll
-    for (int j = 0; j < R; ++j) { p.mu[j] = row[j]; p.lam[j] = row[R + j]; p.om[j] = row[2 * R + j]; }
+    for (int j = 0; j < R; ++j) { p.mu[j] = row[j]; p.lam[j] = row[RS + j]; p.om[j] = row[2 * RS + j]; }
+}
+
+template <int R>
+SMC_DEV void store_param(double *row, const Param<R> &p)
+{
+#pragma unroll
+    for (int j = 0; j < R; ++j) { row[j] = p.mu[j]; row[RS + j] = p.lam[j]; row[2 * RS + j] = p.om[j]; }
 }
 
 // update_log_likelihood: -n/2 log 2pi + sum_k log sum_j w_j exp(.5 log l_j - .5 l_j r^2).
@@ -36,7 +45,8 @@ SMC_DEV void load_param(const double *row, Param &p)
 // table exp of smc_fastmath.h (shared-memory table) and the k-sum as one log of a renormalized
 // product (LogProd): per (point, component) ~12 fp64 ops instead of libdevice exp + a log per point.
 // Differs from the oracle's sum of libm logs by rounding only (|d llh| ~ 1e-10 at n = 1000).
-SMC_DEV double log_likelihood(const Param &p, const double *__restrict__ y, int nd,
+template <int R>
+SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, int nd,
                               const smc_fm::ExpEntry *__restrict__ tab)
 {
     double c[R], b[R];
@@ -60,15 +70,17 @@ SMC_DEV double log_likelihood(const Param &p, const double *__restrict__ y, int 
 }
 
 // update_log_prior: Normal(xi, 1/kappa) per mu, Gamma(nu, chi) per
-// lambda, symmetric Dirichlet(rho) for omega.
-SMC_DEV double log_prior(const Param &p, const Hyper &h)
+// lambda (absent when lambda is known), symmetric Dirichlet(rho) for omega.
+template <int R>
+SMC_DEV double log_prior(const Param<R> &p, const Hyper &h)
 {
     double lp = 0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const double d = p.mu[j] - h.xi;
         lp += h.log_kappa_2pi * 0.5 - 0.5 * h.kappa * d * d;
-        lp += (h.nu - 1) * log(p.lam[j]) - p.lam[j] / h.chi - h.lgamma_nu - h.nu * h.log_chi;
+        if (!(h.lambda_known > 0))
+            lp += (h.nu - 1) * log(p.lam[j]) - p.lam[j] / h.chi - h.lgamma_nu - h.nu * h.log_chi;
         if (h.rho != 1.0) lp += (h.rho - 1) * log(p.om[j]);
     }
     return lp + h.dir_const;
@@ -88,6 +100,7 @@ size_t smem_bytes(int nd) { return TAB_BYTES + (size_t)nd * sizeof(double); }
 
 // gmm_init::initialize_state: per component, in order,
 // mu ~ N(mu0, sd0), lambda ~ Gamma(shape0, scale0), weight ~ Gamma(1, 1); normalize.
+template <int R>
 __global__ void __launch_bounds__(GB) k_gmm_init(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
                                                  uint64_t *__restrict__ ctrs, const double *__restrict__ data, int nd,
                                                  Hyper h)
@@ -100,21 +113,21 @@ __global__ void __launch_bounds__(GB) k_gmm_init(double *__restrict__ x, int64_t
     if (i >= n) return;
     const uint64_t si = sbase + (uint64_t)i;
     uint64_t c = ctrs[i];
-    Param p;
+    Param<R> p;
     const double sd0 = 1.0 / sqrt(h.kappa);
     double sum = 0;
     for (int j = 0; j < R; ++j) {
         p.mu[j] = h.xi + sd0 * normal_at(c, si, key);
         c += 2;
-        p.lam[j] = h.chi * gamma_from(c, si, key, h.nu);
+        p.lam[j] = h.lambda_known > 0 ? h.lambda_known : h.chi * gamma_from(c, si, key, h.nu);
         p.om[j] = 1.0 * gamma_from(c, si, key, 1.0);
         sum += p.om[j];
     }
     for (int j = 0; j < R; ++j) p.om[j] /= sum;
     ctrs[i] = c;
     double *row = x + i * W;
-#pragma unroll
-    for (int j = 0; j < R; ++j) { row[j] = p.mu[j]; row[R + j] = p.lam[j]; row[2 * R + j] = p.om[j]; }
+    for (int j = 0; j < 12; ++j) row[j] = 0.0;
+    store_param(row, p);
     row[12] = log_prior(p, h);
     row[13] = log_likelihood(p, s_y, nd, s_tab);
 }
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(256) k_gmm_reweight(const double *__restrict__
 // gmm_move_mu / _lambda / _weight: random walk,
 // recompute caches, accept iff log U < p_new - p_old (+ Jacobian).  Draws: the block's
 // normals in component order, then one uniform.
-template <int BLOCK>
+template <int BLOCK, int R>
 __global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
                                                uint64_t *__restrict__ ctrs, const double *__restrict__ data, int nd,
                                                Hyper h, double alpha, double sd,
@@ -155,7 +168,7 @@ __global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n
     int acc = 0;
     if (i < n) {
         double *row = x + i * W;
-        Param p;
+        Param<R> p;
         load_param(row, p);
         const double lp_old = row[12], ll_old = row[13];
         const double p_old = lp_old + alpha * ll_old;
@@ -199,8 +212,7 @@ __global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n
         c += 1;
         ctrs[i] = c;
         if (u < dp) {  // accept (strict)
-#pragma unroll
-            for (int j = 0; j < R; ++j) { row[j] = p.mu[j]; row[R + j] = p.lam[j]; row[2 * R + j] = p.om[j]; }
+            store_param(row, p);
             row[12] = lp_new;
             row[13] = ll_new;
             acc = 1;
@@ -219,6 +231,7 @@ __global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n
 }
 
 // log-prior / log-likelihood of given parameter rows (the cache-coherence hook).
+template <int R>
 __global__ void __launch_bounds__(GB) k_gmm_eval(double *__restrict__ x, int64_t n, const double *__restrict__ data,
                                                  int nd, Hyper h)
 {
@@ -229,31 +242,34 @@ __global__ void __launch_bounds__(GB) k_gmm_eval(double *__restrict__ x, int64_t
     const int64_t i = (int64_t)blockIdx.x * GB + threadIdx.x;
     if (i >= n) return;
     double *row = x + i * W;
-    Param p;
+    Param<R> p;
     load_param(row, p);
     row[12] = log_prior(p, h);
     row[13] = log_likelihood(p, s_y, nd, s_tab);
 }
 
-Hyper make_hyper(const double *hyper5)
+Hyper make_hyper(const double *hyper6, int R)
 {
     Hyper h;
-    h.xi = hyper5[0];
-    h.kappa = hyper5[1];
-    h.nu = hyper5[2];
-    h.chi = hyper5[3];
-    h.rho = hyper5[4];
+    h.xi = hyper6[0];
+    h.kappa = hyper6[1];
+    h.nu = hyper6[2];
+    h.chi = hyper6[3];
+    h.rho = hyper6[4];
+    h.lambda_known = hyper6[5];
     h.lgamma_nu = lgamma(h.nu);
     h.log_chi = log(h.chi);
     h.log_kappa_2pi = log(h.kappa / (2.0 * 3.141592653589793));
-    h.dir_const = lgamma(R * h.rho) - R * lgamma(h.rho);  // Dirichlet normalizer (ln (r-1)! at rho = 1)
+    h.dir_const = lgamma(R * h.rho) - R * lgamma(h.rho);  // Dirichlet normalizer (ln (r-1)! at rho = 1), R = r
     return h;
 }
 
-int gmm_check(const double *x, int64_t n, const double *data, int nd, const double *hyper, const char *who)
+int gmm_check(const double *x, int64_t n, int r, const double *data, int nd, const double *hyper, const char *who)
 {
     if (!x || n < 1 || n >= ((int64_t)1 << 31) || !data || nd < 1 || nd > SMC_GMM_MAX_DATA || !hyper)
         return smc_set_error(SMC_EINVAL, "%s: bad args", who);
+    if (r < 1 || r > SMC_GMM_MAX_R) return smc_set_error(SMC_EINVAL, "%s: r = %d outside [1, %d]", who, r, SMC_GMM_MAX_R);
+    if (hyper[5] < 0 || hyper[5] != hyper[5]) return smc_set_error(SMC_EINVAL, "%s: lambda_known must be >= 0", who);
     if (!(hyper[1] > 0 && hyper[2] > 0 && hyper[3] > 0 && hyper[4] > 0))
         return smc_set_error(SMC_EINVAL, "%s: hyperparameters must be positive", who);
     return SMC_OK;
@@ -261,23 +277,36 @@ int gmm_check(const double *x, int64_t n, const double *data, int nd, const doub
 
 }  // namespace
 
-extern "C" int smc_gmm_init(double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs, const double *data,
-                            int nd, const double *hyper, void *stream)
+// r -> template instantiation (r = 1..SMC_GMM_MAX_R)
+#define SMC_GMM_DISPATCH(r, CALL)          \
+    switch (r) {                            \
+    case 1: { constexpr int R = 1; CALL; } break; \
+    case 2: { constexpr int R = 2; CALL; } break; \
+    case 3: { constexpr int R = 3; CALL; } break; \
+    default: { constexpr int R = 4; CALL; } break; \
+    }
+
+extern "C" int smc_gmm_init(double *x, int64_t n, int r, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
+                            const double *data, int nd, const double *hyper, void *stream)
 {
-    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_init");
+    int rc = gmm_check(x, n, r, data, nd, hyper, "smc_gmm_init");
     if (rc) return rc;
     if (!ctrs) return smc_set_error(SMC_EINVAL, "smc_gmm_init: ctrs");
-    k_gmm_init<<<(unsigned)((n + GB - 1) / GB), GB, smem_bytes(nd), (cudaStream_t)stream>>>(
-        x, n, stream_base, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, data, nd, make_hyper(hyper));
+    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const Hyper h = make_hyper(hyper, r);
+    const unsigned nb = (unsigned)((n + GB - 1) / GB);
+    SMC_GMM_DISPATCH(r, (k_gmm_init<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, stream_base, key, ctrs,
+                                                                                       data, nd, h)));
     return smc_check_launch("smc_gmm_init");
 }
 
-extern "C" int smc_gmm_eval(double *x, int64_t n, const double *data, int nd, const double *hyper, void *stream)
+extern "C" int smc_gmm_eval(double *x, int64_t n, int r, const double *data, int nd, const double *hyper, void *stream)
 {
-    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_eval");
+    int rc = gmm_check(x, n, r, data, nd, hyper, "smc_gmm_eval");
     if (rc) return rc;
-    k_gmm_eval<<<(unsigned)((n + GB - 1) / GB), GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, data, nd,
-                                                                                               make_hyper(hyper));
+    const Hyper h = make_hyper(hyper, r);
+    const unsigned nb = (unsigned)((n + GB - 1) / GB);
+    SMC_GMM_DISPATCH(r, (k_gmm_eval<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, data, nd, h)));
     return smc_check_launch("smc_gmm_eval");
 }
 
@@ -301,21 +330,24 @@ extern "C" int smc_gmm_reweight(const double *x, double *lw_raw, int64_t n, doub
     return smc_check_launch("smc_gmm_reweight");
 }
 
-extern "C" int smc_gmm_mh(int block, double *x, int64_t n, uint64_t stream_base, uint64_t seed, uint64_t *ctrs,
-                          const double *data, int nd, const double *hyper, double alpha, double sd,
+extern "C" int smc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t stream_base, uint64_t seed,
+                          uint64_t *ctrs, const double *data, int nd, const double *hyper, double alpha, double sd,
                           unsigned long long *accepted, void *stream)
 {
-    int rc = gmm_check(x, n, data, nd, hyper, "smc_gmm_mh");
+    int rc = gmm_check(x, n, r, data, nd, hyper, "smc_gmm_mh");
     if (rc) return rc;
     if (!ctrs || !accepted || block < 0 || block > 2 || !(sd >= 0))
         return smc_set_error(SMC_EINVAL, "smc_gmm_mh: bad args");
     cudaStream_t s = (cudaStream_t)stream;
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
-    const Hyper h = make_hyper(hyper);
+    const Hyper h = make_hyper(hyper, r);
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
     const size_t sm = smem_bytes(nd);
-    if (block == 0) k_gmm_mh<0><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
-    else if (block == 1) k_gmm_mh<1><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
-    else k_gmm_mh<2><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted);
+#define SMC_GMM_MH(B) \
+    SMC_GMM_DISPATCH(r, (k_gmm_mh<B, R><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted)))
+    if (block == 0) { SMC_GMM_MH(0) }
+    else if (block == 1) { SMC_GMM_MH(1) }
+    else { SMC_GMM_MH(2) }
+#undef SMC_GMM_MH
     return smc_check_launch("smc_gmm_mh");
 }

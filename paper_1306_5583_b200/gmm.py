@@ -29,9 +29,10 @@ from .rng import RngStreamSet
 
 __all__ = ["GmmState", "generate_data", "default_hyper", "alpha_linear", "alpha_prior", "gmm_init", "gmm_move_smc",
            "gmm_move_mu", "gmm_move_lambda", "gmm_move_weight", "gmm_path", "make_sampler", "ROW", "R",
-           "TRUE_MU", "TRUE_LAMBDA", "TRUE_OMEGA"]
+           "TRUE_MU", "TRUE_LAMBDA", "TRUE_OMEGA", "MAX_R", "conjugate_log_evidence"]
 
-R = 4
+R = 4     # the paper's 4-component model (config 3); 1 <= components <= MAX_R
+MAX_R = 4
 ROW = 16  # SMC_GMM_ROW: mu[4] lambda[4] omega[4] log_prior log_likelihood pad pad
 TRUE_MU = (-3.0, 0.0, 3.0, 6.0)
 TRUE_LAMBDA = 2.0
@@ -48,11 +49,23 @@ def generate_data(n=1000, seed=1306, device="cuda"):
     return np.asarray(TRUE_MU)[c] + z / math.sqrt(TRUE_LAMBDA)
 
 
-def default_hyper(data):
-    """xi = midrange, kappa = 1/R^2, nu = 2, chi = 50/R^2, rho = 1 (R = data range)."""
+def default_hyper(data, lambda_known=0.0):
+    """SPEC.md:592: xi = midrange, kappa = 1/R^2, nu = 2, chi = 50/R^2, rho = 1 (R = data range);
+    6th value lambda_known (0: lambda unknown with the Gamma prior)."""
     lo, hi = float(np.min(data)), float(np.max(data))
     rng = hi - lo
-    return [0.5 * (lo + hi), 1.0 / (rng * rng), 2.0, 50.0 / (rng * rng), 1.0]
+    return [0.5 * (lo + hi), 1.0 / (rng * rng), 2.0, 50.0 / (rng * rng), 1.0, float(lambda_known)]
+
+
+def conjugate_log_evidence(data, xi, kappa, lam):
+    """Closed-form log p(y) for y_k ~ N(mu, 1/lam), mu ~ N(xi, 1/kappa) (the conjugate oracle,
+    SPEC.md:586-587): y ~ N(xi 1, I/lam + 11'/kappa)."""
+    y = np.asarray(data, np.float64) - xi
+    n = y.size
+    s2, t2 = 1.0 / lam, 1.0 / kappa
+    logdet = (n - 1) * math.log(s2) + math.log(s2 + n * t2)
+    quad = (float(np.dot(y, y)) - t2 * float(y.sum()) ** 2 / (s2 + n * t2)) / s2
+    return -0.5 * n * math.log(2 * math.pi) - 0.5 * logdet - 0.5 * quad
 
 
 def alpha_linear(T):
@@ -68,8 +81,11 @@ def alpha_prior(T, p=2.0):
 class GmmState(StateMatrix):
     """StateMatrix<RowMajor, 16, double> + data, hyperparameters, alpha (PAPER.md:1683-1740)."""
 
-    def __init__(self, size, device="cuda"):
+    def __init__(self, size, device="cuda", components=R):
         super().__init__(size, ROW, ROW_MAJOR, device)
+        if not 1 <= int(components) <= MAX_R:
+            raise ValueError(f"components must be in [1, {MAX_R}]")
+        self.r = int(components)
         self.y = None
         self.hyper = None
         self._hyper_c = None
@@ -82,8 +98,16 @@ class GmmState(StateMatrix):
         if not 0 < arr.size <= 4096:
             raise ValueError("GMM data must hold 1..4096 points")
         self.y = torch.as_tensor(arr).to(self.device)
-        self.hyper = list(default_hyper(arr) if hyper is None else hyper)
-        self._hyper_c = (ctypes.c_double * 5)(*self.hyper)
+        h = list(default_hyper(arr) if hyper is None else hyper)
+        h += [0.0] * (6 - len(h))
+        if len(h) != 6:
+            raise ValueError("hyper: xi, kappa, nu, chi, rho[, lambda_known]")
+        self.hyper = h
+        self._hyper_c = (ctypes.c_double * 6)(*self.hyper)
+
+    @property
+    def lambda_known(self):
+        return self.hyper is not None and self.hyper[5] > 0
 
     def set_alpha(self, a):
         """gmm_state::alpha (PAPER.md:1690-1702): clamp to [0, 1], track the increment."""
@@ -114,7 +138,7 @@ def gmm_init(system, param=None):
     v.set_alpha(0.0)
     v.pending = None
     system.weight_set.reset_log_zconst()
-    _abi.call("smc_gmm_init", _abi.ptr(v.raw), system.size, system.stream_base, system.rng_set.seed,
+    _abi.call("smc_gmm_init", _abi.ptr(v.raw), system.size, v.r, system.stream_base, system.rng_set.seed,
               _abi.ptr(system.rng_set.counters), _abi.ptr(v.y), v.y.numel(), v._hyper_c, _abi.stream())
     return None
 
@@ -141,7 +165,7 @@ def _mh(block, name):
     def kernel(iter_, system):
         v = system.value
         acc = torch.zeros(1, dtype=torch.int64, device=system.device)
-        _abi.call("smc_gmm_mh", block, _abi.ptr(v.raw), system.size, system.stream_base, system.rng_set.seed,
+        _abi.call("smc_gmm_mh", block, _abi.ptr(v.raw), system.size, v.r, system.stream_base, system.rng_set.seed,
                   _abi.ptr(system.rng_set.counters), _abi.ptr(v.y), v.y.numel(), v._hyper_c, v.alpha,
                   v.sds[block], _abi.ptr(acc), _abi.stream())
         return acc  # accepted count
@@ -167,15 +191,20 @@ def gmm_path():
 
 
 def make_sampler(n, data=None, T=100, power=2.0, scheme=ResampleScheme.Stratified, threshold=0.5, seed=0,
-                 hyper=None, device="cuda"):
-    """The paper's GMM main: init, move_smc, mu/lambda/weight MCMC, path sampling."""
-    v = GmmState(n, device)
+                 hyper=None, components=R, device="cuda"):
+    """The paper's GMM main: init, move_smc, mu/lambda/weight MCMC, path sampling.
+
+    components: r (1..4).  hyper[5] = lambda_known > 0 gives the conjugate-oracle model (lambda
+    fixed, no lambda block); r = 1 has no weight block (omega = 1)."""
+    v = GmmState(n, device, components)
     v.set_data(generate_data(1000, 1306, device) if data is None else data, hyper)
     s = Sampler(n, scheme, threshold, seed, value=v, device=device)
     s.set_init(gmm_init)
     s.add_move(gmm_move_smc(alpha_prior(T, power) if power != 1 else alpha_linear(T)), False)
     s.add_mcmc(gmm_move_mu(), False)
-    s.add_mcmc(gmm_move_lambda(), True)
-    s.add_mcmc(gmm_move_weight(), True)
+    if not v.lambda_known:
+        s.add_mcmc(gmm_move_lambda(), True)
+    if v.r > 1:
+        s.add_mcmc(gmm_move_weight(), True)
     s.set_path(gmm_path())
     return s

@@ -132,7 +132,8 @@ def test_logprod_matches_sum_of_logs(fm):
     decimal.getcontext().prec = 60
     rng = np.random.default_rng(6)
     for v in (rng.uniform(1e-3, 2.0, 1000), np.exp(rng.uniform(-300, 5, 1000)), np.full(1000, 1e-200),
-              np.array([1e-310, 0.5, 3e-320, 2.0]), rng.uniform(0.9, 1.1, 4096)):
+              np.array([1e-310, 0.5, 3e-320, 2.0]), rng.uniform(0.9, 1.1, 4096),
+              np.array([1.7, 3 * 2.0 ** -1074, 1.9, 2.0 ** -1000, 2.0 ** 1000, 1e300, 1e-300, 5e-324])):
         exact = sum(decimal.Decimal(float(t)).ln() for t in v)
         got = fm("fm_logprod", v)
         assert abs(decimal.Decimal(got) - exact) <= decimal.Decimal(1e-15) * max(1, abs(exact)), (got, exact)

@@ -61,7 +61,7 @@ def main():
         h5 = gmm.default_hyper(y)
         th = os.cpu_count() or 1
         t0 = time.perf_counter()
-        ref = O.gmm_run(args.cpu_n, 1307, "stratified", 0.5, y, h5, T, 2.0, nthreads=th)
+        ref = O.gmm_run(args.cpu_n, 1307, "stratified", 0.5, y, h5, T, 2.0, r=gmm.R, nthreads=th)
         dt = time.perf_counter() - t0
         out["cpu_baseline"] = {"value": args.cpu_n * T / dt, "unit": "particle-iterations/s", "cores": th,
                                "kind": "port", "sample": f"oracle orc_gmm_run N={args.cpu_n} T={T}",
