@@ -283,6 +283,34 @@ int smc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t stream_base, uin
                const double *data, int nd, const double *hyper, double alpha, double sd,
                unsigned long long *accepted, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* user particle kernels, compiled at run time -- replaces the per-particle  */
+/* `kernel(iter, SingleParticleView) -> int` / MoveAdapter / monitor and    */
+/* path evaluators      */
+/* ------------------------------------------------------------------------ */
+/* source: CUDA C++ that includes "smc_user.cuh" (pass -I<csrc dir> in
+ * options) and ends with SMC_USER_MOVE(fn) or SMC_USER_EVAL(fn).  NVRTC
+ * compiles it for sm_100a (--fmad=false); libnvrtc / libcuda are loaded on
+ * first use.  log (may be NULL) receives the compiler log.  The module handle
+ * is freed with smc_user_free. */
+#define SMC_USER_MOVE 1
+#define SMC_USER_EVAL 2
+int smc_user_compile(const char *source, const char *const *options, int n_options, void **module_out, char *log,
+                     size_t log_bytes);
+int smc_user_kind(const void *module);
+int smc_user_free(void *module);
+/* One thread per particle: fn(Particle&, iter, params) with the particle's row
+ * of x (n x dim, row- or column-major), its stream stream_base + i (counter
+ * ctrs[i], written back), scratch row i (n x sdim); *accepted += sum of the
+ * returned ints (exact). */
+int smc_user_launch_move(void *module, uint64_t iter, double *x, int64_t n, int dim, int col_major,
+                         uint64_t stream_base, uint64_t seed, uint64_t *ctrs, double *scratch, int sdim,
+                         const double *params, unsigned long long *accepted, void *stream);
+/* fn(const Particle&, iter, params, out + i*m): m values per particle (a monitor's
+ * h_1..h_m, res[i*dim + j] of PAPER.md:574-586, or a path integrand with m = 1). */
+int smc_user_launch_eval(void *module, uint64_t iter, const double *x, int64_t n, int dim, int col_major,
+                         const double *params, double *out, int m, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

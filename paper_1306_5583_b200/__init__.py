@@ -19,7 +19,7 @@ from .resample import (ResampleScheme, replication_to_parents, resample, resampl
                        resample_stratified, resample_systematic)
 from .rng import RngStream, RngStreamSet  # noqa: E402
 from .weights import WeightSet  # noqa: E402
-from . import gmm, pf  # noqa: E402
+from . import gmm, pf, user  # noqa: E402
 
 __version__ = "0.1.0"
 
@@ -29,5 +29,5 @@ __all__ = [
     "resample_residual_systematic", "replication_to_parents", "StateMatrix", "ParticleSystem",
     "SingleParticleView", "Sampler", "MonitorRecord", "PathAccumulator", "NormalizingConstant", "Backend",
     "ParticleKernelOp", "MonitorEval", "PathEval", "apply_move", "apply_monitor_eval", "apply_path_eval",
-    "make_op_from_kernel", "pf", "gmm", "ROW_MAJOR", "COL_MAJOR",
+    "make_op_from_kernel", "pf", "gmm", "user", "ROW_MAJOR", "COL_MAJOR",
 ]

@@ -87,6 +87,11 @@ _SIGS = {
     "smc_gmm_workspace_bytes": ([_i64], _sz),
     "smc_gmm_reweight": ([_vp, _vp, _i64, _f64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gmm_mh": ([_i32, _vp, _i64, _i32, _u64, _u64, _vp, _vp, _i32, _vp, _f64, _f64, _vp, _vp], C.c_int),
+    "smc_user_compile": ([C.c_char_p, _vp, _i32, _vp, C.c_char_p, _sz], C.c_int),
+    "smc_user_kind": ([_vp], C.c_int),
+    "smc_user_free": ([_vp], C.c_int),
+    "smc_user_launch_move": ([_vp, _u64, _vp, _i64, _i32, _i32, _u64, _u64, _vp, _vp, _i32, _vp, _vp, _vp], C.c_int),
+    "smc_user_launch_eval": ([_vp, _u64, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp], C.c_int),
     "smc_pf_workspace_bytes": ([_i64], _sz),
     "smc_pf_init": ([_vp, _vp, _i64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],

@@ -8,96 +8,11 @@
 #include <stdint.h>
 
 #include "../../include/smc_abi.h"
-#include "smc_fastmath.h"
+#include "smc_rng_device.cuh"
 
 typedef unsigned __int128 u128;
 
-#define SMC_DEV __device__ __forceinline__
-
 namespace smc {
-
-// ---------------------------------------------------------------------------
-// Philox4x32-10 (rng.py:48-72).  Counter = (draw_lo, draw_hi, stream_lo,
-// stream_hi), key = (seed_lo, seed_hi); ten rounds, key bumped after each.
-// ---------------------------------------------------------------------------
-constexpr uint32_t PHILOX_M0 = 0xD2511F53u;
-constexpr uint32_t PHILOX_M1 = 0xCD9E8D57u;
-constexpr uint32_t PHILOX_W0 = 0x9E3779B9u;
-constexpr uint32_t PHILOX_W1 = 0xBB67AE85u;
-
-struct Key {
-    uint32_t k0, k1;
-};
-
-SMC_DEV Key make_key(uint64_t seed) { return Key{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
-
-SMC_DEV uint4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, Key key)
-{
-    uint32_t k0 = key.k0, k1 = key.k1;
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(PHILOX_M0, c0), lo0 = PHILOX_M0 * c0;
-        const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;
-        const uint32_t n0 = hi1 ^ c1 ^ k0;
-        const uint32_t n2 = hi0 ^ c3 ^ k1;
-        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-        k0 += PHILOX_W0;
-        k1 += PHILOX_W1;
-    }
-    return make_uint4(c0, c1, c2, c3);
-}
-
-// 53-bit integer of draw `ctr` of stream `stream` (rng.py:81-82):
-// ((w0 >> 5) << 26) | (w1 >> 6); the uniform is this times 2^-53, exactly.
-SMC_DEV uint64_t draw53(uint64_t ctr, uint64_t stream, Key key)
-{
-    const uint4 w = philox10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream,
-                             (uint32_t)(stream >> 32), key);
-    return ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
-}
-
-SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, Key key)
-{
-    return __dmul_rn(__ull2double_rn(draw53(ctr, stream, key)), 1.0 / 9007199254740992.0);
-}
-
-// rng.py:85-91: Box-Muller cosine branch on 1 - u1, exactly two draws.
-// (All TUs build with --fmad=false, so no contraction changes the rounding;
-// log is smc_fastmath.h's table log (<= 0.55 ulp, 99.6 % bit-identical to glibc,
-// 8 % cheaper than libdevice on B200); cos is libdevice's (the fdlibm-style
-// smc_fm::cos diverges per quadrant and measured 40 % slower); sqrt is IEEE.)
-SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, Key key)
-{
-    const double u1 = u01_at(ctr, stream, key);
-    const double u2 = u01_at(ctr + 1, stream, key);
-    return sqrt(-2.0 * smc_fm::log(1.0 - u1)) * cos((2.0 * 3.141592653589793) * u2);
-}
-
-// rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the
-// variable number of draws it consumes.
-SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, Key key, double shape)
-{
-    double boost = 1.0;
-    double a = shape;
-    if (a < 1.0) {
-        const double u = 1.0 - u01_at(ctr, stream, key);
-        ctr += 1;
-        boost = pow(u, 1.0 / a);
-        a = a + 1.0;
-    }
-    const double d = a - 1.0 / 3.0;
-    const double c = 1.0 / sqrt(9.0 * d);
-    for (;;) {
-        const double x = normal_at(ctr, stream, key);
-        ctr += 2;
-        const double t = 1.0 + c * x;
-        if (t <= 0.0) continue;
-        const double v = t * t * t;
-        const double u = 1.0 - u01_at(ctr, stream, key);
-        ctr += 1;
-        if (smc_fm::log(u) < 0.5 * x * x + d - d * v + d * smc_fm::log(v)) return boost * d * v;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Normalized log-weights from the raw vector + device record (smc_abi.h).

@@ -15,9 +15,19 @@
 //          pi/2 in two 33-bit pieces + tail, then fdlibm's __kernel_cos/_sin
 //          polynomials on |r| <= pi/4.
 #pragma once
+#ifdef __CUDACC_RTC__  // run-time compiled user kernels (NVRTC has no libc headers)
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+#ifndef INFINITY
+#define INFINITY __longlong_as_double(0x7ff0000000000000LL)
+#endif
+#else
 #include <stdint.h>
 #include <string.h>
 #include <math.h>
+#endif
 
 #ifdef __CUDACC__
 #define SMC_HD __host__ __device__ __forceinline__

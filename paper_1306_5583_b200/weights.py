@@ -88,9 +88,10 @@ class WeightSet:
         n_total: the global particle count of a sharded system (equal weight 1/n_total)."""
         _abi.call("smc_weights_set_equal", self.state_ptr, int(n_total or self.size), gate_ptr, _abi.stream())
 
-    def set_log_weight(self, values, check=None):
-        """Normalize values by max-shift + log-sum-exp."""
-        self._update(SET_LOG, values, check=check)
+    def set_log_weight(self, values, accumulate_nc=False, check=None):
+        """Normalize values by max-shift + log-sum-exp.  accumulate_nc:
+        log_zconst += log mean exp(values) (the initial weights' contribution to log Z)."""
+        self._update(SET_LOG, values, accumulate_nc, check=check)
 
     def add_log_weight(self, increments, accumulate_nc=False, check=None):
         """log_weight += increments, renormalize (SPEC.md:51-59)."""
