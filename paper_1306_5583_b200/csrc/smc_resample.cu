@@ -18,10 +18,10 @@
 //   B  k_rs_counts  : per tile (coalesced loads staged through shared memory),
 //                     local scan + tile prefix -> Q; counts in O(1) per particle
 //                     via F(X) = #{k : P_k < X} (fp64 with a guard band, exact
-//                     128-bit fallback inside it); then a DECOUPLED-LOOKBACK scan
-//                     of (zero slots, surplus children, surplus parents) that
-//                     emits the survivor half of the parent map, the compacted
-//                     zero-slot list and the compacted surplus-parent list.
+//                     128-bit fallback inside it) and the tile's (zero slots,
+//                     surplus parents, surplus children) aggregate.
+//   S2 k_rs_zsp_scan: one block: exclusive prefixes of those aggregates.
+//   B2 k_rs_ranks   : per tile: the compacted surplus-parent list + rank anchors.
 //   C  k_rs_assign  : per tile of zero-slot ranks: the tile's slice of the
 //                     surplus-parent prefix staged in shared memory (merge-path
 //                     boundaries by binary search), a linear merge walk per
@@ -55,7 +55,6 @@ struct RsHeader {
     int64_t draws;
     int32_t active;   // 0 => gated off or failed; later kernels exit
     int32_t trivial;  // N == 1
-    uint32_t tile_ctr;
     uint32_t Z_total, S_total, P_total;
     uint64_t qoff;    // this shard's CDF offset (0 on one GPU)
 };
@@ -66,8 +65,8 @@ struct Layout {
     int64_t *tile_f;
     uint64_t *tile_qr;
     uint64_t *tile_pre;
-    uint32_t *lb_status;
-    uint4 *lb_agg, *lb_incl;
+    uint64_t *tile_zsp;  // per slot tile: packed (zero slots, surplus parents, surplus children)
+    uint4 *tile_excl;   // per slot tile: exclusive (Z, S, P) prefix
     int32_t *anchor, *sp_idx, *sp_start;  // anchor[k]: surplus parent covering rank k*ANCHOR
     int32_t *tile_z0;   // per slot tile: its first zero rank (and Z at index nt)
     uint64_t *qfull;
@@ -89,9 +88,8 @@ Layout layout(void *ws, int64_t n)
     L.tile_f = (int64_t *)take(sizeof(int64_t) * nt);
     L.tile_qr = (uint64_t *)take(sizeof(uint64_t) * nt);
     L.tile_pre = (uint64_t *)take(sizeof(uint64_t) * nt);
-    L.lb_status = (uint32_t *)take(sizeof(uint32_t) * nt);
-    L.lb_agg = (uint4 *)take(sizeof(uint4) * nt);
-    L.lb_incl = (uint4 *)take(sizeof(uint4) * nt);
+    L.tile_zsp = (uint64_t *)take(sizeof(uint64_t) * nt);
+    L.tile_excl = (uint4 *)take(sizeof(uint4) * (nt + 1));
     L.anchor = (int32_t *)take(sizeof(int32_t) * (n / ANCHOR + 2));
     L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));  // P <= n even for invalid counts
     L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
@@ -203,7 +201,6 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
         L.tile_q[blockIdx.x] = a;
         L.tile_qr[blockIdx.x] = b;
         L.tile_f[blockIdx.x] = c;
-        L.lb_status[blockIdx.x] = 0;
     }
 }
 
@@ -319,7 +316,6 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         h->guard = (double)(M > 0 ? M : 1) * 7.105427357601002e-15;
         h->draws = draws;
         h->trivial = (n_total == 1);
-        h->tile_ctr = 0;
         h->Z_total = h->S_total = h->P_total = 0;
         if (ok) {
             const uint64_t c0 = u ? 0 : *ctr;
@@ -454,28 +450,168 @@ SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
     return s + (d > 0.0 ? 1 : 0);
 }
 
-// Pass B2 tiles are larger than pass A/B1/C tiles: the lookback cost is per
-// tile, and these tiles are cheap (8 KiB of counts), so fewer of them win.
-constexpr int RI2 = 32;
-constexpr int TILE2 = RT * RI2;  // 8192 counts per rank-scan tile
-
 // pack (zero slots, surplus parents) in the top 2 x 14 bits, surplus children in
-// the low 36 -- tile-local sums never carry across fields (<= 8192, < 2^31).
+// the low 36 -- tile-local sums never carry across fields (<= 2048, < 2^31).
 SMC_DEV uint64_t pack_zsp(uint32_t z, uint32_t p, uint64_t s) { return ((uint64_t)z << 50) | ((uint64_t)p << 36) | s; }
 SMC_DEV uint32_t unz(uint64_t v) { return (uint32_t)(v >> 50); }
 SMC_DEV uint32_t unp(uint64_t v) { return (uint32_t)((v >> 36) & 0x3FFF); }
 SMC_DEV uint64_t uns(uint64_t v) { return v & ((1ull << 36) - 1); }
 
-SMC_DEV uint32_t ld_status(const uint32_t *p) { return *(volatile const uint32_t *)p; }
-
 // blocked smem index with one pad word per 16: conflict-free for 64-bit reads of t*8+j
 SMC_DEV int pad16(int i) { return i + (i >> 4); }
+
+// replication_to_parents' rank scan as REDUCE-THEN-SCAN over
+// 2048-slot tiles: (1) the pass that holds a tile's counts publishes its
+// (zero slots, surplus parents, surplus children) aggregate; (2) one block scans
+// the aggregates (k_rs_zsp_scan); (3) k_rs_ranks re-reads the counts and emits
+// the compacted surplus-parent list.  (A decoupled lookback fused into pass B1
+// was measured slower on B200: the status chain over 8192 tiles costs more than
+// the 4 B/slot re-read -- DESIGN.md §6.)
+SMC_DEV void tile_aggregate(const int32_t (&c)[RI], int64_t b, const Layout &L)
+{
+    __shared__ uint64_t sm[RT / 32 + 1];
+    uint32_t tz = 0, tp = 0;
+    uint64_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        tz += (c[j] == 0);
+        tp += (c[j] >= 2);
+        ts += c[j] >= 2 ? (uint64_t)(c[j] - 1) : 0;
+    }
+    uint64_t agg;
+    block_exclusive_sum<RT, uint64_t>(pack_zsp(tz, tp, ts), sm, &agg);
+    if (threadIdx.x == 0) L.tile_zsp[b] = agg;
+}
+
+// One block: exclusive (Z, S, P) prefix of the tile aggregates, the totals, each
+// slot tile's first zero rank, and the sum(counts) == N check.
+__global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32_t *status, Layout L)
+{
+    RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    __shared__ uint64_t s_zp[SB / 32 + 1], s_s[SB / 32 + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = SB / 32;
+    const int64_t C = (nt + NW - 1) / NW;  // warp w owns tiles [w C, (w+1) C)
+    const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
+    // (Z, P) as two 32-bit halves of one u64 (totals < 2^31 never carry), S as u64
+    auto zp = [&](uint64_t v) { return ((uint64_t)unz(v) << 32) | unp(v); };
+    uint64_t a = 0, bs = 0;
+    for (int64_t t = w0 + lane; t < w1; t += 32) {
+        const uint64_t v = L.tile_zsp[t];
+        a += zp(v);
+        bs += uns(v);
+    }
+    a = warp_sum(a);
+    bs = warp_sum(bs);
+    if (lane == 0) { s_zp[warp] = a; s_s[warp] = bs; }
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t x = s_zp[lane], y = s_s[lane];
+        const uint64_t ix = warp_inclusive_sum(x), iy = warp_inclusive_sum(y);
+        s_zp[lane] = ix - x;
+        s_s[lane] = iy - y;
+        if (lane == 31) {
+            const uint32_t Z = (uint32_t)(ix >> 32), P = (uint32_t)ix, S = (uint32_t)iy;
+            h->Z_total = Z;
+            h->S_total = S;
+            h->P_total = P;
+            L.sp_start[P] = (int32_t)S;  // sentinel
+            L.tile_z0[nt] = (int32_t)Z;
+            L.tile_excl[nt] = make_uint4(Z, S, P, 0);
+            // sum(counts) != N; a shard's Z and S only balance globally (host check)
+            if (whole && Z != S) raise_status(status, SMC_ECOUNTS);
+        }
+    }
+    __syncthreads();
+    uint64_t ca = s_zp[warp], cs = s_s[warp];
+    for (int64_t t0 = w0; t0 < w1; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const uint64_t v = t < w1 ? L.tile_zsp[t] : 0;
+        const uint64_t x = zp(v), y = uns(v);
+        const uint64_t ix = warp_inclusive_sum(x), iy = warp_inclusive_sum(y);
+        if (t < w1) {
+            const uint64_t ex = ca + ix - x, ey = cs + iy - y;
+            L.tile_excl[t] = make_uint4((uint32_t)(ex >> 32), (uint32_t)ey, (uint32_t)ex, 0);
+            L.tile_z0[t] = (int32_t)(ex >> 32);
+        }
+        ca += __shfl_sync(0xffffffffu, ix, 31);
+        cs += __shfl_sync(0xffffffffu, iy, 31);
+    }
+}
+
+// Emission for one tile whose exclusive prefix is known: the tile's slice of the
+// compacted surplus-parent list (index, first surplus rank) -- staged in shared
+// memory and stored coalesced -- and the rank anchors (the surplus parent
+// covering every ANCHOR-th surplus rank).
+__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int32_t *status,
+                                                 int check, Layout L)
+{
+    RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI>()];
+    __shared__ int32_t s_stage[2 * TILE];
+    __shared__ uint64_t sm[RT / 32 + 1];
+    const int64_t b = blockIdx.x;
+    int32_t c[RI];
+    load_blocked<RT, RI, int32_t>(cin, b * TILE, n, c, s_c, 1);  // coalesced; pad: not zero, no surplus
+    if (check) {  // caller-provided counts (replication_to_parents)
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < RI; ++j)
+            if (c[j] < 0) { bad = true; c[j] = 0; }
+        if (bad) raise_status(status, SMC_ECOUNTS);
+    }
+    uint32_t tp = 0;
+    uint64_t ts = 0;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        tp += (c[j] >= 2);
+        ts += c[j] >= 2 ? (uint64_t)(c[j] - 1) : 0;
+    }
+    uint64_t agg;
+    const uint64_t tex = block_exclusive_sum<RT, uint64_t>(pack_zsp(0, tp, ts), sm, &agg);
+    const uint4 ex = __ldcg(&L.tile_excl[b]);
+    uint32_t sr = ex.y + (uint32_t)uns(tex);
+    uint32_t lp = unp(tex);  // tile-local surplus-parent index
+    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) {
+        if (c[j] >= 2 && base + j < n) {
+            s_stage[lp] = (int32_t)(base + j);
+            s_stage[TILE + lp] = (int32_t)sr;
+            const uint32_t se = sr + (uint32_t)(c[j] - 1);
+            for (uint32_t m = (sr + ANCHOR - 1) / ANCHOR * ANCHOR; m < se; m += ANCHOR)
+                L.anchor[m / ANCHOR] = (int32_t)(ex.z + lp);
+            ++lp;
+            sr = se;
+        }
+    }
+    __syncthreads();
+    const uint32_t np = unp(agg);
+    for (uint32_t k = threadIdx.x; k < np; k += RT) {
+        L.sp_idx[ex.z + k] = s_stage[k];
+        L.sp_start[ex.z + k] = s_stage[TILE + k];
+    }
+}
+
+// Aggregates of caller-provided counts (replication_to_parents without pass B1).
+__global__ void __launch_bounds__(RT) k_rs_aggs(const int32_t *__restrict__ cin, int64_t n, Layout L)
+{
+    if (!L.hdr->active || L.hdr->trivial) return;
+    __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI>()];
+    int32_t c[RI];
+    load_blocked<RT, RI, int32_t>(cin, (int64_t)blockIdx.x * TILE, n, c, s_c, 1);
+#pragma unroll
+    for (int j = 0; j < RI; ++j) c[j] = c[j] < 0 ? 0 : c[j];  // k_rs_ranks raises ECOUNTS
+    tile_aggregate(c, blockIdx.x, L);
+}
 
 // Pass B1: counts per particle.  Embarrassingly parallel (no inter-tile wait);
 // the counts go to `counts` (the caller's or the workspace's).
 __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                   Key key, uint64_t stream, const double *__restrict__ u,
-                                                  int32_t *__restrict__ counts, Layout L)
+                                                  int32_t *__restrict__ counts, int ranks, Layout L)
 {
     RsHeader *h = L.hdr;
     if (!h->active) return;
@@ -565,121 +701,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
     }
     __syncthreads();  // s_fb may still be read by the residual staging path
     store_blocked<RT, RI, int32_t>(counts, tbase, n, c, s_fb);  // coalesced
-}
-
-// Pass B2: replication_to_parents' rank scan.  A cheap tile
-// (32 counts per thread) publishes its (zero slots, surplus children, surplus
-// parents) aggregate at once, then a DECOUPLED LOOKBACK finds its exclusive
-// prefix.  It emits the compacted surplus-parent list (index, first surplus
-// rank), rank anchors every ANCHOR ranks, and each slot tile's first zero rank.
-// Writes are per-thread contiguous runs; no 4-byte scatter.
-__global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int64_t nt2, int whole,
-                                                 int32_t *status, Layout L)
-{
-    RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
-    __shared__ uint64_t sm[RT / 32 + 1];
-    __shared__ uint32_t s_tile;
-    __shared__ uint4 s_excl;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&h->tile_ctr, 1u);  // dynamic tile id: predecessors already started
-    __syncthreads();
-    const int64_t b = s_tile;
-    const int64_t base = b * TILE2 + (int64_t)threadIdx.x * RI2;
-    int32_t c[RI2];
-    {
-        __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI2>()];
-        load_blocked<RT, RI2, int32_t>(cin, b * TILE2, n, c, s_c, 1);  // coalesced; pad: not zero, no surplus
-    }
-    bool bad = false;
-#pragma unroll
-    for (int j = 0; j < RI2; ++j)
-        if (c[j] < 0) { bad = true; c[j] = 0; }
-    if (bad) raise_status(status, SMC_ECOUNTS);
-    uint32_t tz = 0, tp = 0;
-    uint64_t ts = 0;
-#pragma unroll
-    for (int j = 0; j < RI2; ++j) {
-        tz += (c[j] == 0);
-        tp += (c[j] >= 2);
-        ts += c[j] >= 2 ? (uint64_t)(c[j] - 1) : 0;
-    }
-    uint64_t agg;
-    const uint64_t tex = block_exclusive_sum<RT, uint64_t>(pack_zsp(tz, tp, ts), sm, &agg);
-    const uint4 a4 = make_uint4(unz(agg), (uint32_t)uns(agg), unp(agg), 0);
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        uint4 ex = make_uint4(0, 0, 0, 0);
-        if (b == 0) {
-            if (lane == 0) {
-                L.lb_incl[0] = a4;
-                __threadfence();
-                atomicExch(&L.lb_status[0], 2u);
-            }
-        } else {
-            if (lane == 0) {
-                L.lb_agg[b] = a4;
-                __threadfence();
-                atomicExch(&L.lb_status[b], 1u);
-            }
-            int64_t pred = b - 1;
-            for (;;) {
-                const int64_t jb = pred - lane;
-                uint32_t stv = 2;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (jb >= 0) {
-                    do { stv = ld_status(&L.lb_status[jb]); } while (stv == 0);
-                    __threadfence();
-                    v = stv == 2 ? __ldcg(&L.lb_incl[jb]) : __ldcg(&L.lb_agg[jb]);
-                }
-                const unsigned m2 = __ballot_sync(0xffffffffu, stv == 2);
-                const int stop = m2 ? __ffs(m2) - 1 : 32;
-                if (lane > stop) v = make_uint4(0, 0, 0, 0);
-                ex.x += warp_sum(v.x);
-                ex.y += warp_sum(v.y);
-                ex.z += warp_sum(v.z);
-                if (m2) break;
-                pred -= 32;
-            }
-            if (lane == 0) {
-                L.lb_incl[b] = make_uint4(ex.x + a4.x, ex.y + a4.y, ex.z + a4.z, 0);
-                __threadfence();
-                atomicExch(&L.lb_status[b], 2u);
-            }
-        }
-        if (lane == 0) {
-            s_excl = ex;
-            if (b == nt2 - 1) {
-                const uint32_t Z = ex.x + a4.x, S = ex.y + a4.y, P = ex.z + a4.z;
-                h->Z_total = Z;
-                h->S_total = S;
-                h->P_total = P;
-                L.sp_start[P] = (int32_t)S;  // sentinel
-                L.tile_z0[(n + TILE - 1) / TILE] = (int32_t)Z;
-                // sum(counts) != N; a shard's Z and S only balance globally (host check)
-                if (whole && Z != S) raise_status(status, SMC_ECOUNTS);
-            }
-        }
-    }
-    __syncthreads();
-    uint32_t zr = s_excl.x + unz(tex);
-    uint32_t sr = s_excl.y + (uint32_t)uns(tex);
-    uint32_t pr = s_excl.z + unp(tex);
-#pragma unroll
-    for (int j = 0; j < RI2; ++j) {
-        const int64_t i = base + j;
-        if (i >= n) break;
-        if ((i & (TILE - 1)) == 0) L.tile_z0[i / TILE] = (int32_t)zr;  // first zero rank of slot tile i / TILE
-        zr += (c[j] == 0);
-        if (c[j] >= 2) {
-            L.sp_idx[pr] = (int32_t)i;
-            L.sp_start[pr] = (int32_t)sr;
-            const uint32_t se = sr + (uint32_t)(c[j] - 1);
-            for (uint32_t m = (sr + ANCHOR - 1) / ANCHOR * ANCHOR; m < se; m += ANCHOR)
-                L.anchor[m / ANCHOR] = (int32_t)pr;  // the surplus parent covering rank m
-            ++pr;
-            sr = se;
-        }
-    }
+    if (ranks) tile_aggregate(c, b, L);  // the parent map's per-tile (Z, S, P) for k_rs_zsp_scan
 }
 
 // ------------------------------------------------------------------ pass C --
@@ -859,17 +881,12 @@ __global__ void k_rs_export_zsp(Layout L, uint32_t *out)
     out[3] = h->active;
 }
 
-__global__ void k_rs_reset(int64_t n, int64_t nt, Layout L)
+__global__ void k_rs_reset(Layout L)
 {
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nt; b += (int64_t)gridDim.x * blockDim.x)
-        L.lb_status[b] = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        RsHeader *h = L.hdr;
-        h->active = 1;
-        h->trivial = 0;
-        h->tile_ctr = 0;
-        h->Z_total = h->S_total = h->P_total = 0;
-    }
+    RsHeader *h = L.hdr;
+    h->active = 1;
+    h->trivial = 0;
+    h->Z_total = h->S_total = h->P_total = 0;
 }
 
 __global__ void __launch_bounds__(RT) k_copy_inplace(char *rows, int64_t row_bytes, const int32_t *__restrict__ parents,
@@ -946,10 +963,11 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         k_rs_multinomial<<<grid_cap((m_out + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
     }
     int32_t *cout = counts ? counts : L.cnt;
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr,
+                                            L);
     if (parents) {
-        const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-        k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, 1, status, L);
+        k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
+        k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, status, 0, L);
         k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
@@ -972,9 +990,10 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
-    k_rs_reset<<<grid_cap((nt + 255) / 256), 256, 0, s>>>(n, nt, L);
-    const int64_t nt2 = (n + TILE2 - 1) / TILE2;
-    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(counts, n, nt2, 1, status, L);
+    k_rs_reset<<<1, 1, 0, s>>>(L);
+    k_rs_aggs<<<(unsigned)nt, RT, 0, s>>>(counts, n, L);
+    k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
+    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(counts, n, status, 1, L);
     k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
@@ -1060,7 +1079,7 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
         return smc_set_error(SMC_EINVAL, "smc_resample_shard_counts: bad shard args");
     if (counts && ((uintptr_t)counts & 15)) return smc_set_error(SMC_EINVAL, "smc_resample_shard_counts: counts");
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t nt = (n + TILE - 1) / TILE, nt2 = (n + TILE2 - 1) / TILE2;
+    const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     WSrc src{w, lw_raw, st, n_total};
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
@@ -1072,8 +1091,9 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
         k_rs_multinomial<<<grid_cap((m_total + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
     }
     int32_t *cout = counts ? counts : L.cnt;
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, L);
-    k_rs_ranks<<<(unsigned)nt2, RT, 0, s>>>(cout, n, nt2, 0, status, L);
+    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
+    k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 0, status, L);
+    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, status, 0, L);
     k_rs_export_zsp<<<1, 1, 0, s>>>(L, zsp_out);
     return smc_check_launch("smc_resample_shard_counts");
 }
