@@ -33,9 +33,11 @@ typedef int int32_t;
 #define SMC_HD __host__ __device__ __forceinline__
 #define SMC_HDM __host__ __device__ __forceinline__
 #define SMC_TABLE __device__ const
+#define SMC_CONSTANT __constant__
 #else
 #define SMC_HD static inline
 #define SMC_HDM inline
+#define SMC_CONSTANT static const
 #define SMC_TABLE static const
 #endif
 
@@ -48,6 +50,12 @@ struct LogEntry {
 SMC_TABLE LogEntry kLogTab[128] = {
 #include "smc_logtab.inc"
 };
+
+// Constants with non-zero low words live in the constant bank, so each FP64
+// instruction takes them as a c[][] operand (as literals they cost two UMOVs
+// per use in the issue stream).
+SMC_CONSTANT double kLogK[6] = {0x1.2492492492492p-3, -0x1.5555555555555p-3, 0x1.999999999999ap-3,
+                                0x1.5555555555555p-2, 0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45};
 
 SMC_HD uint64_t bits(double x)
 {
@@ -83,12 +91,10 @@ SMC_HD const LogEntry &log_entry(int i)
     return kLogTab[i];
 }
 
-// Natural log of a positive normal finite double; other inputs go to libm.
-SMC_HD double log(double x)
+// Natural log of a positive normal finite double (precondition; no check).
+SMC_HD double log_core(double x)
 {
     const uint64_t ix = bits(x);
-    // positive normal finite: exponent field in [1, 2046]
-    if ((ix >> 52) - 1u >= 2046u) return ::log(x);
     const uint64_t OFF = 0x3fe6000000000000ull;
     const uint64_t tmp = ix - OFF;
     const int i = (int)((tmp >> 45) & 127);
@@ -103,7 +109,7 @@ SMC_HD double log(double x)
 #endif
     const double r = fma_(z, invc, -1.0);
     const double kd = (double)k;
-    const double LN2_HI = 0x1.62e42fefa3800p-1, LN2_LO = 0x1.ef35793c76730p-45;
+    const double LN2_HI = kLogK[4], LN2_LO = kLogK[5];
     // hi + lo = k ln2 + log c + r with error-free sums (k LN2_HI is exact: 42 + 11 bits)
     const double a = kd * LN2_HI;
     const double w = a + lhi;
@@ -114,13 +120,20 @@ SMC_HD double log(double x)
     const double he = (w - (hi - hb)) + (r - hb);   // TwoSum(w, r)
     const double lo = (he + we) + fma_(kd, LN2_LO, llo);
     // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
-    double p = fma_(r, -0.125, 0x1.2492492492492p-3);
-    p = fma_(r, p, -0x1.5555555555555p-3);
-    p = fma_(r, p, 0x1.999999999999ap-3);
+    double p = fma_(r, -0.125, kLogK[0]);
+    p = fma_(r, p, kLogK[1]);
+    p = fma_(r, p, kLogK[2]);
     p = fma_(r, p, -0.25);
-    p = fma_(r, p, 0x1.5555555555555p-2);
+    p = fma_(r, p, kLogK[3]);
     p = fma_(r, p, -0.5);
     return hi + fma_(r * r, p, lo);
+}
+
+// Natural log; inputs that are not positive normal finite doubles go to libm.
+SMC_HD double log(double x)
+{
+    // positive normal finite: exponent field in [1, 2046]
+    return (bits(x) >> 52) - 1u < 2046u ? log_core(x) : ::log(x);
 }
 
 // cos(x) for |x| < 8; larger arguments go to libm.

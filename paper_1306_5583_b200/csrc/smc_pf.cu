@@ -36,7 +36,7 @@ SMC_DEV double cv_llh(double xp, double yp, double xo, double yo)
     const double ax = 1 + rx * rx / nu;
     const double ay = 1 + ry * ry / nu;
     const double p = ax * ay;
-    const double s = p < INFINITY ? smc_fm::log(p) : smc_fm::log(ax) + smc_fm::log(ay);
+    const double s = p < INFINITY ? smc_fm::log_core(p) : smc_fm::log(ax) + smc_fm::log(ay);  // p >= 1
     return -0.5 * (nu + 1) * s;
 }
 
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         double x0, x1, x2, x3;
         ld_row(x_in + 4 * src, x0, x1, x2, x3);
         if (MON) {
-            const double w = nl.eq ? w_equal : exp(prev);  // 1 / N_total after a resample
+            const double w = nl.eq ? w_equal : smc_fm::exp(prev, smc_fm::kExpTab);  // 1 / N_total after a resample
             h0 = w * x0;
             h1 = w * x1;
         }

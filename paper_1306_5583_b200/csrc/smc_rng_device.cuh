@@ -67,7 +67,7 @@ SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, Key key)
 {
     const double u1 = u01_at(ctr, stream, key);
     const double u2 = u01_at(ctr + 1, stream, key);
-    return sqrt(-2.0 * smc_fm::log(1.0 - u1)) * cos((2.0 * 3.141592653589793) * u2);
+    return sqrt(-2.0 * smc_fm::log_core(1.0 - u1)) * cos((2.0 * 3.141592653589793) * u2);  // 1 - u1 in [2^-53, 1]
 }
 
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the

@@ -25,7 +25,8 @@ SMC_DEV LsePartial block_lse_partial(double v)
     double bm = sm_m[0];
 #pragma unroll
     for (int w = 1; w < NT / 32; ++w) bm = fmax(bm, sm_m[w]);
-    double e = (v == -INFINITY) ? 0.0 : exp(v - bm);
+    // table exp (smc_fastmath.h, <= 0.52 ulp; -inf -> 0) from the L1-resident global table
+    double e = smc_fm::exp(v - bm, smc_fm::kExpTab);
     double s1 = warp_sum(e), s2 = warp_sum(e * e);
     if (lane == 0) { sm_s1[warp] = s1; sm_s2[warp] = s2; }
     __syncthreads();
