@@ -50,7 +50,7 @@ SMC_DEV void st_row(double *p, double a, double b, double c, double d)
 }
 
 __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *__restrict__ lw_raw, int64_t n,
-                                                uint64_t sbase, Key key, uint64_t *__restrict__ ctrs,
+                                                uint64_t sbase, const KeySched key, uint64_t *__restrict__ ctrs,
                                                 const double *__restrict__ obs,
                                                 PfConst k, smc_wstate *st, LsePartial *__restrict__ parts)
 {
@@ -83,7 +83,7 @@ template <bool MON>
 __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
                                                    double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
-                                                   double w_equal, Key key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
+                                                   double w_equal, const KeySched key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
@@ -177,7 +177,7 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t stream
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
     void *scratch = pf_scratch(ws, nb);
-    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, stream_base, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, ctrs, obs_t,
+    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, stream_base, make_key_sched(seed), ctrs, obs_t,
                                 pf_constants(), st, parts);
     smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     return smc_check_launch("smc_pf_init");
@@ -199,7 +199,7 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     LsePartial *parts = (LsePartial *)ws;
     double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
     void *scratch = pf_scratch(ws, nb);
-    const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
     if (monitor_prev) {
         k_pf_move<true><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,

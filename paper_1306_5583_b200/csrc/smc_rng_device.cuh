@@ -24,36 +24,59 @@ constexpr uint32_t PHILOX_W1 = 0xBB67AE85u;
 
 struct Key {
     uint32_t k0, k1;
+    SMC_DEV uint32_t r0(int r) const { return k0 + (uint32_t)r * PHILOX_W0; }
+    SMC_DEV uint32_t r1(int r) const { return k1 + (uint32_t)r * PHILOX_W1; }
+};
+
+// The ten round keys precomputed on the host.  Passed BY VALUE as a kernel
+// parameter it lives in the constant bank, so each round's xor takes its key
+// as a c[][] operand: no key-schedule instructions in the particle loop.
+struct KeySched {
+    uint32_t k0[10], k1[10];
+    SMC_DEV uint32_t r0(int r) const { return k0[r]; }
+    SMC_DEV uint32_t r1(int r) const { return k1[r]; }
 };
 
 SMC_DEV Key make_key(uint64_t seed) { return Key{(uint32_t)seed, (uint32_t)(seed >> 32)}; }
 
-SMC_DEV uint4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, Key key)
+#ifndef __CUDACC_RTC__
+inline KeySched make_key_sched(uint64_t seed)
 {
-    uint32_t k0 = key.k0, k1 = key.k1;
+    KeySched ks;
+    for (int r = 0; r < 10; ++r) {
+        ks.k0[r] = (uint32_t)seed + (uint32_t)r * PHILOX_W0;
+        ks.k1[r] = (uint32_t)(seed >> 32) + (uint32_t)r * PHILOX_W1;
+    }
+    return ks;
+}
+#endif
+
+template <class K>
+SMC_DEV uint4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const K &key)
+{
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
         const uint32_t hi0 = __umulhi(PHILOX_M0, c0), lo0 = PHILOX_M0 * c0;
         const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;
-        const uint32_t n0 = hi1 ^ c1 ^ k0;
-        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        const uint32_t n0 = hi1 ^ c1 ^ key.r0(r);
+        const uint32_t n2 = hi0 ^ c3 ^ key.r1(r);
         c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
-        k0 += PHILOX_W0;
-        k1 += PHILOX_W1;
     }
     return make_uint4(c0, c1, c2, c3);
 }
 
 // 53-bit integer of draw `ctr` of stream `stream` (rng.py:81-82):
 // ((w0 >> 5) << 26) | (w1 >> 6); the uniform is this times 2^-53, exactly.
-SMC_DEV uint64_t draw53(uint64_t ctr, uint64_t stream, Key key)
+template <class K>
+SMC_DEV uint64_t draw53(uint64_t ctr, uint64_t stream, const K &key)
 {
     const uint4 w = philox10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream,
                              (uint32_t)(stream >> 32), key);
     return ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
 }
 
-SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, Key key)
+template <class K>
+SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, const K &key)
 {
     return __dmul_rn(__ull2double_rn(draw53(ctr, stream, key)), 1.0 / 9007199254740992.0);
 }
@@ -63,7 +86,8 @@ SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, Key key)
 // log is smc_fastmath.h's table log (<= 0.55 ulp, 99.6 % bit-identical to glibc,
 // 8 % cheaper than libdevice on B200); cos is libdevice's (the fdlibm-style
 // smc_fm::cos diverges per quadrant and measured 40 % slower); sqrt is IEEE.)
-SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, Key key)
+template <class K>
+SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, const K &key)
 {
     const double u1 = u01_at(ctr, stream, key);
     const double u2 = u01_at(ctr + 1, stream, key);
@@ -72,7 +96,8 @@ SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, Key key)
 
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the
 // variable number of draws it consumes.
-SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, Key key, double shape)
+template <class K>
+SMC_DEV double gamma_from(uint64_t &ctr, uint64_t stream, const K &key, double shape)
 {
     double boost = 1.0;
     double a = shape;
