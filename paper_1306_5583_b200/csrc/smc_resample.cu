@@ -115,6 +115,8 @@ struct WSrc {
     SMC_DEV double weight(double r, const NormLw &nl) const  // the math
     {
         if (w) return r;
+        // libdevice exp: with 8 independent lookups per thread the table exp of
+        // smc_fastmath.h measured slower here (shared / L1 wavefronts)
         return nl.eq ? nl.weq : exp(nl(r));
     }
 };
@@ -408,6 +410,8 @@ struct StratCtx {
     const double *u;
     Key key;
     bool systematic;
+    bool force;     // test hook g_force_exact, read once per thread
+    double us_sys;  // m_sys 2^-53 (systematic)
 };
 
 SMC_DEV uint64_t m_of(const StratCtx &c, uint64_t s)
@@ -438,15 +442,14 @@ SMC_DEV uint64_t F_exact(const StratCtx &c, uint64_t X)
 SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
 {
     if (X >= c.Tm) return c.M;
-    if (X == 0) return 0;
     const double z = (double)X * c.ratio;
     const double fl = floor(z);
     const double fr = z - fl;
-    if (g_force_exact || fr < c.guard || fr > 1.0 - c.guard) return F_exact(c, X);
     const uint64_t s = (uint64_t)fl;
-    const double us = (double)m_of(c, s) * INV53;
+    const double us = c.systematic ? c.us_sys : (double)m_of(c, s) * INV53;
     const double d = fr - us;
-    if (d < c.guard && d > -c.guard) return F_exact(c, X);
+    // |fr - 1/2| > 1/2 - guard  <=>  fr < guard or fr > 1 - guard (X == 0 lands here too)
+    if (c.force || fabs(fr - 0.5) > 0.5 - c.guard || fabs(d) < c.guard) return F_exact(c, X);
     return s + (d > 0.0 ? 1 : 0);
 }
 
@@ -685,6 +688,8 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
             sc.u = u;
             sc.key = key;
             sc.systematic = is_systematic(scheme);
+            sc.force = g_force_exact != 0;
+            sc.us_sys = (double)sc.m_sys * INV53;
             uint64_t Fp = (base < n && sc.M) ? F_fast(sc, X) : 0;
 #pragma unroll
             for (int j = 0; j < RI; ++j) {
@@ -750,6 +755,7 @@ struct ShardC {
     int64_t row_bytes;
 };
 
+template <bool SHARD>
 __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
                                                   int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
@@ -806,7 +812,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     for (int j = 0; j < RI; ++j) {
         par[j] = (int32_t)(base + j);  // survivors keep their slot
         if (c[j] == 0) {
-            if (g >= soff && g < soff + s_self) {
+            if (!SHARD || (g >= soff && g < soff + s_self)) {
                 const int64_t s = g - soff;
                 while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
                 par[j] = s_idx[lo];
@@ -968,7 +974,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (parents) {
         k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
         k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, status, 0, L);
-        k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+        k_rs_assign<false><<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
                 k_rs_copy<32><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, 32, n, L);
@@ -994,7 +1000,7 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     k_rs_aggs<<<(unsigned)nt, RT, 0, s>>>(counts, n, L);
     k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
     k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(counts, n, status, 1, L);
-    k_rs_assign<<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+    k_rs_assign<false><<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
@@ -1132,7 +1138,7 @@ extern "C" int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     const int32_t *cin = counts ? counts : L.cnt;
-    k_rs_assign<<<(unsigned)nt, RT, 0, (cudaStream_t)stream>>>(
+    k_rs_assign<true><<<(unsigned)nt, RT, 0, (cudaStream_t)stream>>>(
         cin, n, parents, ShardC{zoff, soff, s_self, (const char *)recv, (char *)rows, row_bytes}, L);
     return smc_check_launch("smc_resample_shard_assign");
 }
