@@ -795,35 +795,59 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
             s_idx[k] = __ldcg(&L.sp_idx[a0 + k]);
         }
     }
+    if (threadIdx.x == 0) s_start[cnt] = 0x7fffffff;  // walk sentinel (cnt < CSTAGE)
     uint32_t tot;
-    const int64_t zr = z0 + block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);  // first local zero rank
+    const uint32_t ex = block_exclusive_sum<RT, uint32_t>(nz, sm32, &tot);
     int32_t par[RI];
     uint32_t lo = 0;
-    int64_t g = zoff + zr;  // global zero rank of this thread's next zero slot
-    if (nz && cnt) {  // last k with s_start[k] <= first local surplus rank, then a forward merge walk
-        const int64_t s0 = max(g, soff) - soff;
-        uint32_t hi = cnt;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if ((int64_t)s_start[mid] <= s0) lo = mid; else hi = mid;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < RI; ++j) {
-        par[j] = (int32_t)(base + j);  // survivors keep their slot
-        if (c[j] == 0) {
-            if (!SHARD || (g >= soff && g < soff + s_self)) {
-                const int64_t s = g - soff;
-                while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
-                par[j] = s_idx[lo];
-            } else if (sc.recv) {  // surplus child on another shard: its row arrived in recv
-                const int64_t k = g < soff ? g - zoff : g - zoff - piece;
-                const char *src = sc.recv + k * sc.row_bytes;
-                char *dst = sc.rows + (base + j) * sc.row_bytes;
-                for (int64_t b = 0; b < sc.row_bytes; b += 8)
-                    *(int64_t *)(dst + b) = __ldcg((const long long *)(src + b));
+    if (!SHARD) {
+        // one GPU: zero ranks and surplus ranks are the same 32-bit numbers
+        uint32_t g = (uint32_t)z0 + ex;  // zero rank of this thread's next zero slot
+        if (nz && cnt) {  // last k with s_start[k] <= g, then a forward merge walk
+            uint32_t hi = cnt;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((uint32_t)s_start[mid] <= g) lo = mid; else hi = mid;
             }
-            ++g;
+        }
+        const int32_t b32 = (int32_t)base;
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            par[j] = b32 + j;  // survivors keep their slot
+            if (c[j] == 0) {
+                while ((uint32_t)s_start[lo + 1] <= g) ++lo;
+                par[j] = s_idx[lo];
+                ++g;
+            }
+        }
+    } else {
+        const int64_t zr = z0 + ex;  // first local zero rank
+        int64_t g = zoff + zr;       // global zero rank of this thread's next zero slot
+        if (nz && cnt) {
+            const int64_t s0 = max(g, soff) - soff;
+            uint32_t hi = cnt;
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((int64_t)s_start[mid] <= s0) lo = mid; else hi = mid;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            par[j] = (int32_t)(base + j);
+            if (c[j] == 0) {
+                if (g >= soff && g < soff + s_self) {
+                    const int64_t s = g - soff;
+                    while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
+                    par[j] = s_idx[lo];
+                } else if (sc.recv) {  // surplus child on another shard: its row arrived in recv
+                    const int64_t k = g < soff ? g - zoff : g - zoff - piece;
+                    const char *src = sc.recv + k * sc.row_bytes;
+                    char *dst = sc.rows + (base + j) * sc.row_bytes;
+                    for (int64_t b = 0; b < sc.row_bytes; b += 8)
+                        *(int64_t *)(dst + b) = __ldcg((const long long *)(src + b));
+                }
+                ++g;
+            }
         }
     }
     store_blocked<RT, RI, int32_t>(parents, tbase, n, par, s_io);  // coalesced
