@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--scheme", default="systematic")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gmm", action="store_true")
     return ap.parse_args()
 
 
@@ -225,13 +226,15 @@ def run_b200(args):
     peak, peak_src = measured_peaks()
     move_bytes = n * (32 + 32 + 8 + 8 + 8) + n * 8 * float(np.mean(1 - prev_rs))
     move_gbs = move_bytes / (phase["move"] * 1e-3) / 1e9
-    # resample+copy: lw read twice (pass A + B) is implementation traffic; algorithmic = read W (8) +
-    # parents (4) + counts (4, not materialized here) + 64 B per moved row
-    st = s.system
-    par = st.parents.cpu().numpy()
-    frac_moved = float(np.mean(par != np.arange(n)))
-    rc_bytes = n * (8 + 4 + 4) + 64 * frac_moved * n
-    rc_gbs = rc_bytes / (phase["resample"] * 1e-3) / 1e9 if phase.get("resample") else None
+    # resample+copy (the metric's second half, SURVEY §8d config 5 at this N): smc_resample with the
+    # parent map AND the explicit in-place row copy on this run's own final weights, timed alone with
+    # CUDA events (inside the PF step the copy is folded into the next move's gather instead).
+    # Algorithmic bytes: W 8 R + counts 4 W + parents 4 W per particle + 64 B per moved 32-byte row.
+    # the weights right after the resample are equal: take one more move (no resample) so the
+    # benchmark resamples the PF's real pre-resample weight distribution
+    s.move_queue[0](s.iteration + 1, s.system)
+    rc = resample_copy_bench(P, s.system, args.scheme)
+    frac_moved = rc["moved_frac"]
     dominant = max(("move", "resample", "monitor"), key=lambda k: phase.get(k, 0))
 
     value = n_total * args.steps / (ms * 1e-3)
@@ -244,14 +247,19 @@ def run_b200(args):
                        "l2": "inputs larger than L2 (state 512 MiB/GPU at 2^24), no flush",
                        "parallelism": f"particles sharded over {world} GPU(s)"},
             "phase_ms": phase, "resampled_frac": float(np.mean(resampled)), "moved_row_frac": frac_moved,
-            "gpu_launches": args.steps * 10,
+            # per step: k_pf_move, k_lse_level1, k_lse_finalize, k_ess_decide, 6 resample passes
+            # (device-gated: they launch every step), k_set_equal
+            "gpu_launches": args.steps * 11,
             "roofline": {"bound": "hbm", "kernel": "k_pf_move (fused move + add_log_weight + lse/ESS partials)",
                          "achieved": move_gbs, "peak": peak, "unit": "GB/s", "frac": move_gbs / peak,
                          "traffic": None, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": move_bytes},
-            "resample_copy": {"achieved": rc_gbs, "peak": peak, "unit": "GB/s",
-                              "frac": None if rc_gbs is None else rc_gbs / peak,
-                              "algorithmic_bytes_per_step": rc_bytes, "scheme": args.scheme},
+            "resample_copy": {"achieved": rc["gbs"], "peak": peak, "unit": "GB/s", "frac": rc["gbs"] / peak,
+                              "ms": rc["ms"], "algorithmic_bytes": rc["bytes"], "scheme": args.scheme,
+                              "weights": "the PF's pre-resample weights (one extra move after the run)",
+                              "reps": rc["reps"],
+                              "kernels": "k_rs_tiles, k_rs_scan, k_rs_counts, k_rs_zsp_scan, k_rs_ranks, "
+                                         "k_rs_assign, k_rs_copy<32>"},
             "dominant_phase": dominant, "clocks": clk.summary()}
 
     # ---- e2e: the public API with host buffers: per step H2D the observation pair from pinned
@@ -260,6 +268,8 @@ def run_b200(args):
         e = run_e2e(P, s, obs, args.steps)
         line["e2e"] = {"value": n_total * args.steps / e["seconds"], "unit": UNIT,
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"]}
+    if rank == 0 and world == 1 and not args.no_gmm:
+        line["gmm"] = gmm_bench(P)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         cores = len(os.sched_getaffinity(0))
         ncpu = 1 << 22
@@ -270,6 +280,71 @@ def run_b200(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def gmm_bench(P, n=1 << 20, T=100):
+    """BASELINE config 3 alongside the PF line: the GMM SMC sampler (4 components, 1000 synthetic
+    points, prior annealing p = 2, T = 100, N = 2^20), initialize + iterate timed with CUDA events.
+    FP64-issue bound (3 MH blocks x 1000 points x 4 components per particle-iteration)."""
+    import torch
+    from paper_1306_5583_b200 import gmm
+    y = gmm.generate_data(1000, 1306)
+    w = gmm.make_sampler(4096, data=y, T=5, seed=1)  # warm-up (module load, first launches)
+    w.initialize()
+    w.iterate(5)
+    s = gmm.make_sampler(n, data=y, T=T, seed=1307)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s.initialize()
+    s.iterate(T)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"workload": "GMM config 3: N=2^20, 4 components, 1000 points, T=100, prior annealing p=2",
+            "value": n * T / (ms * 1e-3), "unit": "particle-iterations/s", "ms_per_run": ms,
+            "log_zconst_ds": s.log_zconst, "log_zconst_ps": s.path_log_zconst(),
+            "component_evals_per_s": n * (1 + 3 * T) * 1000 * 4 / (ms * 1e-3)}
+
+
+def resample_copy_bench(P, system, scheme, reps=10):
+    """smc_resample (counts + parents + in-place 32-byte row copy) on the system's current
+    normalized weights and a scratch copy of its state; mean ms over `reps` calls."""
+    import ctypes
+
+    import torch
+    from paper_1306_5583_b200 import _abi
+    n = system.size
+    w = system.weight_set.read_weight().contiguous()
+    x = system.value.data.clone()
+    counts = torch.empty(n, dtype=torch.int32, device="cuda")
+    parents = torch.empty(n, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(_abi.lib().smc_resample_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    rng = P.RngStreamSet(n + 1, 1306)
+    from paper_1306_5583_b200.resample import _scheme
+    sid = int(_scheme(scheme))
+
+    def call():
+        _abi.call("smc_resample", sid, _abi.ptr(w), None, None, n, n, rng.seed, n, rng.counter_ptr(n), None, 0,
+                  _abi.ptr(counts), _abi.ptr(parents), ctypes.c_void_p(x.data_ptr()), 32, None, _abi.ptr(status),
+                  _abi.ptr(ws), ws.numel(), _abi.stream())
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    if int(status.item()) != 0:
+        raise RuntimeError(f"resample+copy bench: device status {int(status.item())}")
+    ms = e0.elapsed_time(e1) / reps
+    moved = int((parents != torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
+    byts = n * (8 + 4 + 4) + 64 * moved
+    del x, ws
+    return {"ms": ms, "bytes": byts, "gbs": byts / (ms * 1e-3) / 1e9, "moved_frac": moved / n, "reps": reps}
 
 
 def run_e2e(P, s, obs, steps):

@@ -577,11 +577,11 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     const uint4 ex = __ldcg(&L.tile_excl[b]);
     uint32_t sr = ex.y + (uint32_t)uns(tex);
     uint32_t lp = unp(tex);  // tile-local surplus-parent index
-    const int64_t base = b * TILE + (int64_t)threadIdx.x * RI;
+    const int32_t base = (int32_t)(b * TILE) + (int32_t)threadIdx.x * RI;  // n < 2^31
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
-        if (c[j] >= 2 && base + j < n) {
-            s_stage[lp] = (int32_t)(base + j);
+        if (c[j] >= 2) {  // padding slots load as 1
+            s_stage[lp] = base + j;
             s_stage[TILE + lp] = (int32_t)sr;
             const uint32_t se = sr + (uint32_t)(c[j] - 1);
             for (uint32_t m = (sr + ANCHOR - 1) / ANCHOR * ANCHOR; m < se; m += ANCHOR)
