@@ -16,6 +16,10 @@ constexpr int PB = 256;
 #ifndef PF_MIN_BLOCKS
 #define PF_MIN_BLOCKS 4
 #endif
+#ifndef PF_PPT
+#define PF_PPT 4  // particles per thread in the move kernel
+#endif
+constexpr int MB = PB * PF_PPT;  // particles per move block
 
 struct PfConst {
     double sd_pos0, sd_vel0;  // init: 2, 1
@@ -79,7 +83,12 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // GATHER: the previous resample's copy is folded in -- row i is read from
 // x_in[parents[i]] (when the device gate says the resample ran) and written to
 // x_out[i], a second buffer: the "simultaneous" copy of SPEC.md:343 for free.
-template <bool MON>
+// PPT particles per thread (striped: particle base + k*PB, k < PPT, so every
+// warp access stays coalesced): the block's lse/ESS and monitor reductions are
+// paid once per PPT particles.  The body runs in a non-unrolled loop (code size:
+// the move is ~2.7k SASS); each particle's new log-weight parks in shared memory
+// until the block max is known.
+template <bool MON, int PPT>
 __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
                                                    double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
@@ -87,47 +96,83 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
-    const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
-    double v = -INFINITY;
+    __shared__ double s_v[PPT][PB];
+    const int64_t base = (int64_t)blockIdx.x * (PB * PPT) + threadIdx.x;
     double h0 = 0.0, h1 = 0.0;
-    if (i < n) {
-        const NormLw nl = norm_of(st);
-        const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
-        const int64_t src = (parents && (gate == nullptr || *gate != 0)) ? (int64_t)__ldg(parents + i) : i;
-        double x0, x1, x2, x3;
-        ld_row(x_in + 4 * src, x0, x1, x2, x3);
-        if (MON) {
-            const double w = nl.eq ? w_equal : smc_fm::exp(prev, smc_fm::kExpTab);  // 1 / N_total after a resample
-            h0 = w * x0;
-            h1 = w * x1;
+    const NormLw nl = norm_of(st);
+    const bool gathered = parents && (gate == nullptr || *gate != 0);
+    const double xo = obs[0], yo = obs[1];
+#pragma unroll 1
+    for (int q = 0; q < PPT; ++q) {
+        const int64_t i = base + (int64_t)q * PB;
+        double v = -INFINITY;
+        if (i < n) {
+            const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
+            const int64_t src = gathered ? (int64_t)__ldg(parents + i) : i;
+            double x0, x1, x2, x3;
+            ld_row(x_in + 4 * src, x0, x1, x2, x3);
+            if (MON) {
+                const double w = nl.eq ? w_equal : smc_fm::exp(prev, smc_fm::kExpTab);  // 1 / N_total after a resample
+                h0 += w * x0;
+                h1 += w * x1;
+            }
+            const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;
+            // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
+            x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
+            x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
+            x2 = x2 + (0.0 + k.sd_vel * normal_at(c + 4, si, key));
+            x3 = x3 + (0.0 + k.sd_vel * normal_at(c + 6, si, key));
+            ctrs[i] = c + 8;
+            st_row(x_out + 4 * i, x0, x1, x2, x3);
+            const double incw = cv_llh(x0, x1, xo, yo);
+            if (incw_out) incw_out[i] = incw;
+            v = prev + incw;  // add_log_weight(incw)
+            if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+            lw_raw[i] = v;
         }
-        const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;
-        // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
-        x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
-        x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
-        x2 = x2 + (0.0 + k.sd_vel * normal_at(c + 4, si, key));
-        x3 = x3 + (0.0 + k.sd_vel * normal_at(c + 6, si, key));
-        ctrs[i] = c + 8;
-        st_row(x_out + 4 * i, x0, x1, x2, x3);
-        const double incw = cv_llh(x0, x1, obs[0], obs[1]);
-        if (incw_out) incw_out[i] = incw;
-        v = prev + incw;  // add_log_weight(incw)
-        if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
-        lw_raw[i] = v;
+        s_v[q][threadIdx.x] = v;
     }
-    LsePartial p = block_lse_partial<PB>(v);
-    if (threadIdx.x == 0) parts[blockIdx.x] = p;
+    // block (max, sum e, sum e^2), e = exp(v - max): one pass over the parked values
+    __shared__ double s_red[3][PB / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double tm = s_v[0][threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < PPT; ++q) tm = fmax(tm, s_v[q][threadIdx.x]);
+    tm = warp_max(tm);
+    if (lane == 0) s_red[0][warp] = tm;
+    __syncthreads();
+    double bm = lane < PB / 32 ? s_red[0][lane] : -INFINITY;
+    bm = warp_max(bm);  // every warp reduces the 8 warp maxima itself: no second barrier
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const double e = smc_fm::exp(s_v[q][threadIdx.x] - bm, smc_fm::kExpTab);  // -inf -> 0
+        s1 += e;
+        s2 += e * e;
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
     if (MON) {
-        __shared__ double s_h[2][PB / 32];
         h0 = warp_sum(h0);
         h1 = warp_sum(h1);
-        if ((threadIdx.x & 31) == 0) { s_h[0][threadIdx.x >> 5] = h0; s_h[1][threadIdx.x >> 5] = h1; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double a = 0.0, b = 0.0;
-            for (int w = 0; w < PB / 32; ++w) { a += s_h[0][w]; b += s_h[1][w]; }
-            mon_parts[blockIdx.x] = make_double2(a, b);
+    }
+    __syncthreads();  // s_red[0] reads are done
+    if (lane == 0) {
+        s_red[1][warp] = s1;
+        s_red[2][warp] = s2;
+        if (MON) { s_v[0][warp] = h0; s_v[1 % PPT][PB / 32 + warp] = h1; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LsePartial p{bm, 0.0, 0.0};
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < PB / 32; ++w) {
+            p.s1 += s_red[1][w];
+            p.s2 += s_red[2][w];
+            if (MON) { a += s_v[0][w]; b += s_v[1 % PPT][PB / 32 + w]; }
         }
+        parts[blockIdx.x] = p;
+        if (MON) mon_parts[blockIdx.x] = make_double2(a, b);
     }
 }
 
@@ -146,7 +191,7 @@ PfConst pf_constants()
 
 extern "C" size_t smc_pf_workspace_bytes(int64_t n)
 {
-    return (size_t)((n + PB - 1) / PB + 1) * (sizeof(LsePartial) + sizeof(double2)) + smc_lse_scratch_bytes() + 512;
+    return (size_t)((n + PB - 1) / PB + 1) * (sizeof(LsePartial) + sizeof(double2)) + smc_lse_scratch_bytes() + 1024;
 }
 
 // workspace: [LsePartial nb+1][double2 nb+1][finalize scratch]
@@ -195,18 +240,18 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     if (parents && x_in == x)
         return smc_set_error(SMC_EINVAL, "smc_pf_move: a gathering move needs distinct in/out state buffers");
     cudaStream_t s = (cudaStream_t)stream;
-    const int nb = (int)((n + PB - 1) / PB);
+    const int nb = (int)((n + MB - 1) / MB);
     LsePartial *parts = (LsePartial *)ws;
     double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
     void *scratch = pf_scratch(ws, nb);
     const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
     if (monitor_prev) {
-        k_pf_move<true><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
+        k_pf_move<true, PF_PPT><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
                                           pf_constants(), st, incw_out, parts, mon);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev, partial_out);
     } else {
-        k_pf_move<false><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
+        k_pf_move<false, PF_PPT><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
                                            pf_constants(), st, incw_out, parts, nullptr);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     }
