@@ -99,9 +99,49 @@ SMC_DEV int tpad(int i) { return i + i / (128 / (int)sizeof(T)); }
 template <typename T, int NT, int ITEMS>
 constexpr int tile_smem_elems() { return NT * ITEMS + NT * ITEMS / (128 / (int)sizeof(T)) + 1; }
 
+// Full, 32-byte-aligned tiles skip the transpose: each thread's ITEMS
+// consecutive items are whole 32-byte sectors, read / written with 256-bit
+// accesses (every sector of every instruction fully used).  Partial tiles take
+// the shared-memory path.  The choice is per block (uniform), so the barriers
+// of the fallback stay convergent.
+SMC_DEV void ld_sector(const void *p, uint64_t (&w)[4])
+{
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p));
+}
+SMC_DEV void st_sector(void *p, const uint64_t (&w)[4])
+{
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(w[0]), "l"(w[1]), "l"(w[2]), "l"(w[3])
+                 : "memory");
+}
+
+template <int NT, int ITEMS, typename T>
+SMC_DEV bool vector_tile(const T *g, int64_t base, int64_t n)
+{
+    return (ITEMS * sizeof(T)) % 32 == 0 && (sizeof(T) == 4 || sizeof(T) == 8) && base + NT * ITEMS <= n &&
+           (((uintptr_t)(g + base)) & 31) == 0;
+}
+
 template <int NT, int ITEMS, typename T>
 SMC_DEV void load_blocked(const T *__restrict__ g, int64_t base, int64_t n, T (&v)[ITEMS], T *sm, T pad)
 {
+    if (vector_tile<NT, ITEMS, T>(g, base, n)) {
+        const char *p = (const char *)(g + base + (int64_t)threadIdx.x * ITEMS);
+#pragma unroll
+        for (int c = 0; c < (int)(ITEMS * sizeof(T)) / 32; ++c) {
+            uint64_t w[4];
+            ld_sector(p + 32 * c, w);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (sizeof(T) == 8) {
+                    v[c * 4 + k] = (T)w[k];
+                } else {
+                    v[c * 8 + 2 * k] = (T)(uint32_t)w[k];
+                    v[c * 8 + 2 * k + 1] = (T)(uint32_t)(w[k] >> 32);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) {
         const int li = j * NT + threadIdx.x;
@@ -116,6 +156,22 @@ SMC_DEV void load_blocked(const T *__restrict__ g, int64_t base, int64_t n, T (&
 template <int NT, int ITEMS, typename T>
 SMC_DEV void store_blocked(T *__restrict__ g, int64_t base, int64_t n, const T (&v)[ITEMS], T *sm)
 {
+    if (vector_tile<NT, ITEMS, T>(g, base, n)) {
+        char *p = (char *)(g + base + (int64_t)threadIdx.x * ITEMS);
+#pragma unroll
+        for (int c = 0; c < (int)(ITEMS * sizeof(T)) / 32; ++c) {
+            uint64_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (sizeof(T) == 8)
+                    w[k] = (uint64_t)v[c * 4 + k];
+                else
+                    w[k] = (uint64_t)(uint32_t)v[c * 8 + 2 * k] | ((uint64_t)(uint32_t)v[c * 8 + 2 * k + 1] << 32);
+            }
+            st_sector(p + 32 * c, w);
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < ITEMS; ++j) sm[tpad<T>(threadIdx.x * ITEMS + j)] = v[j];
     __syncthreads();
