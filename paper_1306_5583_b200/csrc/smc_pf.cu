@@ -102,13 +102,30 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
     const NormLw nl = norm_of(st);
     const bool gathered = parents && (gate == nullptr || *gate != 0);
     const double xo = obs[0], yo = obs[1];
+    // software prefetch: the next particle's counter, parent index and old log-weight are
+    // requested before this particle's normals, so their latency hides behind the Philox work
+    uint64_t c_nx = 0;
+    int64_t src_nx = base;
+    double lw_nx = 0.0;
+    if (base < n) {
+        c_nx = ctrs[base];
+        if (gathered) src_nx = __ldg(parents + base);
+        if (nl.needs_raw()) lw_nx = lw_raw[base];
+    }
 #pragma unroll 1
     for (int q = 0; q < PPT; ++q) {
         const int64_t i = base + (int64_t)q * PB;
         double v = -INFINITY;
+        const uint64_t c = c_nx;
+        const int64_t src = src_nx;
+        const double lw_prev = lw_nx;
+        if (q + 1 < PPT && i + PB < n) {
+            c_nx = ctrs[i + PB];
+            src_nx = gathered ? (int64_t)__ldg(parents + i + PB) : i + PB;
+            if (nl.needs_raw()) lw_nx = lw_raw[i + PB];
+        }
         if (i < n) {
-            const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);  // normalized W_{t-1}; no read if equal
-            const int64_t src = gathered ? (int64_t)__ldg(parents + i) : i;
+            const double prev = nl(lw_prev);  // normalized W_{t-1}; no read if equal
             double x0, x1, x2, x3;
             ld_row(x_in + 4 * src, x0, x1, x2, x3);
             if (MON) {
@@ -116,7 +133,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
                 h0 += w * x0;
                 h1 += w * x1;
             }
-            const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;
+            const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
             x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
             x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
