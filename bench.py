@@ -252,7 +252,7 @@ def run_b200(args):
             "gpu_launches": args.steps * 11,
             "roofline": {"bound": "hbm", "kernel": "k_pf_move (fused move + add_log_weight + lse/ESS partials)",
                          "achieved": move_gbs, "peak": peak, "unit": "GB/s", "frac": move_gbs / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": move_traffic(n), "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": move_bytes},
             "resample_copy": {"achieved": rc["gbs"], "peak": peak, "unit": "GB/s", "frac": rc["gbs"] / peak,
                               "ms": rc["ms"], "algorithmic_bytes": rc["bytes"], "scheme": args.scheme,
@@ -305,6 +305,17 @@ def gmm_bench(P, n=1 << 20, T=100):
             "value": n * T / (ms * 1e-3), "unit": "particle-iterations/s", "ms_per_run": ms,
             "log_zconst_ds": s.log_zconst, "log_zconst_ps": s.path_log_zconst(),
             "component_evals_per_s": n * (1 + 3 * T) * 1000 * 4 / (ms * 1e-3)}
+
+
+def move_traffic(n):
+    """DRAM bytes (read + write) per k_pf_move launch from the committed ncu --set full capture
+    (profiles/r1_move_traffic.json), when it was taken at this N; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_move_traffic.json")) as f:
+            d = json.load(f)
+        return d["dram_bytes_read"] + d["dram_bytes_write"] if d.get("n") == n else None
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def resample_copy_bench(P, system, scheme, reps=10):
