@@ -14,7 +14,8 @@
 //   A  k_rs_tiles   : per-tile u128 sums of q, sums of f and q'; validation.
 //   S  k_rs_scan    : one block: T, R, window check, tile prefixes, the stream
 //                     counter advance (on device: no host sync).
-//  [M  k_rs_prefix + k_rs_multinomial: multinomial/residual histogram]
+//  [M  k_rs_prefix + k_mn_{count,scan,scatter,assign}: multinomial/residual histogram
+//      with the draws bucketed by tile]
 //   B  k_rs_counts  : per tile (coalesced loads staged through shared memory),
 //                     local scan + tile prefix -> Q; counts in O(1) per particle
 //                     via F(X) = #{k : P_k < X} (fp64 with a guard band, exact
@@ -57,6 +58,7 @@ struct RsHeader {
     int32_t trivial;  // N == 1
     uint32_t Z_total, S_total, P_total;
     uint64_t qoff;    // this shard's CDF offset (0 on one GPU)
+    int32_t mn_direct;  // multinomial: too many positions for the buckets -> direct search
 };
 
 struct Layout {
@@ -71,6 +73,9 @@ struct Layout {
     int32_t *tile_z0;   // per slot tile: its first zero rank (and Z at index nt)
     uint64_t *qfull;
     int32_t *cnt;       // multinomial histogram, then the counts when the caller passes none
+    uint32_t *mn_cnt, *mn_off, *mn_fill;  // multinomial: draws per position bin, offsets, fill pointers
+    uint64_t *mn_pos;   // multinomial: positions bucketed by bin
+    uint32_t *mn_start; // multinomial: first particle of every bin
     size_t bytes;
 };
 
@@ -96,6 +101,12 @@ Layout layout(void *ws, int64_t n)
     L.tile_z0 = (int32_t *)take(sizeof(int32_t) * (nt + 2));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
+    const int64_t nbins = (n + 255) / 256;  // MN_BIN
+    L.mn_cnt = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
+    L.mn_off = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
+    L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
+    L.mn_pos = (uint64_t *)take(sizeof(uint64_t) * n);  // bucket capacity n positions
+    L.mn_start = (uint32_t *)take(sizeof(uint32_t) * (nbins + 2));
     L.bytes = o;
     return L;
 }
@@ -364,7 +375,12 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
 __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                   Layout L)
 {
-    if (!L.hdr->active || L.hdr->trivial || L.hdr->M == 0) return;
+    if (!L.hdr->active || L.hdr->trivial) return;
+    {  // zero the multinomial bin counters (nbins = n / 256 <= nt * RT)
+        const int64_t b = (int64_t)blockIdx.x * RT + threadIdx.x;
+        if (b <= (n + 255) / 256) L.mn_cnt[b] = 0;
+    }
+    if (L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
     const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * RI;  // blocked
     uint64_t v[RI];
@@ -383,12 +399,196 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     }
 }
 
-// One thread per draw: position P_k = floor(m_k Tm / 2^53), particle = first i
-// with Q_i > P_k; histogram by atomics (counts are order-independent, A.3).
-__global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+// Multinomial positions P_k = floor(m_k Tm / 2^53) (A.3) are iid over the whole CDF,
+// so a per-draw binary search over Q diverges across a warp at every level (32
+// cache lines per load).  Instead the draws are first COUNTING-SORTED into NB
+// equal-width position bins (bin = an arithmetic, monotone function of P: no
+// search), regenerating each draw from its counter rather than storing it
+// twice; then the bucketed positions, now nearly sorted, are searched: a warp's
+// 32 searches share their paths down to the last few levels, so those loads
+// broadcast.  Counts are order-independent integer sums: bit-identical to any
+// other evaluation order.
+constexpr int MN_BIN = 256;  // particles per position bin (on average)
+
+SMC_DEV int64_t mn_bins(int64_t n) { return (n + MN_BIN - 1) / MN_BIN; }
+
+struct MnCtx {
+    uint64_t M, Tm, c0, lo, hi;  // [lo, hi): this shard's slice of the CDF
+    uint32_t nb;
+    uint64_t W;                  // bin width: bin b = positions [lo + b W, lo + (b+1) W)
+    double invW;
+    SMC_DEV uint32_t bin(uint64_t P) const  // exact floor((P - lo) / W)
+    {
+        const uint64_t d = P - lo;
+        uint64_t b = (uint64_t)((double)d * invW);
+        while (b && b * W > d) --b;
+        while ((b + 1) * W <= d) ++b;
+        return (uint32_t)(b < nb ? b : nb - 1);
+    }
+};
+
+SMC_DEV MnCtx mn_ctx(const Layout &L, int64_t n)
+{
+    const RsHeader *h = L.hdr;
+    MnCtx c;
+    c.M = h->M;
+    c.Tm = h->Tm;
+    c.c0 = h->c0;
+    c.lo = h->qoff;
+    c.hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
+    c.nb = (uint32_t)mn_bins(n);
+    const uint64_t span = c.hi > c.lo ? c.hi - c.lo : 1;
+    c.W = span / c.nb + 1;  // nb W > span: every position has a bin
+    c.invW = 1.0 / (double)c.W;
+    return c;
+}
+
+SMC_DEV uint64_t mn_position(const MnCtx &c, uint64_t k, const Key &key, uint64_t stream, const double *u)
+{
+    const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c.c0 + k, stream, key);
+    return (uint64_t)(((u128)m * c.Tm) >> 53);
+}
+
+// atomicAdd(&a[key], 1) for a warp, one atomic when every active lane shares the key
+// (degenerate weights send every draw to one bin / one particle: without this the
+// same-address atomics serialize).  Returns the lane's slot (old value + rank).
+SMC_DEV uint32_t agg_inc(uint32_t *a, uint32_t key, bool active)
+{
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!act) return 0;
+    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+    const uint32_t k0 = __shfl_sync(0xffffffffu, key, leader);
+    if (__all_sync(0xffffffffu, !active || key == k0)) {  // the whole warp hits one counter
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&a[k0], (uint32_t)__popc(act));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        return base + __popc(act & ((1u << lane) - 1));
+    }
+    return active ? atomicAdd(&a[key], 1u) : 0;
+}
+
+__global__ void k_mn_count(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
 {
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
+    const MnCtx c = mn_ctx(L, n);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t kend = (c.M + stride - 1) / stride * stride;  // whole warps iterate together
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
+        const uint64_t P = k < c.M ? mn_position(c, k, key, stream, u) : c.lo;
+        const bool in = k < c.M && P >= c.lo && P < c.hi;  // else: past the end, or on another shard
+        agg_inc(L.mn_cnt, in ? c.bin(P) : 0u, in);
+    }
+}
+
+// one block: exclusive bucket offsets; fill pointers back to zero
+__global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    __shared__ uint64_t sm64[SB / 32 + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = SB / 32;
+    const int64_t nt = nbins;
+    const int64_t C = (nt + NW - 1) / NW;
+    const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
+    uint64_t wsum = 0;
+    for (int64_t b = w0 + lane; b < w1; b += 32) wsum += L.mn_cnt[b];
+    wsum = warp_sum(wsum);
+    if (lane == 0) sm64[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t x = sm64[lane];
+        const uint64_t inc = warp_inclusive_sum(x);
+        sm64[lane] = inc - x;
+    }
+    __syncthreads();
+    uint64_t carry = sm64[warp];
+    for (int64_t b0 = w0; b0 < w1; b0 += 32) {
+        const int64_t b = b0 + lane;
+        const uint64_t v = b < w1 ? L.mn_cnt[b] : 0;
+        const uint64_t inc = warp_inclusive_sum(v);
+        if (b < w1) {
+            L.mn_off[b] = (uint32_t)(carry + inc - v);
+            L.mn_fill[b] = 0;
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (warp == NW - 1 && lane == 31) {
+        L.mn_off[nt] = (uint32_t)carry;  // total positions in this shard
+        L.hdr->mn_direct = carry > (uint64_t)cap;  // buckets hold `cap` positions
+    }
+}
+
+// first particle of every bin: mn_start[b] = first i with Q_i > lo + b W (b = 0..nb)
+__global__ void k_mn_starts(int64_t n, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial || h->mn_direct) return;
+    const MnCtx c = mn_ctx(L, n);
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= c.nb; b += gridDim.x * blockDim.x) {
+        const uint64_t X = c.lo + (uint64_t)b * c.W;
+        int64_t lo = 0, hi = n - 1;
+        if (X >= c.hi) lo = n - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(&L.qfull[mid]) > X) hi = mid; else lo = mid + 1;
+        }
+        L.mn_start[b] = (uint32_t)lo;
+    }
+}
+
+__global__ void k_mn_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    if (h->mn_direct) return;  // more positions than bucket capacity (a shard): k_rs_multinomial
+    const MnCtx c = mn_ctx(L, n);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t kend = (c.M + stride - 1) / stride * stride;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
+        const uint64_t P = k < c.M ? mn_position(c, k, key, stream, u) : c.lo;
+        const bool in = k < c.M && P >= c.lo && P < c.hi;
+        const uint32_t b = in ? c.bin(P) : 0u;
+        const uint32_t r = agg_inc(L.mn_fill, b, in);
+        if (in) L.mn_pos[__ldg(&L.mn_off[b]) + r] = P;
+    }
+}
+
+// per bucketed position: first i with Q_i > P (Q inclusive, materialized by k_rs_prefix),
+// searched only between its bin's first particles
+__global__ void k_mn_assign(int64_t n, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    if (h->mn_direct) return;
+    const MnCtx c = mn_ctx(L, n);
+    const uint32_t total = __ldg(&L.mn_off[mn_bins(n)]);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t jend = (total + stride - 1) / stride * stride;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jend; j += stride) {
+        const bool in = j < total;
+        int64_t lo = 0;
+        if (in) {
+            const uint64_t P = L.mn_pos[j];
+            const uint32_t b = c.bin(P);
+            lo = __ldg(&L.mn_start[b]);
+            int64_t hi = __ldg(&L.mn_start[b + 1]);
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(&L.qfull[mid]) > P) hi = mid; else lo = mid + 1;
+            }
+        }
+        agg_inc(reinterpret_cast<uint32_t *>(L.cnt), (uint32_t)lo, in);
+    }
+}
+
+// Direct fallback (a shard receiving more draws than its bucket capacity): per draw,
+// binary search over this shard's whole Q.
+__global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+{
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial || !h->mn_direct) return;
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M; k += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c0 + k, stream, key);
@@ -989,8 +1189,14 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
                                nullptr, 1, 0, n);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
+        const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
-        k_rs_multinomial<<<grid_cap((m_out + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_scan<<<1, SB, 0, s>>>((n + 255) / 256, n, L);
+        k_mn_starts<<<(unsigned)((n / 256 + 2 + RT - 1) / RT), RT, 0, s>>>(n, L);
+        k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_assign<<<gm, RT, 0, s>>>(n, L);
+        k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr,
@@ -1117,8 +1323,14 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_total, key, stream_index, ctr, u, n_u, gate, status, L,
                                totals_all, G, rank, n_total);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
+        const unsigned gm = grid_cap((m_total + RT - 1) / RT);
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
-        k_rs_multinomial<<<grid_cap((m_total + RT - 1) / RT), RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_scan<<<1, SB, 0, s>>>((n + 255) / 256, n, L);
+        k_mn_starts<<<(unsigned)((n / 256 + 2 + RT - 1) / RT), RT, 0, s>>>(n, L);
+        k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
+        k_mn_assign<<<gm, RT, 0, s>>>(n, L);
+        k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
     k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
