@@ -783,11 +783,8 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
         if (c[j] >= 2) {  // padding slots load as 1
             s_stage[lp] = base + j;
             s_stage[TILE + lp] = (int32_t)sr;
-            const uint32_t se = sr + (uint32_t)(c[j] - 1);
-            for (uint32_t m = (sr + ANCHOR - 1) / ANCHOR * ANCHOR; m < se; m += ANCHOR)
-                L.anchor[m / ANCHOR] = (int32_t)(ex.z + lp);
             ++lp;
-            sr = se;
+            sr += (uint32_t)(c[j] - 1);
         }
     }
     __syncthreads();
@@ -795,6 +792,23 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     for (uint32_t k = threadIdx.x; k < np; k += RT) {
         L.sp_idx[ex.z + k] = s_stage[k];
         L.sp_start[ex.z + k] = s_stage[TILE + k];
+    }
+    // rank anchors: every multiple of ANCHOR in this tile's surplus ranks [ex.y, ex.y + S_tile),
+    // spread over the block (a parent with a huge surplus -- degenerate weights -- would
+    // otherwise write N/ANCHOR anchors from one thread); owner by search in the staged starts
+    // a shard's surplus can exceed its n slots (children leaving for other shards): anchors
+    // exist for ranks < (n/ANCHOR + 2) ANCHOR only -- all pass C needs (its ranks are < n);
+    // k_rs_pack searches beyond them
+    const uint32_t cap_r = (uint32_t)(n / ANCHOR + 2) * ANCHOR;  // the anchor buffer's extent in ranks
+    const uint32_t s0 = ex.y, s1 = min(ex.y + (uint32_t)uns(agg), cap_r);
+    for (uint32_t a = (s0 + ANCHOR - 1) / ANCHOR + threadIdx.x; a * ANCHOR < s1 && np; a += RT) {
+        const uint32_t r = a * ANCHOR;
+        uint32_t lo = 0, hi = np;  // last k with start_k <= r
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint32_t)s_stage[TILE + mid] <= r) lo = mid; else hi = mid;
+        }
+        L.anchor[a] = (int32_t)(ex.z + lo);
     }
 }
 
@@ -986,9 +1000,23 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     const int64_t lo_s = max(zoff + z0, soff) - soff, hi_s = min(zoff + z1, soff + s_self) - soff;
     uint32_t cnt = 0;
     if (hi_s > lo_s) {
-        const uint32_t a0 = (uint32_t)__ldcg(&L.anchor[lo_s / ANCHOR]);
+        // surplus parents covering [lo_s, hi_s): from the rank anchors where they exist
+        // (k_rs_ranks writes them for ranks < (n/ANCHOR + 2) ANCHOR), else by binary search --
+        // a shard's pairs can sit at local surplus ranks beyond its n slots
+        const int64_t acap = n / ANCHOR + 2;
+        auto owner = [&](int64_t r) {  // last p with sp_start[p] <= r
+            int64_t a = 0, b = P;
+            while (b - a > 1) {
+                const int64_t mid = (a + b) >> 1;
+                if ((int64_t)__ldcg(&L.sp_start[mid]) <= r) a = mid; else b = mid;
+            }
+            return (uint32_t)a;
+        };
+        const uint32_t a0 = lo_s / ANCHOR < acap ? (uint32_t)__ldcg(&L.anchor[lo_s / ANCHOR]) : owner(lo_s);
         const int64_t ka = (hi_s - 1) / ANCHOR + 1;
-        const uint32_t a1 = ka * ANCHOR < Sl ? (uint32_t)__ldcg(&L.anchor[ka]) : (uint32_t)(P - 1);
+        const uint32_t a1 = ka * ANCHOR >= Sl ? (uint32_t)(P - 1)
+                          : ka < acap        ? (uint32_t)__ldcg(&L.anchor[ka])
+                                             : owner(hi_s - 1);
         cnt = a1 - a0 + 1;
         for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
             s_start[k] = __ldcg(&L.sp_start[a0 + k]);
@@ -1061,8 +1089,8 @@ struct PackRanges {
     int64_t total;
 };
 
-__global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, PackRanges pr, char *__restrict__ out,
-                          Layout L)
+__global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, int64_t n, PackRanges pr,
+                          char *__restrict__ out, Layout L)
 {
     const int64_t Sl = L.hdr->S_total, P = L.hdr->P_total;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pr.total; k += (int64_t)gridDim.x * blockDim.x) {
@@ -1070,8 +1098,18 @@ __global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, Pack
         while (r + 1 < pr.K && k >= pr.off[r + 1]) ++r;
         const int64_t s = pr.lo[r] + (k - pr.off[r]);  // local surplus rank
         if (s >= Sl) continue;
-        int64_t p = __ldcg(&L.anchor[s / ANCHOR]);
-        while (p + 1 < P && (int64_t)__ldcg(&L.sp_start[p + 1]) <= s) ++p;  // <= ANCHOR steps
+        int64_t p;
+        if (s / ANCHOR < n / ANCHOR + 2) {  // anchored ranks (k_rs_ranks)
+            p = __ldcg(&L.anchor[s / ANCHOR]);
+            while (p + 1 < P && (int64_t)__ldcg(&L.sp_start[p + 1]) <= s) ++p;  // <= ANCHOR steps
+        } else {  // beyond the anchors: last p with sp_start[p] <= s
+            int64_t lo = 0, hi = P;
+            while (hi - lo > 1) {
+                const int64_t mid = (lo + hi) >> 1;
+                if ((int64_t)__ldcg(&L.sp_start[mid]) <= s) lo = mid; else hi = mid;
+            }
+            p = lo;
+        }
         const int64_t src = __ldcg(&L.sp_idx[p]);
         for (int64_t b = 0; b < row_bytes; b += 8)
             *(int64_t *)(out + k * row_bytes + b) = __ldg((const long long *)(rows + src * row_bytes + b));
@@ -1359,7 +1397,7 @@ extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, int6
     if (!off) return SMC_OK;
     Layout L = layout(ws, n);
     const int bs = 256;
-    k_rs_pack<<<grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>((const char *)rows, row_bytes, pr,
+    k_rs_pack<<<grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>((const char *)rows, row_bytes, n, pr,
                                                                               (char *)sendbuf, L);
     return smc_check_launch("smc_resample_shard_pack");
 }

@@ -21,8 +21,9 @@ def _ws(n):
 
 
 @pytest.mark.parametrize("scheme", SCHEMES)
-@pytest.mark.parametrize("G,n", [(2, 3000), (4, 2048), (3, 5001), (8, 700)])
-def test_sharded_resample_equals_single(scheme, G, n):
+@pytest.mark.parametrize("G,n,kind", [(2, 3000, "heavy"), (4, 2048, "heavy"), (3, 5001, "heavy"), (8, 700, "heavy"),
+                                      (4, 4096, "last_shard"), (3, 2500, "first_shard")])
+def test_sharded_resample_equals_single(scheme, G, n, kind):
     from paper_1306_5583_b200 import _abi
     from paper_1306_5583_b200.dist import exchange_plan
     from paper_1306_5583_b200.resample import _scheme
@@ -31,7 +32,12 @@ def test_sharded_resample_equals_single(scheme, G, n):
     N = G * n
     rng = np.random.default_rng(N + sid)
     lw = rng.normal(0, 2.5, N)
-    lw[rng.integers(N)] += 6.0  # one heavy particle: lots of cross-shard surplus
+    if kind == "heavy":
+        lw[rng.integers(N)] += 6.0  # one heavy particle: lots of cross-shard surplus
+    elif kind == "last_shard":  # (almost) all weight on the last shard: its surplus ranks run far past n
+        lw[:-n] -= 40.0
+    else:  # ... or on the first: every other shard is all zero slots
+        lw[n:] -= 40.0
     w = O.normalize_log(lw)[1]
     u = rng.random(N)
     x = rng.normal(size=(N, 4))
