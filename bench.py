@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=N_DEFAULT,
+                    help="particles per GPU (use --particles under torchrun: it claims --n*)")
     ap.add_argument("--scheme", default="systematic")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -171,10 +172,19 @@ def run_b200(args):
     import torch
 
     rank, local, world = dist_env()
+    # SMC_BENCH_FUNCTIONAL=1: a functional check of the multi-rank path on ONE GPU (every rank on
+    # cuda:0, host-staged gloo collectives, so no kernel waits on another rank's kernel).  Its
+    # timings are meaningless; the driver's runs use NCCL with one GPU per rank.
+    functional = os.environ.get("SMC_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1306_5583_b200 as P
 
     n_total = args.n * world if world > 1 else args.n  # weak scaling: N per GPU fixed
@@ -326,7 +336,10 @@ def resample_copy_bench(P, system, scheme, reps=10):
     import torch
     from paper_1306_5583_b200 import _abi
     n = system.size
-    w = system.weight_set.read_weight().contiguous()
+    w = system.weight_set.read_weight()
+    if system.shard is not None:  # a shard's weights sum to its share of the global mass
+        w = w / w.sum()
+    w = w.contiguous()
     x = system.value.data.clone()
     counts = torch.empty(n, dtype=torch.int32, device="cuda")
     parents = torch.empty(n, dtype=torch.int32, device="cuda")

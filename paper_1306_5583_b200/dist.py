@@ -89,17 +89,33 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves host memory only: CUDA tensors are staged through the host (CPU tests and
+        # the one-GPU functional check of the multi-rank bench); NCCL takes device memory
+        self.staged = dist.get_backend(group) == "gloo"
 
     def allgather(self, t):
+        if self.staged:
+            h = t.detach().cpu().contiguous()
+            out = torch.empty((self.world,) + tuple(h.shape), dtype=h.dtype)
+            self.dist.all_gather(list(out.unbind(0)), h, group=self.group)
+            return out.to(t.device)
         out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        if t.is_cuda:
-            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        else:  # gloo (CPU tests)
-            self.dist.all_gather(list(out.unbind(0)), t.contiguous(), group=self.group)
+        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
         return out
 
     def exchange(self, sends, recvs):
         """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- one grouped send/recv round."""
+        if self.staged:
+            hs = [(p, t.detach().cpu().contiguous()) for p, t in sends if t.numel()]
+            hr = [(p, t, torch.empty(t.shape, dtype=t.dtype)) for p, t in recvs if t.numel()]
+            ops = [self.dist.P2POp(self.dist.isend, h, p, group=self.group) for p, h in hs]
+            ops += [self.dist.P2POp(self.dist.irecv, h, p, group=self.group) for p, _, h in hr]
+            if ops:
+                for w in self.dist.batch_isend_irecv(ops):
+                    w.wait()
+            for _, t, h in hr:
+                t.copy_(h)
+            return
         ops = [self.dist.P2POp(self.dist.isend, t, p, group=self.group) for p, t in sends if t.numel()]
         ops += [self.dist.P2POp(self.dist.irecv, t, p, group=self.group) for p, t in recvs if t.numel()]
         if ops:
