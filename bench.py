@@ -157,11 +157,14 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles, {args.scheme} resampling, "
-                                   "ESS<N/2, 4-dim state, Student-t(10) likelihood", "n_particles": n,
-                       "scheme": args.scheme},
+            # the same workload line as the B200 arm (N per GPU x world); each step is a bounded
+            # sample of it: one host runs N = args.n particles and the rate is per particle-step
+            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles per GPU, {args.scheme} "
+                                   "resampling at ESS<N/2, 4-dim state, Student-t(10) likelihood, 100-obs model "
+                                   "track", "n_particles": n * world, "scheme": args.scheme},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full PF steps at N={n} after {args.warmup} warm-up steps"},
+                             "sample": f"{args.steps} full PF steps of the C oracle at N={n} on one host "
+                                       f"(after {args.warmup} warm-up steps), OpenMP per-particle loops"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
