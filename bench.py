@@ -383,11 +383,13 @@ def run_e2e(P, s, obs, steps):
     dev_obs = value.obs
     host_obs = torch.from_numpy(np.ascontiguousarray(obs)).pin_memory()
     ncols = len(s._cols)
-    host_row = torch.empty(ncols, dtype=torch.float64).pin_memory()
+    host_rows = torch.empty((steps + 1, ncols), dtype=torch.float64).pin_memory()
     # re-initialize so iteration indices line up with the host observation buffer
     s.initialize(obs)
     torch.cuda.synchronize()
     hist = s._hist
+    stream = torch.cuda.current_stream()
+    done = [None] * (steps + 1)
     t0 = time.perf_counter()
     for k in range(steps):
         t = s.iteration + 1
@@ -396,10 +398,13 @@ def run_e2e(P, s, obs, steps):
         # D2H: the newest COMPLETE history record.  The "pos" monitor of step t is
         # reduced by step t+1's move (fused), so each step reads record t-1; the
         # last record is flushed and read after the loop, inside the timed region.
-        host_row.copy_(s._hist[t - 1], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-    host_row.copy_(s.history_row(s.iteration), non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+        host_rows[k].copy_(s._hist[t - 1], non_blocking=True)
+        done[k] = torch.cuda.Event()
+        done[k].record(stream)
+        if k:  # streaming consumer: step k-1's record is in host memory before step k+1 is issued
+            done[k - 1].synchronize()
+    host_rows[steps].copy_(s.history_row(s.iteration), non_blocking=True)
+    stream.synchronize()
     sec = time.perf_counter() - t0
     del hist
     s.check()
