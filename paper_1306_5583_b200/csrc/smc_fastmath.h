@@ -221,6 +221,35 @@ SMC_HD double exp(double x, const ExpEntry *tab)
     return x < -746.0 ? 0.0 : (x > XMAX ? INFINITY : res);  // exp(-746) rounds to +0
 }
 
+// exp(x) for x <= ~0 without a table (resampling weights W = exp(lw - lse): many
+// independent calls per thread, where table lookups congest shared memory / L1):
+// x = k ln2 + r, |r| <= ln2/2, exp(r) by its degree-13 Taylor polynomial
+// (truncation < 5e-18 relative), coefficients from the constant bank.  Results
+// below 2^-1022 (x < -708) flush to +0 -- for a weight that is exactly what its
+// quantization floor(W 2^63) gives; x > 708 is outside the contract.
+SMC_CONSTANT double kExpPolyK[16] = {
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+    1.0 / 40320.0, 1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+    0x1.71547652b82fep+0, 0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45, 0.0, 0.0};  // 1/ln2, ln2 hi, lo
+
+SMC_HD double exp_weight(double x)
+{
+    const double SH = 0x1.8p52;
+    double kd = fma_(x, kExpPolyK[11], SH);
+    const int64_t k = (int32_t)(uint32_t)bits(kd);
+    kd -= SH;
+    double r = fma_(-kd, kExpPolyK[12], x);
+    r = fma_(-kd, kExpPolyK[13], r);
+    double p = fma_(r, kExpPolyK[0], kExpPolyK[1]);
+#pragma unroll
+    for (int i = 2; i < 11; ++i) p = fma_(r, p, kExpPolyK[i]);
+    p = fma_(r, p, 0.5);
+    p = fma_(r * r, p, r);  // exp(r) - 1
+    const double m = 1.0 + p;
+    const double res = from_bits(bits(m) + ((uint64_t)k << 52));
+    return x < -708.0 ? 0.0 : res;  // NaN passes (the comparison is false)
+}
+
 // sum_k log(v_k) as one log of a running product: the product's exponent is
 // peeled off after every factor (integer ops), so the mantissa m stays in [1, 2).
 // Factors outside [2^-999, 2^1000) (subnormal, zero, huge, non-finite, negative)

@@ -126,9 +126,9 @@ struct WSrc {
     SMC_DEV double weight(double r, const NormLw &nl) const  // the math
     {
         if (w) return r;
-        // libdevice exp: with 8 independent lookups per thread the table exp of
-        // smc_fastmath.h measured slower here (shared / L1 wavefronts)
-        return nl.eq ? nl.weq : exp(nl(r));
+        // table-free polynomial exp (<= 1 ulp; no lookups, no branches, coefficients
+        // from the constant bank): 8 independent calls per thread
+        return nl.eq ? nl.weq : smc_fm::exp_weight(nl(r));
     }
 };
 

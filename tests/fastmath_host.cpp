@@ -9,3 +9,4 @@ extern "C" double fm_logprod(const double *x, long n)
     for (long i = 0; i < n; ++i) lp.add(x[i]);
     return lp.result();
 }
+extern "C" void fm_exp_weight(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp_weight(x[i]); }

@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp):
+    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -139,3 +139,20 @@ def test_logprod_matches_sum_of_logs(fm):
         got = fm("fm_logprod", v)
         assert abs(decimal.Decimal(got) - exact) <= decimal.Decimal(1e-15) * max(1, abs(exact)), (got, exact)
     assert fm("fm_logprod", np.array([0.5, 0.0, 2.0])) == -np.inf
+
+
+def test_exp_weight(fm):
+    """smc_fm::exp_weight (resampling weights, x <= 0): <= 1 ulp against 60-digit exp, flush below -708."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(7)
+    xs = np.concatenate([rng.uniform(-707.9, 0, 3000), rng.uniform(-1, 0, 3000), -rng.random(500) * 1e-6,
+                         [0.0, -0.0, -1.0, -707.5, -1e-300, 1e-16]])
+    got = fm("fm_exp_weight", xs)
+    exact = [decimal.Decimal(float(x)).exp() for x in xs]
+    assert ulp_err(got, exact) <= 1.0
+    a, b = fm("fm_exp_weight", rng.uniform(-700, 0, 1_000_000)), None
+    x = rng.uniform(-700, 0, 1_000_000)
+    a, b = fm("fm_exp_weight", x), np.exp(x)
+    assert np.max(np.abs(a - b) / np.spacing(b)) <= 1.0 and np.mean(a == b) > 0.8
+    edge = fm("fm_exp_weight", np.array([-708.5, -745.0, -np.inf, np.nan]))
+    assert edge[0] == 0.0 and edge[1] == 0.0 and edge[2] == 0.0 and np.isnan(edge[3])
