@@ -44,6 +44,7 @@ class CVState(StateMatrix):
     def __init__(self, size, device="cuda"):
         super().__init__(size, 4, ROW_MAJOR, device)
         self.obs = None  # (T, 2) float64 on the device
+        self.graph_obs = None  # CUDA-graph replay: the step's observation, gathered by a device index
 
     def read_data(self, source):
         if isinstance(source, (str, os.PathLike)):
@@ -55,6 +56,8 @@ class CVState(StateMatrix):
         self.obs = torch.as_tensor(arr, dtype=torch.float64).to(self.device).contiguous()
 
     def obs_ptr(self, t):
+        if self.graph_obs is not None:
+            return ctypes.c_void_p(self.graph_obs.data_ptr())
         if self.obs is None:
             raise RuntimeError("no observations loaded")
         if not 0 <= t < self.obs.shape[0]:
@@ -111,8 +114,12 @@ def _cv_move_kernel(iter_, system):
 
 
 def cv_move():
-    """cv_move as a ParticleKernelOp; post add_log_weight is fused."""
-    return ParticleKernelOp(_cv_move_kernel, name="cv_move")
+    """cv_move as a ParticleKernelOp; post add_log_weight is fused.
+    graph_safe: every launch is stream-ordered device work with fixed addresses, so the
+    sampler may capture and replay it in a CUDA graph (core.Sampler._iterate_graph)."""
+    op = ParticleKernelOp(_cv_move_kernel, name="cv_move")
+    op.graph_safe = True
+    return op
 
 
 def cv_monitor(dim=2):

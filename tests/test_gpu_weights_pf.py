@@ -188,3 +188,27 @@ def test_statematrix_copy_simultaneous():
     c.data.copy_(torch.tensor([[1.0, 2, 3], [4, 5, 6]]))
     c.copy_particles([0, 0, 2])
     assert c.read_state(0).tolist() == [1, 1, 3] and c.read_state(1).tolist() == [4, 4, 6]
+
+
+@pytest.mark.parametrize("scheme,n", [("systematic", 10000), ("stratified", 4096), ("multinomial", 3000)])
+def test_graph_replay_is_bit_identical_to_eager(scheme, n):
+    """core.Sampler's CUDA-graph replay of iterate() runs the eager step's kernels in the
+    same order: history, state, weights and log Z are bit-identical."""
+    from paper_1306_5583_b200 import pf
+    obs, _ = _obs(60)
+    runs = []
+    for graph in (False, "auto"):
+        s = pf.make_sampler(n, scheme, threshold=0.5, seed=11)
+        s.graph = graph
+        s.graph_min_steps = 4
+        s.initialize(obs)
+        s.iterate(20)
+        mid = s.history_array()  # a read between iterate() calls (flushes the fused monitor)
+        s.iterate(17)
+        s.iterate(21)
+        runs.append((mid, s.history_array(), s.system.value.data.cpu().numpy(),
+                     s.system.weight_set.read_log_weight().cpu().numpy(), s.log_zconst))
+    assert getattr(s, "_gbuf", None) is not None and s._gbuf["graphs"], "graph mode did not engage"
+    (m0, h0, x0, w0, z0), (m1, h1, x1, w1, z1) = runs
+    assert np.array_equal(m0, m1) and np.array_equal(h0, h1)
+    assert np.array_equal(x0, x1) and np.array_equal(w0, w1) and z0 == z1
