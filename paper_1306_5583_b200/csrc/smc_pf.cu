@@ -257,20 +257,25 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     if (parents && x_in == x)
         return smc_set_error(SMC_EINVAL, "smc_pf_move: a gathering move needs distinct in/out state buffers");
     cudaStream_t s = (cudaStream_t)stream;
-    const int nb = (int)((n + MB - 1) / MB);
+    // PF_PPT particles per thread only while the grid still gives every SM >= 4 blocks;
+    // below that (e.g. config 1, N = 10^4) one particle per thread spreads the latency
+    const bool many = n >= (int64_t)MB * 148 * 4;
+    const int nb = (int)(many ? (n + MB - 1) / MB : (n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
     double2 *mon = (double2 *)((char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255));
     void *scratch = pf_scratch(ws, nb);
     const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
+#define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                         \
+    k_pf_move<MONV, PPTV><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t, \
+                                            pf_constants(), st, incw_out, parts, MONP)
     if (monitor_prev) {
-        k_pf_move<true, PF_PPT><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
-                                          pf_constants(), st, incw_out, parts, mon);
+        if (many) SMC_PF_MOVE(true, PF_PPT, mon); else SMC_PF_MOVE(true, 1, mon);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev, partial_out);
     } else {
-        k_pf_move<false, PF_PPT><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t,
-                                           pf_constants(), st, incw_out, parts, nullptr);
+        if (many) SMC_PF_MOVE(false, PF_PPT, nullptr); else SMC_PF_MOVE(false, 1, nullptr);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     }
+#undef SMC_PF_MOVE
     return smc_check_launch("smc_pf_move");
 }
