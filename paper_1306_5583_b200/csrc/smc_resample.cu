@@ -81,6 +81,15 @@ struct Layout {
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// multinomial position bins: ~256 particles each, at most 2^17 (the one-block bin scan
+// stays ~40 us at any N; bins get wider, the bin-local searches a few levels deeper)
+constexpr int64_t MN_MAX_BINS = 1 << 17;
+__host__ __device__ inline int64_t mn_bins(int64_t n)
+{
+    const int64_t b = (n + 255) / 256;
+    return b < MN_MAX_BINS ? b : MN_MAX_BINS;
+}
+
 Layout layout(void *ws, int64_t n)
 {
     const int64_t nt = (n + TILE - 1) / TILE;
@@ -101,7 +110,7 @@ Layout layout(void *ws, int64_t n)
     L.tile_z0 = (int32_t *)take(sizeof(int32_t) * (nt + 2));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
-    const int64_t nbins = (n + 255) / 256;  // MN_BIN
+    const int64_t nbins = mn_bins(n);
     L.mn_cnt = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
     L.mn_off = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
     L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
@@ -376,9 +385,9 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
                                                   Layout L)
 {
     if (!L.hdr->active || L.hdr->trivial) return;
-    {  // zero the multinomial bin counters (nbins = n / 256 <= nt * RT)
+    {  // zero the multinomial bin counters (nbins <= n / 256 + 1 <= nt * RT)
         const int64_t b = (int64_t)blockIdx.x * RT + threadIdx.x;
-        if (b <= (n + 255) / 256) L.mn_cnt[b] = 0;
+        if (b <= mn_bins(n)) L.mn_cnt[b] = 0;
     }
     if (L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
@@ -410,7 +419,6 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
 // other evaluation order.
 constexpr int MN_BIN = 256;  // particles per position bin (on average)
 
-SMC_DEV int64_t mn_bins(int64_t n) { return (n + MN_BIN - 1) / MN_BIN; }
 
 struct MnCtx {
     uint64_t M, Tm, c0, lo, hi;  // [lo, hi): this shard's slice of the CDF
@@ -1230,8 +1238,8 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
         k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_scan<<<1, SB, 0, s>>>((n + 255) / 256, n, L);
-        k_mn_starts<<<(unsigned)((n / 256 + 2 + RT - 1) / RT), RT, 0, s>>>(n, L);
+        k_mn_scan<<<1, SB, 0, s>>>(mn_bins(n), n, L);
+        k_mn_starts<<<(unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s>>>(n, L);
         k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
         k_mn_assign<<<gm, RT, 0, s>>>(n, L);
         k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct
@@ -1364,8 +1372,8 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
         const unsigned gm = grid_cap((m_total + RT - 1) / RT);
         k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
         k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_scan<<<1, SB, 0, s>>>((n + 255) / 256, n, L);
-        k_mn_starts<<<(unsigned)((n / 256 + 2 + RT - 1) / RT), RT, 0, s>>>(n, L);
+        k_mn_scan<<<1, SB, 0, s>>>(mn_bins(n), n, L);
+        k_mn_starts<<<(unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s>>>(n, L);
         k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
         k_mn_assign<<<gm, RT, 0, s>>>(n, L);
         k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct

@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--max-log2", type=int, default=30)
     ap.add_argument("--step", type=int, default=2)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--schemes", default=",".join(SCHEMES))
+    ap.add_argument("--kinds", default="uniform,skewed1,skewed3,degenerate")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                        "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6547.8
@@ -59,10 +61,10 @@ def main():
         ws = torch.empty(_abi.lib().smc_resample_workspace_bytes(n), dtype=torch.uint8, device="cuda")
         status = torch.zeros(1, dtype=torch.int32, device="cuda")
         rng = P.RngStreamSet(n + 1, 1306)
-        kinds = ["uniform", "skewed1", "skewed3", "degenerate"]
+        kinds = args.kinds.split(",")
         for kind in kinds:
             w = weights(n, kind, g)
-            for scheme in SCHEMES:
+            for scheme in args.schemes.split(","):
                 sid = int(P.ResampleScheme[scheme.title().replace("_", "")])
 
                 def call():
