@@ -221,6 +221,27 @@ SMC_HD double exp(double x, const ExpEntry *tab)
     return x < -746.0 ? 0.0 : (x > XMAX ? INFINITY : res);  // exp(-746) rounds to +0
 }
 
+// exp(x) for x <= 0 with the table: no overflow side and no subnormal results
+// (below 2^-1022 it flushes to +0) -- for sums whose largest term is exp(0) = 1,
+// where anything that small is far below their rounding (the GMM likelihood).
+SMC_HD double exp_nonpos(double x, const ExpEntry *tab)
+{
+    const double SH = 0x1.8p52;
+    double kd = fma_(x, 0x1.71547652b82fep+7, SH);
+    const int64_t k = (int32_t)(uint32_t)bits(kd);
+    kd -= SH;
+    double r = fma_(-kd, 0x1.62e42fefc0000p-8, x);
+    r = fma_(-kd, -0x1.c610ca86c3899p-44, r);
+    double p = fma_(r, 1.0 / 120, 1.0 / 24);
+    p = fma_(r, p, 1.0 / 6);
+    p = fma_(r, p, 0.5);
+    p = fma_(r * r, p, r);
+    const ExpEntry t = tab[k & 127];
+    const double m = fma_(t.hi, p, t.lo) + t.hi;
+    const double res = from_bits(bits(m) + ((uint64_t)(k >> 7) << 52));
+    return x < -708.0 ? 0.0 : res;  // -inf included
+}
+
 // exp(x) for x <= ~0 without a table (resampling weights W = exp(lw - lse): many
 // independent calls per thread, where table lookups congest shared memory / L1):
 // x = k ln2 + r, |r| <= ln2/2, exp(r) by its degree-13 Taylor polynomial

@@ -41,32 +41,77 @@ SMC_DEV void store_param(double *row, const Param<R> &p)
 }
 
 // update_log_likelihood: -n/2 log 2pi + sum_k log sum_j w_j exp(.5 log l_j - .5 l_j r^2).
-// Evaluated as sum_k log sum_j exp(c_j + b_j r^2), c_j = .5 log l_j + log w_j, b_j = -l_j / 2, with the
-// table exp of smc_fastmath.h (shared-memory table) and the k-sum as one log of a renormalized
-// product (LogProd): per (point, component) ~12 fp64 ops instead of libdevice exp + a log per point.
-// Differs from the oracle's sum of libm logs by rounding only (|d llh| ~ 1e-10 at n = 1000).
+// Evaluated per point k as  x_j = c_j + b_j r_j^2  (c_j = .5 log l_j + log w_j, b_j = -l_j / 2),
+// m = max_j x_j,  log sum_j exp(x_j) = m + log S,  S = sum_j exp(x_j - m) in [1, R]:
+// the max-shifted terms never overflow, anything below 2^-1022 is far under S's rounding
+// (exp_nonpos flushes it), and a point far from every component keeps its exact, finite
+// log density.  sum_k m_k is a plain running sum; prod_k S_k one log of a renormalized
+// running product (S_k >= 1: no checks).  Per (point, component) ~13 fp64 ops.  Agrees
+// with the oracle's sum of libm logs to ~1e-12 relative.  Non-finite parameters take the
+// direct evaluation (log_likelihood_direct) so NaN / inf propagate as in the reference.
+template <int R>
+SMC_DEV double log_likelihood_direct(const Param<R> &p, const double *__restrict__ y, int nd)
+{
+    double ll = -0.5 * (double)nd * 1.8378770664093455;
+    for (int k = 0; k < nd; ++k) {
+        double lli = 0;
+        for (int j = 0; j < R; ++j) {
+            const double resid = y[k] - p.mu[j];
+            lli += p.om[j] * exp(0.5 * log(p.lam[j]) - 0.5 * p.lam[j] * resid * resid);
+        }
+        ll += log(lli);
+    }
+    return ll;
+}
+
 template <int R>
 SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, int nd,
                               const smc_fm::ExpEntry *__restrict__ tab)
 {
     double c[R], b[R];
+    bool finite = true;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         c[j] = 0.5 * log(p.lam[j]) + log(p.om[j]);  // update_log_lambda
         b[j] = -0.5 * p.lam[j];
+        finite = finite && isfinite(p.mu[j]) && isfinite(b[j]) && p.lam[j] > 0 && !isnan(c[j]) && c[j] < INFINITY;
     }
-    smc_fm::LogProd lp;
+    if (!finite) return log_likelihood_direct(p, y, nd);
+    double msum = 0.0, prod = 1.0;
+    int64_t ex = 0;
+    smc_fm::LogProd far;  // points whose largest term is near / below the underflow threshold
     for (int k = 0; k < nd; ++k) {
         const double yk = y[k];
-        double lli = 0;
+        double x[R];
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const double resid = yk - p.mu[j];
-            lli += smc_fm::exp(__fma_rn(b[j], resid * resid, c[j]), tab);
+            x[j] = __fma_rn(b[j], resid * resid, c[j]);
         }
-        lp.add(lli);
+        double m = x[0];
+#pragma unroll
+        for (int j = 1; j < R; ++j) m = fmax(m, x[j]);
+        if (m >= -700.0) {
+            double S = 0.0;
+#pragma unroll
+            for (int j = 0; j < R; ++j) S += smc_fm::exp_nonpos(x[j] - m, tab);
+            msum += m;
+            prod *= S;  // prod in [1, 2) times S in [1, R]: normal; peel the exponent off
+            const uint64_t pb = smc_fm::bits(prod);
+            ex += (int64_t)(pb >> 52) - 1023;
+            prod = smc_fm::from_bits((pb & 0x000fffffffffffffull) | 0x3ff0000000000000ull);
+        } else {
+            // rare (a point far from every component): the reference's own arithmetic, terms
+            // rounded into the subnormal range and a zero sum giving -inf, as libm does
+            double lli = 0.0;
+#pragma unroll
+            for (int j = 0; j < R; ++j) lli += smc_fm::exp(x[j], tab);
+            far.add(lli);
+        }
     }
-    return -0.5 * (double)nd * 1.8378770664093455 + lp.result();
+    const double e = (double)ex;
+    return -0.5 * (double)nd * 1.8378770664093455 + msum +
+           (e * 0x1.62e42fefa3800p-1 + (smc_fm::log_core(prod) + e * 0x1.ef35793c76730p-45)) + far.result();
 }
 
 // update_log_prior: Normal(xi, 1/kappa) per mu, Gamma(nu, chi) per

@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight):
+    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -156,3 +156,15 @@ def test_exp_weight(fm):
     assert np.max(np.abs(a - b) / np.spacing(b)) <= 1.0 and np.mean(a == b) > 0.8
     edge = fm("fm_exp_weight", np.array([-708.5, -745.0, -np.inf, np.nan]))
     assert edge[0] == 0.0 and edge[1] == 0.0 and edge[2] == 0.0 and np.isnan(edge[3])
+
+
+def test_exp_nonpos(fm):
+    """smc_fm::exp_nonpos (GMM likelihood, max-shifted terms): the table exp's accuracy on
+    [-708, 0], +0 below."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(8)
+    xs = np.concatenate([rng.uniform(-707.9, 0, 3000), rng.uniform(-2, 0, 3000), [0.0, -0.0, -1e-300, -707.9]])
+    got = fm("fm_exp_nonpos", xs)
+    assert ulp_err(got, [decimal.Decimal(float(x)).exp() for x in xs]) <= 0.52
+    edge = fm("fm_exp_nonpos", np.array([-708.5, -745.0, -1e6, -np.inf]))
+    assert np.all(edge == 0.0)
