@@ -13,6 +13,9 @@ using namespace smc;
 namespace {
 
 constexpr int GB = 128;  // threads per block (register-heavy per-particle loops)
+#ifndef GMM_MIN_BLOCKS
+#define GMM_MIN_BLOCKS 4
+#endif
 constexpr int RS = 4;    // column stride of mu / lambda / omega in a row (SMC_GMM_MAX_R)
 constexpr int W = SMC_GMM_ROW;
 
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256) k_gmm_reweight(const double *__restrict__
 // recompute caches, accept iff log U < p_new - p_old (+ Jacobian).  Draws: the block's
 // normals in component order, then one uniform.
 template <int BLOCK, int R>
-__global__ void __launch_bounds__(GB) k_gmm_mh(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
+__global__ void __launch_bounds__(GB, GMM_MIN_BLOCKS) k_gmm_mh(double *__restrict__ x, int64_t n, uint64_t sbase, Key key,
                                                uint64_t *__restrict__ ctrs, const double *__restrict__ data, int nd,
                                                Hyper h, double alpha, double sd,
                                                unsigned long long *__restrict__ accepted)
