@@ -29,7 +29,7 @@ from .rng import RngStreamSet
 from .weights import WeightSet
 
 __all__ = ["StateMatrix", "ParticleSystem", "SingleParticleView", "Sampler", "MonitorRecord",
-           "PathAccumulator", "NormalizingConstant", "ROW_MAJOR", "COL_MAJOR"]
+           "PathAccumulator", "NormalizingConstant", "ROW_MAJOR", "COL_MAJOR", "nc_add_log_weight", "sampler_new"]
 
 ROW_MAJOR, COL_MAJOR = "row", "col"
 
@@ -242,6 +242,28 @@ class NormalizingConstant:
     @property
     def log_zconst(self):
         return self.weight_set.log_zconst
+
+
+def nc_add_log_weight(nc, incw, weight_set):
+    """log_zconst += log sum_i W_i exp(incw_i) over the current (pre-update)
+    weights; the weights themselves are not changed.  (The samplers fuse this into their
+    add_log_weight pass -- ``WeightSet.add_log_weight(incw, accumulate_nc=True)``; this
+    standalone form runs the same kernels on a scratch copy and keeps only the increment.)"""
+    ws = weight_set if weight_set is not None else nc.weight_set
+    v = torch.as_tensor(incw, dtype=torch.float64, device=ws.device).contiguous()
+    if v.numel() != ws.size:
+        raise ValueError(f"expected {ws.size} increments, got {v.numel()}")
+    lw, st = ws.lw_raw.clone(), ws.state.clone()
+    buf, nb = ws._ws.get(_abi.lib().smc_weights_workspace_bytes(ws.size))
+    _abi.call("smc_weights_update", 1, _abi.ptr(lw), _abi.ptr(v), ws.size, ctypes.c_void_p(st.data_ptr()), 1, buf,
+              nb, _abi.stream())  # SMC_W_ADD_LOG with the NC increment
+    off = _abi.WSTATE_OFF["log_zconst"]
+    ws.state[off:off + 8].copy_(st[off:off + 8])
+
+
+def sampler_new(N, scheme=None, threshold=0.5, **kw):
+    """SPEC.md:290: ``sampler_new(N, scheme = Stratified, threshold = 0.5)``."""
+    return Sampler(N, ResampleScheme.Stratified if scheme is None else scheme, threshold, **kw)
 
 
 class Sampler:

@@ -20,7 +20,9 @@ import torch
 
 from . import _abi
 
-__all__ = ["RngStreamSet", "RngStream", "DRAW_U01", "DRAW_NORMAL", "DRAW_GAMMA"]
+__all__ = ["RngStreamSet", "RngStream", "DRAW_U01", "DRAW_NORMAL", "DRAW_GAMMA", "philox_block", "u01",
+           "std_normal", "std_gamma", "fill_u01", "fill_std_normal", "fill_std_gamma", "sample_uniform01",
+           "sample_normal", "sample_gamma"]
 
 DRAW_U01, DRAW_NORMAL, DRAW_GAMMA = 0, 1, 2
 
@@ -108,3 +110,74 @@ class RngStream:
         if not (shape > 0.0 and scale > 0.0):
             raise ValueError(f"gamma needs shape > 0 and scale > 0, got shape={shape}, scale={scale}")
         return self._fill(DRAW_GAMMA, n, shape, 0.0, scale)
+
+
+# -- the reference's compiled-kernel primitives (rng.py:59-135) on device counters -------------
+# smckit calls these from numba kernels on a host counter array; here ``ctrs`` is the device
+# counter tensor of an RngStreamSet (int64 holding the uint64 bits) and (k0, k1) the key
+# halves, exactly as ``RngStreamSet.key`` returns them.  Scalar forms synchronize.
+def philox_block(c0, c1, c2, c3, k0, k1):
+    """One Philox4x32-10 block (rng.py:59-72) -> 4 uint32 words."""
+    _abi.require_cuda()
+    import numpy as np
+    ctr = torch.tensor(np.array([c0, c1, c2, c3], np.uint32).view(np.int32), device="cuda")
+    out = torch.zeros(4, dtype=torch.int32, device="cuda")
+    _abi.call("smc_philox_blocks", _abi.ptr(ctr), 1, (int(k0) & 0xFFFFFFFF) | ((int(k1) & 0xFFFFFFFF) << 32),
+              _abi.ptr(out), _abi.stream())
+    return tuple(int(w) for w in out.cpu().numpy().view(np.uint32))
+
+
+def _draw(kind, ctrs, i, k0, k1, shape, out):
+    if not (isinstance(ctrs, torch.Tensor) and ctrs.is_cuda and ctrs.dtype == torch.int64):
+        raise TypeError("ctrs must be the CUDA int64 counter tensor of an RngStreamSet")
+    if not 0 <= int(i) < ctrs.numel():
+        raise IndexError("stream index out of range")
+    seed = (int(k0) & 0xFFFFFFFF) | ((int(k1) & 0xFFFFFFFF) << 32)
+    _abi.call("smc_rng_fill", kind, seed, int(i), _abi.ptr(ctrs), float(shape), 0.0, 1.0, _abi.ptr(out),
+              out.numel(), _abi.stream())
+    return out
+
+
+def u01(ctrs, i, k0, k1):
+    """Uniform in [0, 1) from stream i, advancing ctrs[i] (rng.py:75-82); bit-exact."""
+    return float(_draw(DRAW_U01, ctrs, i, k0, k1, 1.0, torch.empty(1, dtype=torch.float64, device=ctrs.device)))
+
+
+def std_normal(ctrs, i, k0, k1):
+    """Box-Muller normal, two draws (rng.py:85-91)."""
+    return float(_draw(DRAW_NORMAL, ctrs, i, k0, k1, 1.0, torch.empty(1, dtype=torch.float64, device=ctrs.device)))
+
+
+def std_gamma(ctrs, i, k0, k1, shape):
+    """Marsaglia-Tsang gamma(shape, 1) (rng.py:94-117)."""
+    if not shape > 0.0:
+        raise ValueError("gamma needs shape > 0")
+    return float(_draw(DRAW_GAMMA, ctrs, i, k0, k1, shape, torch.empty(1, dtype=torch.float64, device=ctrs.device)))
+
+
+def fill_u01(ctrs, i, k0, k1, out):
+    """out[:] = consecutive uniforms of stream i (rng.py:120-124); out is a CUDA float64 tensor."""
+    return _draw(DRAW_U01, ctrs, i, k0, k1, 1.0, out)
+
+
+def fill_std_normal(ctrs, i, k0, k1, out):
+    return _draw(DRAW_NORMAL, ctrs, i, k0, k1, 1.0, out)
+
+
+def fill_std_gamma(ctrs, i, k0, k1, shape, out):
+    if not shape > 0.0:
+        raise ValueError("gamma needs shape > 0")
+    return _draw(DRAW_GAMMA, ctrs, i, k0, k1, shape, out)
+
+
+# -- SPEC.md:221-223 operation names ---------------------------------------------------------
+def sample_uniform01(stream):
+    return stream.uniform01()
+
+
+def sample_normal(stream, mean, sd):
+    return stream.normal(mean, sd)
+
+
+def sample_gamma(stream, shape, scale):
+    return stream.gamma(shape, scale)

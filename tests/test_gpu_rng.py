@@ -111,3 +111,54 @@ def test_stream_errors():
     with pytest.raises(ValueError):
         ss.stream(0).gamma(0.0)
     assert RngStreamSet(2, (1 << 64) + 5).seed == 5
+
+
+def test_reference_primitives_on_device_counters(golden):
+    """smckit's kernel-callable primitives (rng.py:59-135) by name, on device counters."""
+    from paper_1306_5583_b200 import (RngStreamSet, fill_std_gamma, fill_std_normal, fill_u01, philox_block,
+                                      sample_gamma, sample_normal, sample_uniform01, std_gamma, std_normal, u01)
+    for b in golden["philox"]:
+        assert list(philox_block(*b["ctr"], *b["key"])) == b["out"]
+    for s in golden["streams"]:
+        if s["size"] > 4096:
+            continue
+        ss = RngStreamSet(s["size"], int(s["seed"]))
+        k0, k1 = ss.key
+        for kind, shape, val, ctr in s["ops"]:
+            ref = float.fromhex(val)
+            if kind == "u01":
+                assert u01(ss.counters, s["index"], k0, k1) == ref
+            elif kind == "normal":
+                assert ulps(std_normal(ss.counters, s["index"], k0, k1), ref) <= 8
+            else:
+                assert abs(std_gamma(ss.counters, s["index"], k0, k1, shape) - ref) <= 1e-12 * abs(ref)
+            assert ss.counters_host()[s["index"]] == ctr
+    for f in golden["fills"]:
+        ss = RngStreamSet(4, f["seed"])
+        k0, k1 = ss.key
+        out = torch.empty(f["n"], dtype=torch.float64, device="cuda")
+        ref = np.array([float.fromhex(v) for v in f["values"]])
+        if f["kind"] == "u01":
+            assert np.array_equal(fill_u01(ss.counters, 3, k0, k1, out).cpu().numpy(), ref)
+        elif f["kind"] == "normal":
+            assert ulps(fill_std_normal(ss.counters, 3, k0, k1, out).cpu().numpy(), ref) <= 8
+        else:
+            np.testing.assert_allclose(fill_std_gamma(ss.counters, 3, k0, k1, f["shape"], out).cpu().numpy(), ref,
+                                       rtol=1e-12)
+        assert ss.counters_host()[3] == f["counter"]
+    st = RngStreamSet(2, 5).stream(1)
+    assert 0.0 <= sample_uniform01(st) < 1.0 and isinstance(sample_normal(st, 1.0, 2.0), float)
+    assert sample_gamma(st, 2.0, 3.0) > 0
+
+
+def test_nc_add_log_weight_spec_example():
+    """W = (0.5, 0.5), incw = (ln 2, ln 4) -> increment ln 3; weights unchanged."""
+    from paper_1306_5583_b200 import NormalizingConstant, WeightSet, nc_add_log_weight
+    ws = WeightSet(2)
+    nc = NormalizingConstant(ws)
+    before = ws.read_weight().cpu().numpy()
+    nc_add_log_weight(nc, [math.log(2), math.log(4)], ws)
+    assert abs(nc.log_zconst - math.log(3)) < 1e-15
+    assert np.array_equal(ws.read_weight().cpu().numpy(), before)
+    nc_add_log_weight(nc, [0.7, 0.7], ws)  # all equal c -> increment exactly c
+    assert abs(nc.log_zconst - (math.log(3) + 0.7)) < 1e-15
