@@ -166,3 +166,28 @@ def test_launch_configuration_invariance_sharded_tiles():
     a, _ = gpu_resample("stratified", w, u=u)
     b, _ = gpu_resample("stratified", w, u=u)
     assert np.array_equal(a, b)  # run-to-run determinism
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_unbiasedness_acceptance_1_on_device(scheme):
+    """SPEC.md:671 on the device: W = (.05, .15, .3, .5), N = 4, draws from the sampler's
+    resampling stream (stream N of RngStreamSet(N + 1)), |mean R_i - N W_i| <= 4 SE.
+    20000 replicates (each one smc_resample call; the criterion holds at any count)."""
+    from paper_1306_5583_b200 import RngStreamSet
+    from paper_1306_5583_b200.resample import Resampler
+    W = torch.tensor([0.05, 0.15, 0.3, 0.5], dtype=torch.float64, device="cuda")
+    reps = 20000
+    rng = RngStreamSet(5, 2024)
+    r = Resampler(4)
+    out = torch.empty((reps, 4), dtype=torch.int32, device="cuda")
+    for k in range(reps):
+        r(scheme, weights=W, rng=rng, stream_index=4, counts=out[k])
+    r.check()
+    acc = out.double().cpu().numpy()
+    assert np.all(acc.sum(1) == 4)
+    mean, sd = acc.mean(0), acc.std(0) + 1e-12
+    assert np.all(np.abs(mean - 4 * W.cpu().numpy()) <= 4 * sd / np.sqrt(reps) + 1e-12), mean
+    # and the same stream through the oracle gives the same replicates, bit for bit
+    st = O.Streams(5, 2024)
+    ref = np.array([O.resample_counts(scheme, W.cpu().numpy(), streams=st, stream=4)[0] for _ in range(200)])
+    assert np.array_equal(acc[:200].astype(np.int64), ref)
