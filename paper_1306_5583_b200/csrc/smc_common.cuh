@@ -12,6 +12,30 @@
 
 typedef unsigned __int128 u128;
 
+// Programmatic dependent launch (sm_90+): kernels of the hot chain are launched with
+// the programmatic-stream-serialization attribute, so a kernel's launch and block
+// rasterization overlap the previous kernel's tail; every such kernel starts with
+// SMC_PDL_WAIT (griddepcontrol.wait: all prerequisite grids complete and their memory
+// visible), so stream-order semantics are unchanged.  Without the attribute the wait
+// returns at once.
+#define SMC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
+template <typename... KArgs, typename... Args>
+inline void smc_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 namespace smc {
 
 // ---------------------------------------------------------------------------

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
                                                 const double *__restrict__ obs,
                                                 PfConst k, smc_wstate *st, LsePartial *__restrict__ parts)
 {
+    SMC_PDL_WAIT();
     const int64_t i = (int64_t)blockIdx.x * PB + threadIdx.x;
     double v = -INFINITY;
     if (i < n) {
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
+    SMC_PDL_WAIT();
     __shared__ double s_v[PPT][PB];
     const int64_t base = (int64_t)blockIdx.x * (PB * PPT) + threadIdx.x;
     double h0 = 0.0, h1 = 0.0;
@@ -239,7 +241,7 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t stream
     const int nb = (int)((n + PB - 1) / PB);
     LsePartial *parts = (LsePartial *)ws;
     void *scratch = pf_scratch(ws, nb);
-    k_pf_init<<<nb, PB, 0, s>>>(x, lw_raw, n, stream_base, make_key_sched(seed), ctrs, obs_t,
+    smc_launch(k_pf_init, nb, PB, 0, s, x, lw_raw, n, stream_base, make_key_sched(seed), ctrs, obs_t,
                                 pf_constants(), st, parts);
     smc_launch_lse_finalize(parts, nb, st, n, SMC_W_SET_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     return smc_check_launch("smc_pf_init");
@@ -267,7 +269,7 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
 #define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                         \
-    k_pf_move<MONV, PPTV><<<nb, PB, 0, s>>>(x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t, \
+    smc_launch(k_pf_move<MONV, PPTV>, nb, PB, 0, s, x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t, \
                                             pf_constants(), st, incw_out, parts, MONP)
     if (monitor_prev) {
         if (many) SMC_PF_MOVE(true, PF_PPT, mon); else SMC_PF_MOVE(true, 1, mon);

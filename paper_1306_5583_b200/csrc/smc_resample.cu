@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
                                                  const double *__restrict__ u, int64_t n_u, const int32_t *gate,
                                                  int32_t *status, Layout L)
 {
+    SMC_PDL_WAIT();
     if (gate && *gate == 0) return;
     const int64_t base = (int64_t)blockIdx.x * TILE;
     const bool residual = is_residual(scheme);
@@ -232,6 +233,7 @@ constexpr int SB = 1024;
 // A shard's totals {T lo, T hi, sum f, T'} for the allgather of a G-GPU resample.
 __global__ void __launch_bounds__(SB) k_rs_local_totals(int64_t nt, const int32_t *gate, Layout L, uint64_t *out)
 {
+    SMC_PDL_WAIT();
     __shared__ u128 s_q[SB / 32];
     __shared__ uint64_t s_qr[SB / 32];
     __shared__ int64_t s_f[SB / 32];
@@ -272,6 +274,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
                                                 int64_t n_u, const int32_t *gate, int32_t *status, Layout L,
                                                 const uint64_t *totals_all, int G, int rank, int64_t n_total)
 {
+    SMC_PDL_WAIT();
     __shared__ uint64_t s_off;
     __shared__ uint64_t sm64[SB / 32 + 1];
     __shared__ u128 s_q[SB / 32];
@@ -384,6 +387,7 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
 __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                   Layout L)
 {
+    SMC_PDL_WAIT();
     if (!L.hdr->active || L.hdr->trivial) return;
     {  // zero the multinomial bin counters (nbins <= n / 256 + 1 <= nt * RT)
         const int64_t b = (int64_t)blockIdx.x * RT + threadIdx.x;
@@ -477,6 +481,7 @@ SMC_DEV uint32_t agg_inc(uint32_t *a, uint32_t key, bool active)
 
 __global__ void k_mn_count(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     const MnCtx c = mn_ctx(L, n);
@@ -492,6 +497,7 @@ __global__ void k_mn_count(int64_t n, Key key, uint64_t stream, const double *__
 // one block: exclusive bucket offsets; fill pointers back to zero
 __global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     __shared__ uint64_t sm64[SB / 32 + 1];
@@ -531,6 +537,7 @@ __global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layo
 // first particle of every bin: mn_start[b] = first i with Q_i > lo + b W (b = 0..nb)
 __global__ void k_mn_starts(int64_t n, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial || h->mn_direct) return;
     const MnCtx c = mn_ctx(L, n);
@@ -548,6 +555,7 @@ __global__ void k_mn_starts(int64_t n, Layout L)
 
 __global__ void k_mn_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     if (h->mn_direct) return;  // more positions than bucket capacity (a shard): k_rs_multinomial
@@ -567,6 +575,7 @@ __global__ void k_mn_scatter(int64_t n, Key key, uint64_t stream, const double *
 // searched only between its bin's first particles
 __global__ void k_mn_assign(int64_t n, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     if (h->mn_direct) return;
@@ -595,6 +604,7 @@ __global__ void k_mn_assign(int64_t n, Layout L)
 // binary search over this shard's whole Q.
 __global__ void k_rs_multinomial(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial || !h->mn_direct) return;
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0;
@@ -698,6 +708,7 @@ SMC_DEV void tile_aggregate(const int32_t (&c)[RI], int64_t b, const Layout &L)
 // slot tile's first zero rank, and the sum(counts) == N check.
 __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32_t *status, Layout L)
 {
+    SMC_PDL_WAIT();
     RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     __shared__ uint64_t s_zp[SB / 32 + 1], s_s[SB / 32 + 1];
@@ -758,6 +769,7 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
 __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin, int64_t n, int32_t *status,
                                                  int check, Layout L)
 {
+    SMC_PDL_WAIT();
     RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
     __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI>()];
@@ -823,6 +835,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
 // Aggregates of caller-provided counts (replication_to_parents without pass B1).
 __global__ void __launch_bounds__(RT) k_rs_aggs(const int32_t *__restrict__ cin, int64_t n, Layout L)
 {
+    SMC_PDL_WAIT();
     if (!L.hdr->active || L.hdr->trivial) return;
     __shared__ int32_t s_c[tile_smem_elems<int32_t, RT, RI>()];
     int32_t c[RI];
@@ -838,6 +851,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
                                                   Key key, uint64_t stream, const double *__restrict__ u,
                                                   int32_t *__restrict__ counts, int ranks, Layout L)
 {
+    SMC_PDL_WAIT();
     RsHeader *h = L.hdr;
     if (!h->active) return;
     __shared__ uint64_t sm[RT / 32 + 1];
@@ -981,6 +995,7 @@ template <bool SHARD>
 __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
                                                   int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active) return;
     if (h->trivial) {
@@ -1100,6 +1115,7 @@ struct PackRanges {
 __global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, int64_t n, PackRanges pr,
                           char *__restrict__ out, Layout L)
 {
+    SMC_PDL_WAIT();
     const int64_t Sl = L.hdr->S_total, P = L.hdr->P_total;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pr.total; k += (int64_t)gridDim.x * blockDim.x) {
         int r = 0;
@@ -1133,6 +1149,7 @@ template <int RB>
 __global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
                                                 int64_t n, Layout L)
 {
+    SMC_PDL_WAIT();
     if (!L.hdr->active || L.hdr->trivial) return;
     const int64_t j = (int64_t)blockIdx.x * CB + threadIdx.x;
     if (j >= n) return;
@@ -1149,6 +1166,7 @@ __global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ pare
 
 __global__ void k_rs_export_zsp(Layout L, uint32_t *out)
 {
+    SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     const bool on = h->active && !h->trivial;
     out[0] = on ? h->Z_total : 0;
@@ -1159,6 +1177,7 @@ __global__ void k_rs_export_zsp(Layout L, uint32_t *out)
 
 __global__ void k_rs_reset(Layout L)
 {
+    SMC_PDL_WAIT();
     RsHeader *h = L.hdr;
     h->active = 1;
     h->trivial = 0;
@@ -1168,6 +1187,7 @@ __global__ void k_rs_reset(Layout L)
 __global__ void __launch_bounds__(RT) k_copy_inplace(char *rows, int64_t row_bytes, const int32_t *__restrict__ parents,
                                                      int64_t n, const int32_t *gate)
 {
+    SMC_PDL_WAIT();
     if (gate && *gate == 0) return;
     for (int64_t j = (int64_t)blockIdx.x * RT + threadIdx.x; j < n; j += (int64_t)gridDim.x * RT) {
         const int32_t p = parents[j];
@@ -1178,6 +1198,7 @@ __global__ void __launch_bounds__(RT) k_copy_inplace(char *rows, int64_t row_byt
 __global__ void __launch_bounds__(RT) k_gather(char *__restrict__ dst, const char *__restrict__ src, int64_t row_bytes,
                                                const int32_t *__restrict__ parents, int64_t n)
 {
+    SMC_PDL_WAIT();
     const int64_t words = row_bytes / 8;
     const int64_t total = n * words;
     for (int64_t e = (int64_t)blockIdx.x * RT + threadIdx.x; e < total; e += (int64_t)gridDim.x * RT) {
@@ -1231,31 +1252,31 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     WSrc src{w, lw_raw, st, n};
     const double mo = (double)m_out;
 
-    k_rs_tiles<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, u, n_u, gate, status, L);
-    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
+    smc_launch(k_rs_tiles, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    smc_launch(k_rs_scan, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
                                nullptr, 1, 0, n);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
-        k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
-        k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_scan<<<1, SB, 0, s>>>(mn_bins(n), n, L);
-        k_mn_starts<<<(unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s>>>(n, L);
-        k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_assign<<<gm, RT, 0, s>>>(n, L);
-        k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct
+        smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
+        smc_launch(k_mn_count, gm, RT, 0, s, n, key, stream_index, u, L);
+        smc_launch(k_mn_scan, 1, SB, 0, s, mn_bins(n), n, L);
+        smc_launch(k_mn_starts, (unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s, n, L);
+        smc_launch(k_mn_scatter, gm, RT, 0, s, n, key, stream_index, u, L);
+        smc_launch(k_mn_assign, gm, RT, 0, s, n, L);
+        smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr,
+    smc_launch(k_rs_counts, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr,
                                             L);
     if (parents) {
-        k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
-        k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, status, 0, L);
-        k_rs_assign<false><<<(unsigned)nt, RT, 0, s>>>(cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+        smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 1, status, L);
+        smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
+        smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
         if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
             if (row_bytes == 32)
-                k_rs_copy<32><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, 32, n, L);
+                smc_launch(k_rs_copy<32>, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, 32, n, L);
             else
-                k_rs_copy<0><<<(unsigned)((n + CB - 1) / CB), CB, 0, s>>>(parents, (char *)rows, row_bytes, n, L);
+                smc_launch(k_rs_copy<0>, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, row_bytes, n, L);
         }
     }
     return smc_check_launch("smc_resample");
@@ -1272,11 +1293,11 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     if ((uintptr_t)counts & 15) return smc_set_error(SMC_EINVAL, "smc_replication_to_parents: counts alignment");
-    k_rs_reset<<<1, 1, 0, s>>>(L);
-    k_rs_aggs<<<(unsigned)nt, RT, 0, s>>>(counts, n, L);
-    k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 1, status, L);
-    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(counts, n, status, 1, L);
-    k_rs_assign<false><<<(unsigned)nt, RT, 0, s>>>(counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+    smc_launch(k_rs_reset, 1, 1, 0, s, L);
+    smc_launch(k_rs_aggs, (unsigned)nt, RT, 0, s, counts, n, L);
+    smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 1, status, L);
+    smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, counts, n, status, 1, L);
+    smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
@@ -1286,7 +1307,7 @@ extern "C" int smc_copy_rows_inplace(void *rows, int64_t row_bytes, const int32_
     if (!rows || !parents || n < 1 || row_bytes < 8 || (row_bytes & 7) ||
         (row_bytes == 32 && ((uintptr_t)rows & 31)))
         return smc_set_error(SMC_EINVAL, "smc_copy_rows_inplace: bad args");
-    k_copy_inplace<<<grid_cap((n + RT - 1) / RT), RT, 0, (cudaStream_t)stream>>>((char *)rows, row_bytes, parents,
+    smc_launch(k_copy_inplace, grid_cap((n + RT - 1) / RT), RT, 0, (cudaStream_t)stream, (char *)rows, row_bytes, parents,
                                                                                  n, gate);
     return smc_check_launch("smc_copy_rows_inplace");
 }
@@ -1296,7 +1317,7 @@ extern "C" int smc_gather_rows(void *dst, const void *src, int64_t row_bytes, co
 {
     if (!dst || !src || dst == src || !parents || n < 1 || row_bytes < 8 || (row_bytes & 7))
         return smc_set_error(SMC_EINVAL, "smc_gather_rows: bad args");
-    k_gather<<<grid_cap((n * (row_bytes / 8) + RT - 1) / RT), RT, 0, (cudaStream_t)stream>>>(
+    smc_launch(k_gather, grid_cap((n * (row_bytes / 8) + RT - 1) / RT), RT, 0, (cudaStream_t)stream, 
         (char *)dst, (const char *)src, row_bytes, parents, n);
     return smc_check_launch("smc_gather_rows");
 }
@@ -1342,9 +1363,9 @@ extern "C" int smc_resample_shard_totals(int scheme, const double *w, const doub
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     WSrc src{w, lw_raw, st, n_total};  // equal weights are 1 / N_total
-    k_rs_tiles<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, (double)m_total, shard_rscale(n_total), u, n_u, gate,
+    smc_launch(k_rs_tiles, (unsigned)nt, RT, 0, s, scheme, src, n, (double)m_total, shard_rscale(n_total), u, n_u, gate,
                                            status, L);
-    k_rs_local_totals<<<1, SB, 0, s>>>(nt, gate, L, totals_out);
+    smc_launch(k_rs_local_totals, 1, SB, 0, s, nt, gate, L, totals_out);
     return smc_check_launch("smc_resample_shard_totals");
 }
 
@@ -1366,23 +1387,23 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     WSrc src{w, lw_raw, st, n_total};
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
     const double rscale = shard_rscale(n_total), mo = (double)m_total;
-    k_rs_scan<<<1, SB, 0, s>>>(scheme, n, nt, (uint64_t)m_total, key, stream_index, ctr, u, n_u, gate, status, L,
+    smc_launch(k_rs_scan, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_total, key, stream_index, ctr, u, n_u, gate, status, L,
                                totals_all, G, rank, n_total);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_total + RT - 1) / RT);
-        k_rs_prefix<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, L);
-        k_mn_count<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_scan<<<1, SB, 0, s>>>(mn_bins(n), n, L);
-        k_mn_starts<<<(unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s>>>(n, L);
-        k_mn_scatter<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);
-        k_mn_assign<<<gm, RT, 0, s>>>(n, L);
-        k_rs_multinomial<<<gm, RT, 0, s>>>(n, key, stream_index, u, L);  // exits unless mn_direct
+        smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
+        smc_launch(k_mn_count, gm, RT, 0, s, n, key, stream_index, u, L);
+        smc_launch(k_mn_scan, 1, SB, 0, s, mn_bins(n), n, L);
+        smc_launch(k_mn_starts, (unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s, n, L);
+        smc_launch(k_mn_scatter, gm, RT, 0, s, n, key, stream_index, u, L);
+        smc_launch(k_mn_assign, gm, RT, 0, s, n, L);
+        smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
-    k_rs_counts<<<(unsigned)nt, RT, 0, s>>>(scheme, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
-    k_rs_zsp_scan<<<1, SB, 0, s>>>(nt, 0, status, L);
-    k_rs_ranks<<<(unsigned)nt, RT, 0, s>>>(cout, n, status, 0, L);
-    k_rs_export_zsp<<<1, 1, 0, s>>>(L, zsp_out);
+    smc_launch(k_rs_counts, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
+    smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 0, status, L);
+    smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
+    smc_launch(k_rs_export_zsp, 1, 1, 0, s, L, zsp_out);
     return smc_check_launch("smc_resample_shard_counts");
 }
 
@@ -1405,7 +1426,7 @@ extern "C" int smc_resample_shard_pack(const void *rows, int64_t row_bytes, int6
     if (!off) return SMC_OK;
     Layout L = layout(ws, n);
     const int bs = 256;
-    k_rs_pack<<<grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>((const char *)rows, row_bytes, n, pr,
+    smc_launch(k_rs_pack, grid_cap((off + bs - 1) / bs), bs, 0, (cudaStream_t)stream, (const char *)rows, row_bytes, n, pr,
                                                                               (char *)sendbuf, L);
     return smc_check_launch("smc_resample_shard_pack");
 }
@@ -1420,7 +1441,7 @@ extern "C" int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     const int32_t *cin = counts ? counts : L.cnt;
-    k_rs_assign<true><<<(unsigned)nt, RT, 0, (cudaStream_t)stream>>>(
+    smc_launch(k_rs_assign<true>, (unsigned)nt, RT, 0, (cudaStream_t)stream, 
         cin, n, parents, ShardC{zoff, soff, s_self, (const char *)recv, (char *)rows, row_bytes}, L);
     return smc_check_launch("smc_resample_shard_assign");
 }

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restric
                                                       const double *__restrict__ values, int64_t n,
                                                       smc_wstate *st, LsePartial *__restrict__ parts)
 {
+    SMC_PDL_WAIT();
     const int64_t i = (int64_t)blockIdx.x * WB + threadIdx.x;
     double v = -INFINITY;
     if (i < n) {
@@ -100,6 +101,7 @@ SMC_DEV void lse_slice(const LsePartial *__restrict__ parts, const double2 *__re
 __global__ void __launch_bounds__(FB) k_lse_level1(const LsePartial *__restrict__ parts, int nparts,
                                                     const double2 *__restrict__ mon, LsePartial *l2, double2 *l2mon)
 {
+    SMC_PDL_WAIT();
     const int per = (nparts + FG - 1) / FG;
     const int b0 = min(nparts, (int)blockIdx.x * per), b1 = min(nparts, b0 + per);
     lse_slice(parts, mon, b0, b1, l2 + blockIdx.x, l2mon + blockIdx.x);
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restric
                                                       int has_mon, smc_wstate *st, int64_t n, int mode,
                                                       int accumulate_nc, double *mon_out, double *partial_out)
 {
+    SMC_PDL_WAIT();
     __shared__ LsePartial s_t;
     __shared__ double2 s_h;
     lse_slice(l2, has_mon ? l2mon : nullptr, 0, FG, &s_t, &s_h);
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restric
 __global__ void k_lse_combine(const double *__restrict__ parts, int G, smc_wstate *st, int64_t n_total, int mode,
                               int accumulate_nc, double *mon_out)
 {
+    SMC_PDL_WAIT();
     double M = -INFINITY;
     for (int g = 0; g < G; ++g) M = fmax(M, parts[g * SMC_PARTIAL_STRIDE]);
     LsePartial t{M, 0.0, 0.0};
@@ -181,6 +185,7 @@ __global__ void k_lse_combine(const double *__restrict__ parts, int G, smc_wstat
 
 __global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
 {
+    SMC_PDL_WAIT();
     if (gate && *gate == 0) return;
     st->equal = 1;
     st->lse = log((double)n);  // consistent with lw_raw == 0 everywhere
@@ -194,6 +199,7 @@ __global__ void k_set_equal(smc_wstate *st, int64_t n, const int32_t *gate)
 __global__ void k_weights_read(int what, const double *__restrict__ lw_raw, const smc_wstate *st, int64_t n,
                                double *__restrict__ out)
 {
+    SMC_PDL_WAIT();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const NormLw nl = norm_of(st);
@@ -205,6 +211,7 @@ __global__ void k_weights_read(int what, const double *__restrict__ lw_raw, cons
 // SPEC.md:266 / SURVEY R8: threshold >= 1 always, <= 0 never, else ess/N < threshold.
 __global__ void k_ess_decide(smc_wstate *st, double threshold, double *hist_row)
 {
+    SMC_PDL_WAIT();
     const double eon = st->ess_over_n;
     int r = threshold >= 1.0 ? 1 : (threshold <= 0.0 ? 0 : (eon < threshold ? 1 : 0));
     if (st->status) r = 0;  // never resample on a failed normalization
@@ -220,6 +227,7 @@ __global__ void __launch_bounds__(RB) k_wsum_pass(const double *__restrict__ val
                                                    const double *__restrict__ lw_raw, const smc_wstate *st,
                                                    int64_t n, double *__restrict__ parts, int mtot)
 {
+    SMC_PDL_WAIT();
     __shared__ double sm[RB / 32][RMAX];
     double acc[RMAX];
 #pragma unroll
@@ -248,6 +256,7 @@ __global__ void __launch_bounds__(RB) k_wsum_pass(const double *__restrict__ val
 
 __global__ void k_wsum_final(const double *__restrict__ parts, int nb, int m, double *__restrict__ out)
 {
+    SMC_PDL_WAIT();
     // one warp per column, fixed order
     const int j = blockIdx.x;
     double v = 0.0;
@@ -272,8 +281,8 @@ void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st
 {
     LsePartial *l2 = (LsePartial *)scratch;
     double2 *l2mon = (double2 *)(l2 + FG);
-    k_lse_level1<<<FG, FB, 0, s>>>(parts, nparts, mon_parts, l2, l2mon);
-    k_lse_finalize<<<1, FB, 0, s>>>(l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out,
+    smc_launch(k_lse_level1, FG, FB, 0, s, parts, nparts, mon_parts, l2, l2mon);
+    smc_launch(k_lse_finalize, 1, FB, 0, s, l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out,
                                     partial_out);
 }
 
@@ -282,7 +291,7 @@ extern "C" int smc_weights_combine(const double *partials, int G, smc_wstate *st
 {
     if (!partials || G < 1 || !st || n_total < 1)
         return smc_set_error(SMC_EINVAL, "smc_weights_combine: bad args");
-    k_lse_combine<<<1, 1, 0, (cudaStream_t)stream>>>(partials, G, st, n_total, mode, accumulate_nc, monitor_out);
+    smc_launch(k_lse_combine, 1, 1, 0, (cudaStream_t)stream, partials, G, st, n_total, mode, accumulate_nc, monitor_out);
     return smc_check_launch("smc_weights_combine");
 }
 
@@ -298,7 +307,7 @@ extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values
     if (n < 1 || n >= (int64_t)1 << 31 || !st || mode < 0 || mode > 4)
         return smc_set_error(SMC_EINVAL, "smc_weights_update: bad args (mode=%d n=%lld)", mode, (long long)n);
     if (mode == SMC_W_EQUAL) {
-        k_set_equal<<<1, 1, 0, s>>>(st, n, nullptr);
+        smc_launch(k_set_equal, 1, 1, 0, s, st, n, nullptr);
         return smc_check_launch("smc_weights_update(equal)");
     }
     if (!lw_raw || !values) return smc_set_error(SMC_EINVAL, "smc_weights_update: null vector");
@@ -306,7 +315,7 @@ extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values
         return smc_set_error(SMC_EWORKSPACE, "smc_weights_update: workspace too small");
     const int nb = (int)((n + WB - 1) / WB);
     LsePartial *parts = (LsePartial *)ws;
-    k_weights_pass<<<nb, WB, 0, s>>>(mode, lw_raw, values, n, st, parts);
+    smc_launch(k_weights_pass, nb, WB, 0, s, mode, lw_raw, values, n, st, parts);
     void *scratch = (char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255);
     smc_launch_lse_finalize(parts, nb, st, n, mode, accumulate_nc, s, scratch);
     return smc_check_launch("smc_weights_update");
@@ -315,7 +324,7 @@ extern "C" int smc_weights_update(int mode, double *lw_raw, const double *values
 extern "C" int smc_weights_set_equal(smc_wstate *st, int64_t n, const int32_t *gate, void *stream)
 {
     if (!st || n < 1) return smc_set_error(SMC_EINVAL, "smc_weights_set_equal: bad args");
-    k_set_equal<<<1, 1, 0, (cudaStream_t)stream>>>(st, n, gate);
+    smc_launch(k_set_equal, 1, 1, 0, (cudaStream_t)stream, st, n, gate);
     return smc_check_launch("smc_weights_set_equal");
 }
 
@@ -324,14 +333,14 @@ extern "C" int smc_weights_read(int what, const double *lw_raw, const smc_wstate
 {
     if (n < 1 || !st || !out || !lw_raw || (what != 0 && what != 1))
         return smc_set_error(SMC_EINVAL, "smc_weights_read: bad args");
-    k_weights_read<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(what, lw_raw, st, n, out);
+    smc_launch(k_weights_read, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, what, lw_raw, st, n, out);
     return smc_check_launch("smc_weights_read");
 }
 
 extern "C" int smc_ess_decide(smc_wstate *st, int64_t n, double threshold, double *hist_row, void *stream)
 {
     if (!st || n < 1) return smc_set_error(SMC_EINVAL, "smc_ess_decide: bad args");
-    k_ess_decide<<<1, 1, 0, (cudaStream_t)stream>>>(st, threshold, hist_row);
+    smc_launch(k_ess_decide, 1, 1, 0, (cudaStream_t)stream, st, threshold, hist_row);
     return smc_check_launch("smc_ess_decide");
 }
 
@@ -353,8 +362,8 @@ extern "C" int smc_weighted_reduce(const double *vals, int64_t ld, int64_t m, co
     double *parts = (double *)ws;
     for (int m0 = 0; m0 < m; m0 += RMAX) {
         const int mc = (int)((m - m0) < RMAX ? (m - m0) : RMAX);
-        k_wsum_pass<<<nb, RB, 0, s>>>(vals, ld, m0, mc, lw_raw, st, n, parts, (int)m);
+        smc_launch(k_wsum_pass, nb, RB, 0, s, vals, ld, m0, mc, lw_raw, st, n, parts, (int)m);
     }
-    k_wsum_final<<<(unsigned)m, 32, 0, s>>>(parts, nb, (int)m, out);
+    smc_launch(k_wsum_final, (unsigned)m, 32, 0, s, parts, nb, (int)m, out);
     return smc_check_launch("smc_weighted_reduce");
 }
