@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libsmcb200.so")
+LIB = os.environ.get("SMC_LIB_PATH") or os.path.join(HERE, "libsmcb200.so")  # override: A/B experiments
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
