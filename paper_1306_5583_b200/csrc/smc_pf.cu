@@ -19,6 +19,10 @@ constexpr int PB = 256;
 #ifndef PF_PPT
 #define PF_PPT 4  // particles per thread in the move kernel
 #endif
+#ifndef PF_UNROLL
+#define PF_UNROLL 1  // particles of a thread interleaved by the compiler (ILP vs registers)
+#endif
+constexpr int kPfUnroll = PF_UNROLL;
 constexpr int MB = PB * PF_PPT;  // particles per move block
 
 struct PfConst {
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         if (gathered) src_nx = __ldg(parents + base);
         if (nl.needs_raw()) lw_nx = lw_raw[base];
     }
-#pragma unroll 1
+#pragma unroll kPfUnroll
     for (int q = 0; q < PPT; ++q) {
         const int64_t i = base + (int64_t)q * PB;
         double v = -INFINITY;
