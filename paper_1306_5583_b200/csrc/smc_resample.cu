@@ -156,7 +156,8 @@ struct Quant {
 SMC_DEV Quant quantize(double W, bool residual, double m_out, double rscale, bool &bad)
 {
     Quant r{0, 0, 0};
-    if (!(W >= 0.0 && W <= 1.0)) { bad = true; return r; }
+    const uint64_t wb = smc_fm::bits(W);  // W in [0, 1]: bits <= bits(1.0) (or -0); NaN / < 0 / > 1 are not
+    if (wb > 0x3FF0000000000000ull && wb != 0x8000000000000000ull) { bad = true; return r; }
     r.q = (uint64_t)(W * 9223372036854775808.0);
     if (residual) {
         const double x = m_out * W;  // fl(M W_i), exactly rounded (no FMA: --fmad=false)
@@ -168,6 +169,7 @@ SMC_DEV Quant quantize(double W, bool residual, double m_out, double rscale, boo
 }
 
 // ------------------------------------------------------------------ pass A --
+template <bool RES, bool MULTI>  // residual family / multinomial histogram: resolved at compile time
 __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                  const double *__restrict__ u, int64_t n_u, const int32_t *gate,
                                                  int32_t *status, Layout L)
@@ -175,13 +177,13 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
     SMC_PDL_WAIT();
     if (gate && *gate == 0) return;
     const int64_t base = (int64_t)blockIdx.x * TILE;
-    const bool residual = is_residual(scheme);
     const NormLw nl = src.norm();
+    const bool full = base + TILE <= n;  // no per-element bounds checks on full tiles
     double r[RI];
 #pragma unroll
     for (int j = 0; j < RI; ++j) {  // striped: each warp load is 256 contiguous bytes; all issued up front
         const int64_t i = base + j * RT + threadIdx.x;
-        r[j] = i < n ? src.raw(i, nl) : 0.0;
+        r[j] = (full || i < n) ? src.raw(i, nl) : 0.0;
     }
     u128 sq = 0;
     uint64_t sqr = 0;
@@ -190,13 +192,15 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         const int64_t i = base + j * RT + threadIdx.x;
-        if (i < n) {
-            const Quant qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
+        if (full || i < n) {
+            const Quant qq = quantize(src.weight(r[j], nl), RES, m_out, rscale, bad);
             sq += qq.q;
-            sqr += qq.qr;
-            sf += qq.f;
-            L.qfull[i] = residual ? qq.qr : qq.q;  // the searched quantity, for passes M and B1
-            if (is_multinomial(scheme)) L.cnt[i] = 0;
+            if (RES) {
+                sqr += qq.qr;
+                sf += qq.f;
+            }
+            L.qfull[i] = RES ? qq.qr : qq.q;  // the searched quantity, for passes M and B1
+            if (MULTI) L.cnt[i] = 0;
         }
     }
     bool badu = false;  // explicit uniforms must lie in [0, 1)
@@ -225,6 +229,17 @@ __global__ void __launch_bounds__(RT) k_rs_tiles(int scheme, WSrc src, int64_t n
         L.tile_qr[blockIdx.x] = b;
         L.tile_f[blockIdx.x] = c;
     }
+}
+
+inline void launch_tiles(int scheme, unsigned nt, cudaStream_t s, WSrc src, int64_t n, double mo, double rscale,
+                         const double *u, int64_t n_u, const int32_t *gate, int32_t *status, Layout L)
+{
+    const bool res = scheme == SMC_RESIDUAL || scheme == SMC_RESIDUAL_STRATIFIED || scheme == SMC_RESIDUAL_SYSTEMATIC;
+    const bool multi = scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL;
+    if (res && multi) smc_launch(k_rs_tiles<true, true>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    else if (res) smc_launch(k_rs_tiles<true, false>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    else if (multi) smc_launch(k_rs_tiles<false, true>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    else smc_launch(k_rs_tiles<false, false>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
 }
 
 // ------------------------------------------------------------------ pass S --
@@ -1252,7 +1267,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     WSrc src{w, lw_raw, st, n};
     const double mo = (double)m_out;
 
-    smc_launch(k_rs_tiles, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+    launch_tiles(scheme, (unsigned)nt, s, src, n, mo, rscale, u, n_u, gate, status, L);
     smc_launch(k_rs_scan, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
                                nullptr, 1, 0, n);
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
@@ -1363,7 +1378,7 @@ extern "C" int smc_resample_shard_totals(int scheme, const double *w, const doub
     const int64_t nt = (n + TILE - 1) / TILE;
     Layout L = layout(ws, n);
     WSrc src{w, lw_raw, st, n_total};  // equal weights are 1 / N_total
-    smc_launch(k_rs_tiles, (unsigned)nt, RT, 0, s, scheme, src, n, (double)m_total, shard_rscale(n_total), u, n_u, gate,
+    launch_tiles(scheme, (unsigned)nt, s, src, n, (double)m_total, shard_rscale(n_total), u, n_u, gate,
                                            status, L);
     smc_launch(k_rs_local_totals, 1, SB, 0, s, nt, gate, L, totals_out);
     return smc_check_launch("smc_resample_shard_totals");
