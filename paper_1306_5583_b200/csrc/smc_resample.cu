@@ -647,15 +647,17 @@ struct StratCtx {
     double us_sys;  // m_sys 2^-53 (systematic)
 };
 
+template <bool SYS>
 SMC_DEV uint64_t m_of(const StratCtx &c, uint64_t s)
 {
-    if (c.systematic) return c.m_sys;
+    if (SYS) return c.m_sys;
     if (c.u) return (uint64_t)(c.u[s] * TWO53);
     return draw53(c.c0 + s, c.stream, c.key);
 }
 
 // Exact F(X) = #{k < M : P_k < X},  P_k = floor((k 2^53 + m_k) Tm / (M 2^53)):
 // k < s := floor(X M / Tm) all qualify, k > s none; k = s iff m_s Tm < (X M - s Tm) 2^53.
+template <bool SYS>
 SMC_DEV uint64_t F_exact(const StratCtx &c, uint64_t X)
 {
     if (X >= c.Tm) return c.M;
@@ -665,13 +667,14 @@ SMC_DEV uint64_t F_exact(const StratCtx &c, uint64_t X)
     while ((u128)s * c.Tm > XM) --s;
     while ((u128)(s + 1) * c.Tm <= XM) ++s;
     const u128 rem = XM - (u128)s * c.Tm;
-    const uint64_t m = m_of(c, s);
+    const uint64_t m = m_of<SYS>(c, s);
     return s + (((u128)m * c.Tm < (rem << 53)) ? 1 : 0);
 }
 
 // Same value in ~10 instructions: z = X M / Tm in fp64 (|error| <= 3.4e-16 M);
 // F = floor(z) + [u_s < frac(z)].  Whenever frac(z) or frac(z) - u_s lies
 // inside the guard band the exact path decides, so the result is bit-identical.
+template <bool SYS>
 SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
 {
     if (X >= c.Tm) return c.M;
@@ -679,10 +682,10 @@ SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
     const double fl = floor(z);
     const double fr = z - fl;
     const uint64_t s = (uint64_t)fl;
-    const double us = c.systematic ? c.us_sys : (double)m_of(c, s) * INV53;
+    const double us = SYS ? c.us_sys : (double)m_of<SYS>(c, s) * INV53;
     const double d = fr - us;
     // |fr - 1/2| > 1/2 - guard  <=>  fr < guard or fr > 1 - guard (X == 0 lands here too)
-    if (c.force || fabs(fr - 0.5) > 0.5 - c.guard || fabs(d) < c.guard) return F_exact(c, X);
+    if (c.force || fabs(fr - 0.5) > 0.5 - c.guard || fabs(d) < c.guard) return F_exact<SYS>(c, X);
     return s + (d > 0.0 ? 1 : 0);
 }
 
@@ -862,6 +865,7 @@ __global__ void __launch_bounds__(RT) k_rs_aggs(const int32_t *__restrict__ cin,
 
 // Pass B1: counts per particle.  Embarrassingly parallel (no inter-tile wait);
 // the counts go to `counts` (the caller's or the workspace's).
+template <bool RES, bool MULTI, bool SYS>  // scheme family, resolved at compile time
 __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                   Key key, uint64_t stream, const double *__restrict__ u,
                                                   int32_t *__restrict__ counts, int ranks, Layout L)
@@ -880,14 +884,14 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
     const int64_t tbase = b * TILE;
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
     int32_t c[RI];
+    const bool full = tbase + TILE <= n;  // no per-element bounds checks on full tiles
     {
-        const bool residual = is_residual(scheme);
         uint64_t q[RI];
         int32_t f[RI];
         uint64_t loc = 0;
-        if (!residual) {
+        if (!RES) {
             // q_i was materialized by pass A: no exp / quantization here, 64 contiguous bytes per thread
-            if (!is_multinomial(scheme)) {
+            if (!MULTI) {
                 load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, q, s_q, 0ull);  // coalesced
             } else {
 #pragma unroll
@@ -902,7 +906,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
 #pragma unroll
             for (int j = 0; j < RI; ++j) {
                 const int64_t i = tbase + j * RT + threadIdx.x;
-                r[j] = i < n ? src.raw(i, nl) : 0.0;
+                r[j] = (full || i < n) ? src.raw(i, nl) : 0.0;
             }
             bool bad = false;
 #pragma unroll
@@ -910,7 +914,7 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
                 const int li = j * RT + threadIdx.x;
                 const int64_t i = tbase + li;
                 Quant qq{0, 0, 0};
-                if (i < n) qq = quantize(src.weight(r[j], nl), residual, m_out, rscale, bad);
+                if (full || i < n) qq = quantize(src.weight(r[j], nl), true, m_out, rscale, bad);
                 s_q[pad16(li)] = qq.qr;
                 s_fb[pad16(li)] = (int32_t)qq.f;
             }
@@ -922,9 +926,12 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
                 loc += q[j];
             }
         }
-        if (is_multinomial(scheme)) {
+        if (MULTI) {
+            int32_t h4[RI];
+            if (RES) __syncthreads();  // the staging above may still be reading s_fb
+            load_blocked<RT, RI, int32_t>(L.cnt, tbase, n, h4, s_fb, 0);  // the draws' histogram
 #pragma unroll
-            for (int j = 0; j < RI; ++j) c[j] = base + j < n ? f[j] + L.cnt[base + j] : 1;
+            for (int j = 0; j < RI; ++j) c[j] = (full || base + j < n) ? f[j] + h4[j] : 1;
         } else {
             uint64_t tot;
             uint64_t X = L.tile_pre[b] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
@@ -938,19 +945,24 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
             sc.stream = stream;
             sc.u = u;
             sc.key = key;
-            sc.systematic = is_systematic(scheme);
+            sc.systematic = SYS;
             sc.force = g_force_exact != 0;
             sc.us_sys = (double)sc.m_sys * INV53;
-            uint64_t Fp = (base < n && sc.M) ? F_fast(sc, X) : 0;
+            if (sc.M == 0) {  // residual with no leftovers: the floors are the counts
 #pragma unroll
-            for (int j = 0; j < RI; ++j) {
-                if (base + j < n) {
-                    uint64_t Fc = Fp;
-                    if (q[j] && sc.M) { X += q[j]; Fc = F_fast(sc, X); }
-                    c[j] = f[j] + (int32_t)(Fc - Fp);
-                    Fp = Fc;
-                } else {
-                    c[j] = 1;  // padding: neither zero slot nor surplus
+                for (int j = 0; j < RI; ++j) c[j] = (full || base + j < n) ? f[j] : 1;
+            } else {
+                uint64_t Fp = (full || base < n) ? F_fast<SYS>(sc, X) : 0;
+#pragma unroll
+                for (int j = 0; j < RI; ++j) {
+                    if (full || base + j < n) {
+                        uint64_t Fc = Fp;
+                        if (q[j]) { X += q[j]; Fc = F_fast<SYS>(sc, X); }
+                        c[j] = f[j] + (int32_t)(Fc - Fp);
+                        Fp = Fc;
+                    } else {
+                        c[j] = 1;  // padding: neither zero slot nor surplus
+                    }
                 }
             }
         }
@@ -958,6 +970,22 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
     __syncthreads();  // s_fb may still be read by the residual staging path
     store_blocked<RT, RI, int32_t>(counts, tbase, n, c, s_fb);  // coalesced
     if (ranks) tile_aggregate(c, b, L);  // the parent map's per-tile (Z, S, P) for k_rs_zsp_scan
+}
+
+inline void launch_counts(int scheme, unsigned nt, cudaStream_t s, WSrc src, int64_t n, double mo, double rscale,
+                          Key key, uint64_t stream, const double *u, int32_t *cout, int ranks, Layout L)
+{
+#define SMC_COUNTS(R_, M_, S_) \
+    smc_launch(k_rs_counts<R_, M_, S_>, nt, RT, 0, s, scheme, src, n, mo, rscale, key, stream, u, cout, ranks, L)
+    switch (scheme) {
+    case SMC_MULTINOMIAL: SMC_COUNTS(false, true, false); break;
+    case SMC_RESIDUAL: SMC_COUNTS(true, true, false); break;
+    case SMC_STRATIFIED: SMC_COUNTS(false, false, false); break;
+    case SMC_SYSTEMATIC: SMC_COUNTS(false, false, true); break;
+    case SMC_RESIDUAL_STRATIFIED: SMC_COUNTS(true, false, false); break;
+    default: SMC_COUNTS(true, false, true); break;  // SMC_RESIDUAL_SYSTEMATIC
+    }
+#undef SMC_COUNTS
 }
 
 // ------------------------------------------------------------------ pass C --
@@ -1281,8 +1309,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
-    smc_launch(k_rs_counts, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr,
-                                            L);
+    launch_counts(scheme, (unsigned)nt, s, src, n, mo, rscale, key, stream_index, u, cout, parents != nullptr, L);
     if (parents) {
         smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 1, status, L);
         smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
@@ -1415,7 +1442,7 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
-    smc_launch(k_rs_counts, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
+    launch_counts(scheme, (unsigned)nt, s, src, n, mo, rscale, key, stream_index, u, cout, 1, L);
     smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 0, status, L);
     smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
     smc_launch(k_rs_export_zsp, 1, 1, 0, s, L, zsp_out);
