@@ -1095,24 +1095,37 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     int32_t par[RI];
     uint32_t lo = 0;
     if (!SHARD) {
-        // one GPU: zero ranks and surplus ranks are the same 32-bit numbers
-        uint32_t g = (uint32_t)z0 + ex;  // zero rank of this thread's next zero slot
-        if (nz && cnt) {  // last k with s_start[k] <= g, then a forward merge walk
-            uint32_t hi = cnt;
-            while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if ((uint32_t)s_start[mid] <= g) lo = mid; else hi = mid;
+        // one GPU: zero ranks and surplus ranks are the same 32-bit numbers.  Each staged
+        // surplus parent k writes itself into the tile's rank table for the ranks it covers,
+        // [start_k, start_{k+1}) within [z0, z1); each zero slot then reads its parent by rank.
+        __shared__ int32_t s_par[TILE];
+        __shared__ uint32_t s_long[TILE / 32 + 1], s_nlong;  // runs longer than 32 ranks: block-wide
+        const uint32_t zlo = (uint32_t)z0, zhi = (uint32_t)z1;
+        if (threadIdx.x == 0) s_nlong = 0;
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
+            const uint32_t r0 = max((uint32_t)s_start[k], zlo), r1 = min((uint32_t)s_start[k + 1], zhi);
+            if (r1 > r0 + 32) {
+                s_long[atomicAdd(&s_nlong, 1u)] = k;  // at most TILE / 32 such runs in a tile
+                continue;
             }
+            const int32_t pk = s_idx[k];
+            for (uint32_t r = r0; r < r1; ++r) s_par[r - zlo] = pk;
         }
+        __syncthreads();
+        for (uint32_t l = 0; l < s_nlong; ++l) {  // e.g. one parent with thousands of children
+            const uint32_t k = s_long[l];
+            const uint32_t r0 = max((uint32_t)s_start[k], zlo), r1 = min((uint32_t)s_start[k + 1], zhi);
+            const int32_t pk = s_idx[k];
+            for (uint32_t r = r0 + threadIdx.x; r < r1; r += RT) s_par[r - zlo] = pk;
+        }
+        __syncthreads();
+        uint32_t g = ex;  // tile-local zero rank of this thread's next zero slot
         const int32_t b32 = (int32_t)base;
 #pragma unroll
         for (int j = 0; j < RI; ++j) {
             par[j] = b32 + j;  // survivors keep their slot
-            if (c[j] == 0) {
-                while ((uint32_t)s_start[lo + 1] <= g) ++lo;
-                par[j] = s_idx[lo];
-                ++g;
-            }
+            if (c[j] == 0) par[j] = s_par[g++];
         }
     } else {
         const int64_t zr = z0 + ex;  // first local zero rank
