@@ -212,3 +212,32 @@ def test_graph_replay_is_bit_identical_to_eager(scheme, n):
     (m0, h0, x0, w0, z0), (m1, h1, x1, w1, z1) = runs
     assert np.array_equal(m0, m1) and np.array_equal(h0, h1)
     assert np.array_equal(x0, x1) and np.array_equal(w0, w1) and z0 == z1
+
+
+def test_invariants_shift_trapezoid_ais():
+    """SPEC acceptance 8 invariant suites: log-weight shift invariance, trapezoid exactness on
+    linear integrands, and AIS/SIS equivalence at threshold <= 0 (no resampling: the running
+    log Z telescopes to log mean exp of each particle's accumulated increments)."""
+    from paper_1306_5583_b200 import PathAccumulator, WeightSet, gmm
+    rng = np.random.default_rng(9)
+    v = rng.normal(0, 3, 5000)
+    a, b = WeightSet(5000), WeightSet(5000)
+    a.set_log_weight(v)
+    b.set_log_weight(v + 123.456)
+    np.testing.assert_allclose(a.read_weight().cpu().numpy(), b.read_weight().cpu().numpy(), rtol=1e-12, atol=0)
+    assert abs(a.ess() - b.ess()) <= 1e-9 * a.ess()
+    grid = np.linspace(0, 1, 11) ** 2
+    pa = PathAccumulator(grid, 3.0 - 2.0 * grid)
+    assert abs(pa.log_zconst - 2.0) < 1e-15  # integral of 3 - 2a over [0, 1]
+    # no resampling and no MCMC: the particles stay prior draws and the increments sum to
+    # (sum_t dalpha_t) llh_i = llh_i, so log Z telescopes to log mean_i exp(llh_i)
+    y = gmm.generate_data(60, 21)
+    s = gmm.make_sampler(4096, data=y, T=12, seed=8, threshold=0.0)
+    s.mcmc_queue = []
+    s.initialize()
+    s.iterate(12)
+    assert not np.any(s.history()["resampled"])
+    llh = s.system.value.data[:, 13].cpu().numpy()
+    m = llh.max()
+    ais = m + np.log(np.mean(np.exp(llh - m)))
+    assert abs(s.log_zconst - ais) <= 1e-10 * max(1.0, abs(ais)), (s.log_zconst, ais)
