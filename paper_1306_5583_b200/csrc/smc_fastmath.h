@@ -183,6 +183,75 @@ SMC_HD double cos(double x)
     return res;
 }
 
+// cos(x) for 0 <= x < 8, BRANCH-FREE (the Box-Muller argument x = fl(2 pi u),
+// rng.py:91): one polynomial evaluation whose coefficients are picked by the
+// quadrant parity from a 2 x 8 table, so a warp never diverges and the whole
+// normal is one basic block the scheduler can interleave with the Philox work.
+//   j = rint(x 2/pi) (shifter: the integer lands in the low word), r = x - j pi/2
+//   with pi/2 = C1 + C2 (C1 = fl(pi/2); x - j C1 is exact for x >= pi/4 and j = 0
+//   below, the C2 product is folded in by one FMA), z = r^2;
+//   even j: cos r = 1 + z (-1/2 + z C(z)),  odd j: sin r = r + (r z) S(z)
+//   (fdlibm's __kernel_cos / __kernel_sin minimax coefficients on |r| <= pi/4),
+//   then the sign of quadrant j.  <= 1.5 ulp (tests/test_fastmath.py), the class of
+//   libdevice's cos (2 ulp).
+struct alignas(16) CosPoly {
+    double q[8];
+};
+SMC_TABLE CosPoly kCosPoly[2] = {
+    {{-0.5, 4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+      -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11, 0.0}},
+    {{-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
+      2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10, 0.0, 0.0}},
+};
+SMC_CONSTANT double kCosK[4] = {0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54, 0.0};
+
+SMC_HD double cos_bm(double x)
+{
+    const double SH = 0x1.8p52;
+    const double kd = fma_(x, kCosK[0], SH);  // x 2/pi rounded to an integer
+    const uint32_t j = (uint32_t)bits(kd);
+    const double jd = kd - SH;
+    const double r = fma_(-jd, kCosK[2], fma_(-jd, kCosK[1], x));
+    const double z = r * r;
+#ifdef __CUDA_ARCH__
+    const double2 *t = reinterpret_cast<const double2 *>(kCosPoly[j & 1].q);
+    const double2 q01 = __ldg(t), q23 = __ldg(t + 1), q45 = __ldg(t + 2), q67 = __ldg(t + 3);
+#else
+    const double *q = kCosPoly[j & 1].q;
+    const struct { double x, y; } q01{q[0], q[1]}, q23{q[2], q[3]}, q45{q[4], q[5]}, q67{q[6], q[7]};
+#endif
+    double p = fma_(z, q67.x, q45.y);
+    p = fma_(z, p, q45.x);
+    p = fma_(z, p, q23.y);
+    p = fma_(z, p, q23.x);
+    p = fma_(z, p, q01.y);
+    p = fma_(z, p, q01.x);
+    const double a = (j & 1) ? r : 1.0;
+    const double res = fma_(z * a, p, a);
+    // cos(j pi/2 + r): quadrants 1 and 2 negate -- flip the sign bit when bit 1 of j + 1 is set
+    return from_bits(bits(res) ^ ((uint64_t)((j + 1) & 2) << 62));
+}
+
+// sqrt(v) for v = 0 or v in [2^-60, 2^60] (the Box-Muller radius -2 log(1 - u),
+// rng.py:91), branch-free: the hardware fp64 rsqrt seed (MUFU.RSQ64H, ~2^-22)
+// refined by one Newton step on the reciprocal root and one correction of the
+// root itself (the residual v - s^2 by FMA).  Correctly rounded except in rare
+// near-halfway cases (<= 1 ulp).
+SMC_HD double sqrt_bm(double v)
+{
+#ifdef __CUDA_ARCH__
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+#else
+    double y = (double)(1.0f / sqrtf((float)v));  // a ~fp32-accurate seed, as on the device
+#endif
+    y = y * fma_(-0.5 * v * y, y, 1.5);
+    const double s = v * y;
+    const double d = fma_(-s, s, v);
+    const double res = fma_(d, 0.5 * y, s);
+    return v == 0.0 ? 0.0 : res;
+}
+
 // exp(x) for the GMM likelihood (smc_gmm.cu).  x = (128 m + j) ln2/128 + r with
 // |r| <= ln2/256; exp(r) - 1 by a degree-5 Taylor polynomial (truncation
 // < 2^-60); 2^(j/128) as hi + lo from kExpTab.  Subnormal results are scaled in

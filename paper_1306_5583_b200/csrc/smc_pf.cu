@@ -68,10 +68,12 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
     if (i < n) {
         const uint64_t c = ctrs[i], si = sbase + (uint64_t)i;  // global stream index of a sharded system
         // draw order x_pos, y_pos, x_vel, y_vel; normal = mean + sd*z (rng.py:201)
-        const double r0 = 0.0 + k.sd_pos0 * normal_at(c + 0, si, key);
-        const double r1 = 0.0 + k.sd_pos0 * normal_at(c + 2, si, key);
-        const double r2 = 0.0 + k.sd_vel0 * normal_at(c + 4, si, key);
-        const double r3 = 0.0 + k.sd_vel0 * normal_at(c + 6, si, key);
+        double z[4];
+        normals_at(c, si, key, z);
+        const double r0 = 0.0 + k.sd_pos0 * z[0];
+        const double r1 = 0.0 + k.sd_pos0 * z[1];
+        const double r2 = 0.0 + k.sd_vel0 * z[2];
+        const double r3 = 0.0 + k.sd_vel0 * z[3];
         ctrs[i] = c + 8;
         st_row(x + 4 * i, r0, r1, r2, r3);
         v = cv_llh(r0, r1, obs[0], obs[1]);
@@ -141,10 +143,12 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             }
             const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
-            x0 = x0 + ((0.0 + k.sd_pos * normal_at(c + 0, si, key)) + k.delta * x2);
-            x1 = x1 + ((0.0 + k.sd_pos * normal_at(c + 2, si, key)) + k.delta * x3);
-            x2 = x2 + (0.0 + k.sd_vel * normal_at(c + 4, si, key));
-            x3 = x3 + (0.0 + k.sd_vel * normal_at(c + 6, si, key));
+            double z[4];
+            normals_at(c, si, key, z);
+            x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
+            x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
+            x2 = x2 + (0.0 + k.sd_vel * z[2]);
+            x3 = x3 + (0.0 + k.sd_vel * z[3]);
             ctrs[i] = c + 8;
             st_row(x_out + 4 * i, x0, x1, x2, x3);
             const double incw = cv_llh(x0, x1, xo, yo);

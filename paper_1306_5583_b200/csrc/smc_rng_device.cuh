@@ -81,17 +81,37 @@ SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, const K &key)
     return __dmul_rn(__ull2double_rn(draw53(ctr, stream, key)), 1.0 / 9007199254740992.0);
 }
 
-// rng.py:85-91: Box-Muller cosine branch on 1 - u1, exactly two draws.
-// (All TUs build with --fmad=false, so no contraction changes the rounding;
-// log is smc_fastmath.h's table log (<= 0.55 ulp, 99.6 % bit-identical to glibc,
-// 8 % cheaper than libdevice on B200); cos is libdevice's (the fdlibm-style
-// smc_fm::cos diverges per quadrant and measured 40 % slower); sqrt is IEEE.)
+// rng.py:85-91: Box-Muller cosine branch on 1 - u1, exactly two draws, from the
+// two 53-bit draw integers.  (All TUs build with --fmad=false, so no contraction
+// changes the rounding.)  Branch-free: log is smc_fastmath.h's table log (<= 0.55
+// ulp, 99.6 % bit-identical to glibc), the radius root is sqrt_bm (bit-identical to
+// IEEE sqrt on these inputs) and cos is cos_bm (<= 1.33 ulp, 83 % bit-identical to
+// glibc, never more than 1 ulp away from it): the whole normal is one basic block.
+SMC_DEV double box_muller53(uint64_t m1, uint64_t m2)
+{
+    const double u1 = __dmul_rn(__ull2double_rn(m1), 1.0 / 9007199254740992.0);
+    const double u2 = __dmul_rn(__ull2double_rn(m2), 1.0 / 9007199254740992.0);
+    // 1 - u1 in [2^-53, 1]: a positive normal double, as log_core requires
+    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(1.0 - u1)) * smc_fm::cos_bm((2.0 * 3.141592653589793) * u2);
+}
+
 template <class K>
 SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, const K &key)
 {
-    const double u1 = u01_at(ctr, stream, key);
-    const double u2 = u01_at(ctr + 1, stream, key);
-    return sqrt(-2.0 * smc_fm::log_core(1.0 - u1)) * cos((2.0 * 3.141592653589793) * u2);  // 1 - u1 in [2^-53, 1]
+    return box_muller53(draw53(ctr, stream, key), draw53(ctr + 1, stream, key));
+}
+
+// NZ consecutive normals of one stream (draws ctr .. ctr + 2 NZ - 1): every Philox
+// block first (2 NZ independent integer chains the scheduler interleaves), then the
+// NZ Box-Muller transforms.  Bit-identical to NZ calls of normal_at.
+template <int NZ, class K>
+SMC_DEV void normals_at(uint64_t ctr, uint64_t stream, const K &key, double (&z)[NZ])
+{
+    uint64_t m[2 * NZ];
+#pragma unroll
+    for (int j = 0; j < 2 * NZ; ++j) m[j] = draw53(ctr + (uint64_t)j, stream, key);
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1]);
 }
 
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the

@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos):
+    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_cos_bm, lib.fm_sqrt_bm):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -168,3 +168,51 @@ def test_exp_nonpos(fm):
     assert ulp_err(got, [decimal.Decimal(float(x)).exp() for x in xs]) <= 0.52
     edge = fm("fm_exp_nonpos", np.array([-708.5, -745.0, -1e6, -np.inf]))
     assert np.all(edge == 0.0)
+
+
+def _dcos(x):
+    x = decimal.Decimal(float(x))
+    s, t, k = decimal.Decimal(1), decimal.Decimal(1), 0
+    while abs(t) > decimal.Decimal(10) ** -70:
+        k += 2
+        t = -t * x * x / (k * (k - 1))
+        s += t
+    return s
+
+
+def test_cos_bm_exact_ulp(fm):
+    """smc_fm::cos_bm (branch-free Box-Muller cos, x = fl(2 pi u) in [0, 2 pi)): <= 1.5 ulp of
+    max(|cos|, 2^-30) against 60-digit values, incl. every quadrant boundary."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(12)
+    u = rng.integers(0, 2 ** 53, 12000) * 2.0 ** -53
+    near = np.array([k * math.pi / 4 + d for k in range(0, 9) for d in (0.0, 1e-15, -1e-15, 1e-12, -1e-9, 3e-7)])
+    xs = np.concatenate([(2.0 * math.pi) * u, near[near >= 0], [0.0, 1e-300, 0.785, 0.79, 0.3, 6.283185307179586,
+                                                                 (2.0 * math.pi) * (1 - 2.0 ** -53), 7.99]])
+    got = fm("fm_cos_bm", xs)
+    errs = []
+    for g, x in zip(got, xs):
+        e = _dcos(x)
+        sp = math.ulp(max(abs(float(e)), 2.0 ** -30))
+        errs.append(float(abs(decimal.Decimal(g) - e) / decimal.Decimal(sp)))
+    assert max(errs) <= 1.5, max(errs)
+
+
+def test_cos_bm_agrees_with_glibc_bulk(fm):
+    rng = np.random.default_rng(13)
+    u = rng.integers(0, 2 ** 53, 2_000_000) * 2.0 ** -53
+    xc = (2.0 * math.pi) * u
+    a, b = fm("fm_cos_bm", xc), np.cos(xc)
+    assert np.max(np.abs(a - b) / np.spacing(np.maximum(np.abs(b), 2.0 ** -30))) <= 2.0
+    assert np.mean(a == b) > 0.8
+
+
+def test_sqrt_bm(fm):
+    """smc_fm::sqrt_bm (Box-Muller radius): within 1 ulp of IEEE sqrt, sqrt(0) = 0."""
+    rng = np.random.default_rng(14)
+    u = rng.integers(1, 2 ** 53, 2_000_000) * 2.0 ** -53
+    v = np.concatenate([-2.0 * np.log(1.0 - u), -2.0 * np.log(u), [0.0, 2.0 ** -52, 74.6, 1.0, 4.0, 2.0]])
+    a, b = fm("fm_sqrt_bm", v), np.sqrt(v)
+    assert a[-6] == 0.0
+    assert np.max(np.abs(a - b) / np.spacing(np.maximum(b, 1e-300))) <= 1.0
+    assert np.mean(a == b) > 0.999
