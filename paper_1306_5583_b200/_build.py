@@ -51,6 +51,8 @@ def build(force=False, verbose=False, extra=()):
     """Compile csrc/*.cu into paper_1306_5583_b200/libsmcb200.so (sm_100a)."""
     if not force and not _stale():
         return LIB
+    if not force and os.environ.get("SMC_LIB_PATH") and os.path.exists(LIB):
+        return LIB  # an A/B variant is used as built, never rebuilt from the current sources
     cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *sources()]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

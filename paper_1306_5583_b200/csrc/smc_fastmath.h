@@ -8,6 +8,7 @@
 // the CPU test runs the identical code.
 //
 // log(x) = k ln2 + log(c_i) + log1p(r),  x = 2^k z,  z in [0.6875, 1.375),
+//          k ln2 + log(c_i) exact as a double (table on the 2^-42 grid of LN2_HI),
 //          r = z/c_i - 1 via one FMA (|r| <= 2^-7.5), c_i = 1 exactly around z = 1
 //          so that r = z - 1 is exact there (full relative accuracy near x = 1),
 //          log1p(r) - r by a degree-8 Taylor polynomial (truncation < 2^-59 |r|).
@@ -110,15 +111,13 @@ SMC_HD double log_core(double x)
     const double r = fma_(z, invc, -1.0);
     const double kd = (double)k;
     const double LN2_HI = kLogK[4], LN2_LO = kLogK[5];
-    // hi + lo = k ln2 + log c + r with error-free sums (k LN2_HI is exact: 42 + 11 bits)
-    const double a = kd * LN2_HI;
-    const double w = a + lhi;
-    const double wb = w - a;
-    const double we = (a - (w - wb)) + (lhi - wb);  // TwoSum(a, lhi)
+    // hi + lo = k ln2 + log c + r with error-free sums: k LN2_HI is exact (42 + 11 bits)
+    // and so is w = k LN2_HI + logc_hi (the table puts logc_hi on LN2_HI's 2^-42 grid,
+    // tools/gen_logtab.py); hi = w + r is split by Fast2Sum (|w| >= |r| or w = 0)
+    const double w = fma_(kd, LN2_HI, lhi);
     const double hi = w + r;
-    const double hb = hi - w;
-    const double he = (w - (hi - hb)) + (r - hb);   // TwoSum(w, r)
-    const double lo = (he + we) + fma_(kd, LN2_LO, llo);
+    const double he = r - (hi - w);
+    const double lo = he + fma_(kd, LN2_LO, llo);
     // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
     double p = fma_(r, -0.125, kLogK[0]);
     p = fma_(r, p, kLogK[1]);
@@ -185,24 +184,31 @@ SMC_HD double cos(double x)
 
 // cos(x) for 0 <= x < 8, BRANCH-FREE (the Box-Muller argument x = fl(2 pi u),
 // rng.py:91): one polynomial evaluation whose coefficients are picked by the
-// quadrant parity from a 2 x 8 table, so a warp never diverges and the whole
+// quadrant from a 4-row table, so a warp never diverges and the whole
 // normal is one basic block the scheduler can interleave with the Philox work.
 //   j = rint(x 2/pi) (shifter: the integer lands in the low word), r = x - j pi/2
 //   with pi/2 = C1 + C2 (C1 = fl(pi/2); x - j C1 is exact for x >= pi/4 and j = 0
 //   below, the C2 product is folded in by one FMA), z = r^2;
 //   even j: cos r = 1 + z (-1/2 + z C(z)),  odd j: sin r = r + (r z) S(z)
 //   (fdlibm's __kernel_cos / __kernel_sin minimax coefficients on |r| <= pi/4),
-//   then the sign of quadrant j.  <= 1.5 ulp (tests/test_fastmath.py), the class of
-//   libdevice's cos (2 ulp).
+//   and the sign of quadrant j: cos(j pi/2 + r) = A + (z A) p(z) with A = +-1 (even j)
+//   or +-r (odd j), A = fma(a1, r, a0) from the (j mod 4) table row.  <= 1.5 ulp
+//   (tests/test_fastmath.py), the class of libdevice's cos (2 ulp).
 struct alignas(16) CosPoly {
-    double q[8];
+    double a0, a1, q[8];  // A = a1 r + a0; q[7] = 0 pads the row to 5 x 16 bytes
 };
-SMC_TABLE CosPoly kCosPoly[2] = {
-    {{-0.5, 4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
-      -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11, 0.0}},
-    {{-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
-      2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10, 0.0, 0.0}},
+#define SMC_COS_Q {-0.5, 4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05, \
+                   -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11, 0.0}
+#define SMC_SIN_Q {-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04, \
+                   2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10, 0.0, 0.0}
+SMC_TABLE CosPoly kCosPoly[4] = {
+    {1.0, 0.0, SMC_COS_Q},    // j = 0 mod 4:  cos r
+    {0.0, -1.0, SMC_SIN_Q},   // j = 1:       -sin r
+    {-1.0, 0.0, SMC_COS_Q},   // j = 2:       -cos r
+    {0.0, 1.0, SMC_SIN_Q},    // j = 3:        sin r
 };
+#undef SMC_COS_Q
+#undef SMC_SIN_Q
 SMC_CONSTANT double kCosK[4] = {0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54, 0.0};
 
 SMC_HD double cos_bm(double x)
@@ -214,11 +220,12 @@ SMC_HD double cos_bm(double x)
     const double r = fma_(-jd, kCosK[2], fma_(-jd, kCosK[1], x));
     const double z = r * r;
 #ifdef __CUDA_ARCH__
-    const double2 *t = reinterpret_cast<const double2 *>(kCosPoly[j & 1].q);
-    const double2 q01 = __ldg(t), q23 = __ldg(t + 1), q45 = __ldg(t + 2), q67 = __ldg(t + 3);
+    const double2 *t = reinterpret_cast<const double2 *>(&kCosPoly[j & 3]);
+    const double2 a = __ldg(t), q01 = __ldg(t + 1), q23 = __ldg(t + 2), q45 = __ldg(t + 3), q67 = __ldg(t + 4);
 #else
-    const double *q = kCosPoly[j & 1].q;
-    const struct { double x, y; } q01{q[0], q[1]}, q23{q[2], q[3]}, q45{q[4], q[5]}, q67{q[6], q[7]};
+    const CosPoly &e = kCosPoly[j & 3];
+    const struct { double x, y; } a{e.a0, e.a1}, q01{e.q[0], e.q[1]}, q23{e.q[2], e.q[3]}, q45{e.q[4], e.q[5]},
+        q67{e.q[6], e.q[7]};
 #endif
     double p = fma_(z, q67.x, q45.y);
     p = fma_(z, p, q45.x);
@@ -226,30 +233,29 @@ SMC_HD double cos_bm(double x)
     p = fma_(z, p, q23.x);
     p = fma_(z, p, q01.y);
     p = fma_(z, p, q01.x);
-    const double a = (j & 1) ? r : 1.0;
-    const double res = fma_(z * a, p, a);
-    // cos(j pi/2 + r): quadrants 1 and 2 negate -- flip the sign bit when bit 1 of j + 1 is set
-    return from_bits(bits(res) ^ ((uint64_t)((j + 1) & 2) << 62));
+    const double A = fma_(a.y, r, a.x);  // exact: +-1 or +-r
+    return fma_(z * A, p, A);
 }
 
 // sqrt(v) for v = 0 or v in [2^-60, 2^60] (the Box-Muller radius -2 log(1 - u),
-// rng.py:91), branch-free: the hardware fp64 rsqrt seed (MUFU.RSQ64H, ~2^-22)
-// refined by one Newton step on the reciprocal root and one correction of the
-// root itself (the residual v - s^2 by FMA).  Correctly rounded except in rare
-// near-halfway cases (<= 1 ulp).
+// rng.py:91), branch- and select-free: the hardware fp64 rsqrt seed (MUFU.RSQ64H,
+// ~2^-22) of v + 2^-1000 (= v unless v = 0, where it keeps the seed finite so the
+// root comes out as 0 * y = 0) refined by one Newton step on the reciprocal root
+// and one correction of the root itself (the residual v - s^2 by FMA).  Correctly
+// rounded except in rare near-halfway cases (<= 1 ulp).
 SMC_HD double sqrt_bm(double v)
 {
+    const double vp = v + 0x1p-1000;
 #ifdef __CUDA_ARCH__
     double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(vp));
 #else
-    double y = (double)(1.0f / sqrtf((float)v));  // a ~fp32-accurate seed, as on the device
+    double y = from_bits(bits(1.0 / ::sqrt(vp)) & 0xffffffffe0000000ull);  // a ~fp32-accurate seed, as on the device
 #endif
-    y = y * fma_(-0.5 * v * y, y, 1.5);
+    y = y * fma_(-0.5 * vp * y, y, 1.5);
     const double s = v * y;
     const double d = fma_(-s, s, v);
-    const double res = fma_(d, 0.5 * y, s);
-    return v == 0.0 ? 0.0 : res;
+    return fma_(d, 0.5 * y, s);
 }
 
 // exp(x) for the GMM likelihood (smc_gmm.cu).  x = (128 m + j) ln2/128 + r with

@@ -89,10 +89,11 @@ SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, const K &key)
 // glibc, never more than 1 ulp away from it): the whole normal is one basic block.
 SMC_DEV double box_muller53(uint64_t m1, uint64_t m2)
 {
-    const double u1 = __dmul_rn(__ull2double_rn(m1), 1.0 / 9007199254740992.0);
-    const double u2 = __dmul_rn(__ull2double_rn(m2), 1.0 / 9007199254740992.0);
-    // 1 - u1 in [2^-53, 1]: a positive normal double, as log_core requires
-    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(1.0 - u1)) * smc_fm::cos_bm((2.0 * 3.141592653589793) * u2);
+    // 1 - u1 = 1 - m1 2^-53 in [2^-53, 1] (exact, one FMA): a positive normal double, as
+    // log_core requires; fl(2 pi u2) = fl((2 pi 2^-53) m2), the power-of-two scale being exact
+    const double v1 = __fma_rn(-__ull2double_rn(m1), 1.0 / 9007199254740992.0, 1.0);
+    const double x2 = __dmul_rn(__ull2double_rn(m2), (2.0 * 3.141592653589793) / 9007199254740992.0);
+    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(v1)) * smc_fm::cos_bm(x2);
 }
 
 template <class K>
