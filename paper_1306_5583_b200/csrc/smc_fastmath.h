@@ -44,8 +44,8 @@ typedef int int32_t;
 
 namespace smc_fm {
 
-struct LogEntry {
-    double invc, logc_hi, logc_lo;
+struct alignas(16) LogEntry {
+    double invc, logc_hi, logc_lo, pad;  // 32 bytes: two 128-bit loads per lookup
 };
 
 SMC_TABLE LogEntry kLogTab[128] = {
@@ -102,9 +102,9 @@ SMC_HD double log_core(double x)
     const int64_t k = (int64_t)tmp >> 52;
     const double z = from_bits(ix - (tmp & (0xfffull << 52)));
 #ifdef __CUDA_ARCH__
-    const double invc = __ldg(&kLogTab[i].invc);
-    const double lhi = __ldg(&kLogTab[i].logc_hi);
-    const double llo = __ldg(&kLogTab[i].logc_lo);
+    const double2 e0 = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]));
+    const double2 e1 = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]) + 1);
+    const double invc = e0.x, lhi = e0.y, llo = e1.x;
 #else
     const double invc = kLogTab[i].invc, lhi = kLogTab[i].logc_hi, llo = kLogTab[i].logc_lo;
 #endif
@@ -263,7 +263,7 @@ SMC_HD double sqrt_bm(double v)
 // < 2^-60); 2^(j/128) as hi + lo from kExpTab.  Subnormal results are scaled in
 // two steps; overflow gives +inf; NaN propagates.  No libm call, no branch.  The table is passed in so the device can
 // stage it in shared memory (one LDS.128 per call instead of a global gather).
-struct ExpEntry {
+struct alignas(16) ExpEntry {
     double hi, lo;
 };
 

@@ -12,9 +12,12 @@ using namespace smc;
 
 namespace {
 
-constexpr int PB = 256;
+#ifndef PF_PB
+#define PF_PB 128  // threads per PF block (same-box A/B: 128 x 8 blocks/SM 2 % faster than 256 x 4)
+#endif
+constexpr int PB = PF_PB;
 #ifndef PF_MIN_BLOCKS
-#define PF_MIN_BLOCKS 4
+#define PF_MIN_BLOCKS 8
 #endif
 #ifndef PF_PPT
 #define PF_PPT 4  // particles per thread in the move kernel
