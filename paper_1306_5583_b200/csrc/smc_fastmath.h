@@ -45,8 +45,9 @@ typedef int int32_t;
 namespace smc_fm {
 
 struct alignas(16) LogEntry {
-    double invc, logc_hi, logc_lo, pad;  // 32 bytes: two 128-bit loads per lookup
-};
+    double logc_hi;       // -log(invc) on the 2^-42 grid
+    float invc, logc_lo;  // 1/c in single precision (exact as a double), the |lo| <= 2^-43 rest
+};                        // 16 bytes: one 128-bit load per lookup
 
 SMC_TABLE LogEntry kLogTab[128] = {
 #include "smc_logtab.inc"
@@ -102,11 +103,11 @@ SMC_HD double log_core(double x)
     const int64_t k = (int64_t)tmp >> 52;
     const double z = from_bits(ix - (tmp & (0xfffull << 52)));
 #ifdef __CUDA_ARCH__
-    const double2 e0 = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]));
-    const double2 e1 = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]) + 1);
-    const double invc = e0.x, lhi = e0.y, llo = e1.x;
+    const double2 e = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]));
+    const uint64_t w1 = (uint64_t)__double_as_longlong(e.y);
+    const double lhi = e.x, invc = (double)__uint_as_float((uint32_t)w1), llo = (double)__uint_as_float((uint32_t)(w1 >> 32));
 #else
-    const double invc = kLogTab[i].invc, lhi = kLogTab[i].logc_hi, llo = kLogTab[i].logc_lo;
+    const double invc = kLogTab[i].invc, lhi = kLogTab[i].logc_hi, llo = kLogTab[i].logc_lo;  // float -> double exact
 #endif
     const double r = fma_(z, invc, -1.0);
     const double kd = (double)k;
