@@ -279,7 +279,7 @@ def run_b200(args):
                               "weights": "the PF's pre-resample weights (one extra move after the run)",
                               "reps": rc["reps"],
                               "kernels": "k_rs_tiles, k_rs_scan, k_rs_counts, k_rs_zsp_scan, k_rs_ranks, "
-                                         "k_rs_assign, k_rs_copy<32>"},
+                                         "k_rs_assign<copy fused>"},
             "dominant_phase": dominant, "clocks": clk.summary()}
 
     # ---- e2e: the public API with host buffers: per step H2D the observation pair from pinned

@@ -1034,7 +1034,11 @@ struct ShardC {
     int64_t row_bytes;
 };
 
-template <bool SHARD>
+// COPY32 (one GPU, 32-byte rows): the value collection's in-place copy fused in -- every zero
+// slot's row is overwritten by its parent's as soon as the parent is known (sources have
+// count >= 2, destinations count 0: disjoint), saving the separate copy pass and
+// its re-read of the parent vector.
+template <bool SHARD, bool COPY32 = false>
 __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
                                                   int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
@@ -1126,6 +1130,19 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
         for (int j = 0; j < RI; ++j) {
             par[j] = b32 + j;  // survivors keep their slot
             if (c[j] == 0) par[j] = s_par[g++];
+        }
+        if (COPY32) {  // 4 row loads in flight per thread, then their stores
+            double *rows = (double *)sc.rows;
+#pragma unroll
+            for (int j0 = 0; j0 < RI; j0 += 4) {
+                double4 v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c[j0 + j] == 0) ld256(rows + (int64_t)par[j0 + j] * 4, v[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (c[j0 + j] == 0) st256(rows + (base + j0 + j) * 4, v[j]);
+            }
         }
     } else {
         const int64_t zr = z0 + ex;  // first local zero rank
@@ -1326,11 +1343,12 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (parents) {
         smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 1, status, L);
         smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
-        smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
-        if (rows) {  // the value collection's copy: one moved row per thread, full occupancy
-            if (row_bytes == 32)
-                smc_launch(k_rs_copy<32>, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, 32, n, L);
-            else
+        if (rows && row_bytes == 32) {  // the value collection's copy fused into pass C
+            smc_launch(k_rs_assign<false, true>, (unsigned)nt, RT, 0, s, cout, n, parents,
+                       ShardC{0, 0, -1, nullptr, (char *)rows, 32}, L);
+        } else {
+            smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+            if (rows)  // other row sizes: one moved row per thread, full occupancy
                 smc_launch(k_rs_copy<0>, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, row_bytes, n, L);
         }
     }
