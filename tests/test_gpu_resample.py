@@ -191,3 +191,26 @@ def test_unbiasedness_acceptance_1_on_device(scheme):
     st = O.Streams(5, 2024)
     ref = np.array([O.resample_counts(scheme, W.cpu().numpy(), streams=st, stream=4)[0] for _ in range(200)])
     assert np.array_equal(acc[:200].astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("scheme", ["systematic", "residual_stratified"])
+def test_multichunk_tile_scans_bit_exact(scheme):
+    """N > 2^24: more tiles (16391) than one chunk of the single-block scans (passes S and S2
+    walk 1024 threads x 8 tiles per chunk), counts / parents / the fused 32-byte row copy
+    bit-exact with the oracle."""
+    n = (1 << 25) + 12345
+    w = weights(n, "skewed")
+    u = np.random.default_rng(9).random(n)
+    x = None
+    if scheme == "systematic":
+        x = np.random.default_rng(3).normal(size=(n, 4))
+        xg = torch.as_tensor(x).cuda().contiguous()
+        got, par = gpu_resample(scheme, w, u=u, rows=xg)
+    else:
+        got, par = gpu_resample(scheme, w, u=u)
+    ref, _ = O.resample_counts(scheme, w, u=u)
+    assert np.array_equal(got, ref)
+    pref = O.replication_to_parents(ref)
+    assert np.array_equal(par, pref)
+    if x is not None:
+        assert np.array_equal(xg.cpu().numpy(), x[pref])
