@@ -26,7 +26,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DEFAULT = 1 << 24
+N_DEFAULT = 1 << 24       # config 2: one B200
+N_SHARDED = 1 << 28       # config 4: the whole filter sharded over G B200 (2^28 / G particles per GPU)
 METRIC = "PF particle-steps/sec at N=2^24 (resample+copy GB/s vs HBM peak reported alongside)"
 UNIT = "particle-steps/s"
 
@@ -37,13 +38,31 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)  # ~0.3 s timed: several clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--particles", "--n", dest="n", type=int, default=N_DEFAULT,
-                    help="particles per GPU (use --particles under torchrun: it claims --n*)")
+    ap.add_argument("--particles", "--n", dest="n", type=int, default=None,
+                    help="particles per GPU (default: 2^24 on one GPU -- config 2 -- and 2^28 / G on G > 1 "
+                         "GPUs -- config 4, strong scaling); use --particles under torchrun: it claims --n*")
     ap.add_argument("--scheme", default="systematic")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gmm", action="store_true")
     return ap.parse_args()
+
+
+def workload(n, world, scheme, strong):
+    """(scaling, config) of the JSON line: config 2 on one GPU, config 4 (2^28 in total) on G > 1."""
+    if strong:
+        name = (f"PF config 4: N=2^{(n * world).bit_length() - 1} particles in total sharded over {world} GPUs "
+                f"(2^{n.bit_length() - 1} per GPU), ")
+    else:
+        name = f"PF config 2: N=2^{n.bit_length() - 1} particles per GPU, "
+    name += f"{scheme} resampling at ESS<N/2, 4-dim state, Student-t(10) likelihood, 100-obs model track"
+    return ("strong" if strong else "weak"), {"workload": name, "n_particles": n * world, "scheme": scheme}
+
+
+def particles_per_gpu(args, world):
+    if args.n is not None:
+        return args.n
+    return N_DEFAULT if world == 1 else N_SHARDED // world
 
 
 def dist_env():
@@ -149,7 +168,7 @@ def run_reference(args):
     import numpy as np
 
     cores = len(os.sched_getaffinity(0))
-    n = args.n
+    n = particles_per_gpu(args, world)
     # bounded sample: every step runs the full PF step on N_s <= N particles, N_s the largest power of
     # two with (W + K) N_s <= 4e8 particle-steps (about a minute on a 16-core host, whatever K the
     # driver passes), and the rate is reported per particle-step
@@ -160,14 +179,13 @@ def run_reference(args):
     times = cpu_baseline_pf(ns, args.warmup + args.steps, args.scheme, obs, cores)
     t = sum(times[args.warmup:])
     v = ns * args.steps / t
+    scaling, cfg = workload(n, world, args.scheme, world > 1 and args.n is None)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps * (n / ns), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             # the same workload line as the B200 arm (N per GPU x world); each step is a bounded
-            # sample of it: one host runs N = args.n particles and the rate is per particle-step
-            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles per GPU, {args.scheme} "
-                                   "resampling at ESS<N/2, 4-dim state, Student-t(10) likelihood, 100-obs model "
-                                   "track", "n_particles": n * world, "scheme": args.scheme},
+            # sample of it: one host runs N_s particles and the rate is per particle-step
+            "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{args.steps} full PF steps of the C oracle at N={ns} (of the workload's "
                                        f"N={n}) on one host (after {args.warmup} warm-up steps), OpenMP "
@@ -197,8 +215,11 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1306_5583_b200 as P
 
-    n_total = args.n * world if world > 1 else args.n  # weak scaling: N per GPU fixed
-    n = args.n
+    n = particles_per_gpu(args, world)
+    n_total = n * world
+    # one GPU: config 2 (N = 2^24); G > 1: config 4 (N = 2^28 in total, 2^28 / G per GPU: strong
+    # scaling) unless --particles fixes the per-GPU size (then weak)
+    strong = world > 1 and args.n is None
     T = args.warmup + args.steps + 2
     rs = np.random.default_rng(1306)
     # synthetic observations of the paper's shape: a smooth track + noise (T x 2)
@@ -258,14 +279,12 @@ def run_b200(args):
     dominant = max(("move", "resample", "monitor"), key=lambda k: phase.get(k, 0))
 
     value = n_total * args.steps / (ms * 1e-3)
+    scaling, cfg = workload(n, world, args.scheme, strong)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"PF config 2: N=2^{n.bit_length() - 1} particles per GPU, {args.scheme} "
-                                   "resampling at ESS<N/2, 4-dim state, Student-t(10) likelihood, 100-obs model "
-                                   "track", "n_particles": n_total, "scheme": args.scheme,
-                       "l2": "inputs larger than L2 (state 512 MiB/GPU at 2^24), no flush",
-                       "parallelism": f"particles sharded over {world} GPU(s)"},
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(cfg, l2=f"inputs larger than L2 (state {32 * n >> 20} MiB per GPU), no flush",
+                           parallelism=f"particles sharded over {world} GPU(s)"),
             "phase_ms": phase, "resampled_frac": float(np.mean(resampled)), "moved_row_frac": frac_moved,
             # per step: k_pf_move, k_lse_level1, k_lse_finalize, k_ess_decide, 6 resample passes
             # (device-gated: they launch every step), k_set_equal
