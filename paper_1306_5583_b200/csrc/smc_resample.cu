@@ -689,6 +689,22 @@ SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
     return s + (d > 0.0 ? 1 : 0);
 }
 
+// F_fast without its branch: the fast value, and `ex` set when the exact path must decide
+// (X >= Tm, X == 0 or a guard-band hit) -- per-element loops stay branch-free and fall
+// back warp-wide only when some lane needs it.
+template <bool SYS>
+SMC_DEV uint64_t F_fast_flag(const StratCtx &c, uint64_t X, bool &ex)
+{
+    const double z = (double)X * c.ratio;
+    const double fl = floor(z);
+    const double fr = z - fl;
+    const uint64_t s = (uint64_t)fl;
+    const double us = SYS ? c.us_sys : (double)m_of<SYS>(c, s < c.M ? s : c.M - 1) * INV53;
+    const double d = fr - us;
+    ex = c.force || X >= c.Tm || fabs(fr - 0.5) > 0.5 - c.guard || fabs(d) < c.guard;
+    return s + (d > 0.0 ? 1 : 0);
+}
+
 // pack (zero slots, surplus parents) in the top 2 x 14 bits, surplus children in
 // the low 36 -- tile-local sums never carry across fields (<= 2048, < 2^31).
 SMC_DEV uint64_t pack_zsp(uint32_t z, uint32_t p, uint64_t s) { return ((uint64_t)z << 50) | ((uint64_t)p << 36) | s; }
@@ -952,17 +968,36 @@ __global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t 
 #pragma unroll
                 for (int j = 0; j < RI; ++j) c[j] = (full || base + j < n) ? f[j] : 1;
             } else {
-                uint64_t Fp = (full || base < n) ? F_fast<SYS>(sc, X) : 0;
+                // F at the thread's start and after each of its RI items (padding items have
+                // q = 0: F unchanged) by the branch-free fast path; when any lane of the warp
+                // flagged an item (rare: the guard band, X = 0 at the very start, X >= Tm at
+                // the end) the warp redoes its items with the exact path where flagged
+                bool e, any = false;
+                uint64_t Xj = X;
+                uint64_t Fp = F_fast_flag<SYS>(sc, Xj, e);
+                any |= e;
 #pragma unroll
                 for (int j = 0; j < RI; ++j) {
-                    if (full || base + j < n) {
-                        uint64_t Fc = Fp;
-                        if (q[j]) { X += q[j]; Fc = F_fast<SYS>(sc, X); }
-                        c[j] = f[j] + (int32_t)(Fc - Fp);
+                    Xj += q[j];
+                    const uint64_t Fc = F_fast_flag<SYS>(sc, Xj, e);
+                    any |= e;
+                    c[j] = (full || base + j < n) ? f[j] + (int32_t)(Fc - Fp) : 1;  // padding: 1
+                    Fp = Fc;
+                }
+                if (__any_sync(0xffffffffu, any)) {  // q re-read from pass A's copy: no indexed registers
+                    __shared__ int32_t s_cx[RT * RI];
+                    Xj = X;
+                    Fp = F_fast<SYS>(sc, Xj);
+#pragma unroll 1
+                    for (int j = 0; j < RI; ++j) {
+                        Xj += (full || base + j < n) ? L.qfull[base + j] : 0;
+                        const uint64_t Fc = F_fast<SYS>(sc, Xj);
+                        s_cx[threadIdx.x * RI + j] = (int32_t)(Fc - Fp);
                         Fp = Fc;
-                    } else {
-                        c[j] = 1;  // padding: neither zero slot nor surplus
                     }
+#pragma unroll
+                    for (int j = 0; j < RI; ++j)
+                        if (full || base + j < n) c[j] = f[j] + s_cx[threadIdx.x * RI + j];
                 }
             }
         }
