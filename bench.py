@@ -292,7 +292,10 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "kernel": "k_pf_move (fused move + add_log_weight + lse/ESS partials)",
                          "achieved": move_gbs, "peak": peak, "unit": "GB/s", "frac": move_gbs / peak,
                          "traffic": move_traffic(n), "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": move_bytes},
+                         "algorithmic_bytes_per_launch": move_bytes,
+                         # the kernel is compute-bound by the reference's RNG contract:
+                         # its issue floor from the ncu instruction count, against the measured time
+                         "compute": compute_floor(n, phase["move"])},
             "resample_copy": {"achieved": rc["gbs"], "peak": peak, "unit": "GB/s", "frac": rc["gbs"] / peak,
                               "ms": rc["ms"], "algorithmic_bytes": rc["bytes"], "scheme": args.scheme,
                               "weights": "the PF's pre-resample weights (one extra move after the run)",
@@ -355,6 +358,21 @@ def move_traffic(n):
         return d["dram_bytes_read"] + d["dram_bytes_write"] if d.get("n") == n else None
     except (OSError, ValueError, KeyError):
         return None
+
+
+def compute_floor(n, move_ms):
+    """Issue floor of k_pf_move: instructions per particle (ncu, profiles/r1_ncu_move_mix.txt) over
+    148 SMs x 4 schedulers x 32 lanes at the max SM clock -- the compute roofline the move is held to."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_move_mix.txt")) as f:
+            head = [l for l in f if "warp-instructions (" in l][0]
+        ipp = float(head.split("(")[1].split()[0])
+    except (OSError, IndexError, ValueError):
+        return None
+    floor_ms = n * ipp / (148 * 128 * 1.965e9) * 1e3
+    return {"bound": "issue (IMAD.WIDE Philox on the FMA pipe + fp64 Box-Muller)", "instr_per_particle": ipp,
+            "issue_floor_ms": floor_ms, "achieved_ms": move_ms, "frac": floor_ms / move_ms,
+            "source": "profiles/r1_ncu_move_mix.txt (ncu --set full, one launch at 2^24)"}
 
 
 def resample_copy_bench(P, system, scheme, reps=10):
