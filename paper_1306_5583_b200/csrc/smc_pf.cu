@@ -167,22 +167,14 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
             double z[4];
-#ifdef PF_EXPERIMENT_NO_NORMALS  // cost-attribution experiment only (tools/ab_lib.sh); never the product
-            for (int j = 0; j < 4; ++j) z[j] = (double)(int)((c + si * 7 + j) & 255) * 1e-3;
-#else
             normals_at(c, si, key, z);
-#endif
             x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
             x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
             x2 = x2 + (0.0 + k.sd_vel * z[2]);
             x3 = x3 + (0.0 + k.sd_vel * z[3]);
             ctrs[i] = c + 8;
             st_row(x_out + 4 * i, x0, x1, x2, x3);
-#ifdef PF_EXPERIMENT_NO_LLH
-            const double incw = -0.5 * (x0 - xo) * (x0 - xo);
-#else
             const double incw = cv_llh(x0, x1, xo, yo);
-#endif
             if (incw_out) incw_out[i] = incw;
             v = prev + incw;  // add_log_weight(incw)
             if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }

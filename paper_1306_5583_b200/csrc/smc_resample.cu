@@ -23,11 +23,12 @@
 //                     surplus parents, surplus children) aggregate.
 //   S2 k_rs_zsp_scan: one block: exclusive prefixes of those aggregates.
 //   B2 k_rs_ranks   : per tile: the compacted surplus-parent list + rank anchors.
-//   C  k_rs_assign  : per tile of zero-slot ranks: the tile's slice of the
-//                     surplus-parent prefix staged in shared memory (merge-path
-//                     boundaries by binary search), a linear merge walk per
-//                     thread, the parent map for zero slots, and the in-place
-//                     row copy (256-bit LDG/STG per 32-byte row, 8 in flight).
+//   C  k_rs_assign  : per slot tile: the slice of the surplus-parent list that
+//                     covers the tile's zero ranks (located through the rank
+//                     anchors) staged in shared memory, each staged parent writes
+//                     itself into the tile's rank table, every zero slot reads its
+//                     parent by rank; with 32-byte rows the in-place row copy is
+//                     fused in (256-bit LDG/STG, 4 rows in flight per thread).
 #include "smc_weights.cuh"
 
 using namespace smc;
@@ -302,11 +303,27 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         return;
     }
     const bool residual = is_residual(scheme);
-    // totals: striped, so every warp load is coalesced (integer sums are order independent)
+    // totals: striped, so every warp load is coalesced (integer sums are order independent);
+    // 8 tiles per thread per round, all loads issued before any is consumed (one round trip
+    // per round instead of one per tile)
+    constexpr int KS = 8;
     u128 tq = 0;
     uint64_t tqr = 0;
     int64_t tf = 0;
-    for (int64_t b = threadIdx.x; b < nt; b += SB) { tq += L.tile_q[b]; tqr += L.tile_qr[b]; tf += L.tile_f[b]; }
+    for (int64_t b0 = threadIdx.x; b0 < nt; b0 += (int64_t)KS * SB) {
+        u128 vq[KS];
+        uint64_t vr[KS];
+        int64_t vf[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t b = b0 + (int64_t)k * SB;
+            vq[k] = b < nt ? L.tile_q[b] : (u128)0;
+            vr[k] = residual && b < nt ? L.tile_qr[b] : 0;
+            vf[k] = residual && b < nt ? L.tile_f[b] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < KS; ++k) { tq += vq[k]; tqr += vr[k]; tf += vf[k]; }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         tq += shfl_xor_u128(tq, o);
@@ -377,7 +394,13 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
     auto val = [&](int64_t b) { return residual ? L.tile_qr[b] : (uint64_t)L.tile_q[b]; };
     uint64_t wsum = 0;
-    for (int64_t b = w0 + lane; b < w1; b += 32) wsum += val(b);
+    for (int64_t b0 = w0 + lane; b0 < w1; b0 += 32 * KS) {
+        uint64_t v[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) v[k] = b0 + 32 * k < w1 ? val(b0 + 32 * k) : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) wsum += v[k];
+    }
     wsum = warp_sum(wsum);
     if (lane == 0) sm64[warp] = wsum;
     __syncthreads();
@@ -388,12 +411,20 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     }
     __syncthreads();
     uint64_t carry = sm64[warp] + s_off;
-    for (int64_t b0 = w0; b0 < w1; b0 += 32) {
-        const int64_t b = b0 + lane;
-        const uint64_t v = b < w1 ? val(b) : 0;
-        const uint64_t inc = warp_inclusive_sum(v);
-        if (b < w1) L.tile_pre[b] = carry + inc - v;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
+    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {  // KS warp-rows in flight, then scanned in order
+        uint64_t v[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t b = c0 + 32 * k + lane;
+            v[k] = b < w1 ? val(b) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t b = c0 + 32 * k + lane;
+            const uint64_t inc = warp_inclusive_sum(v[k]);
+            if (b < w1) L.tile_pre[b] = carry + inc - v[k];
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
     }
 }
 
@@ -752,11 +783,14 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
     const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
     // (Z, P) as two 32-bit halves of one u64 (totals < 2^31 never carry), S as u64
     auto zp = [&](uint64_t v) { return ((uint64_t)unz(v) << 32) | unp(v); };
+    constexpr int KS = 8;  // warp-rows of tiles in flight per round (one round trip per round)
     uint64_t a = 0, bs = 0;
-    for (int64_t t = w0 + lane; t < w1; t += 32) {
-        const uint64_t v = L.tile_zsp[t];
-        a += zp(v);
-        bs += uns(v);
+    for (int64_t t0 = w0 + lane; t0 < w1; t0 += 32 * KS) {
+        uint64_t v[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) v[k] = t0 + 32 * k < w1 ? L.tile_zsp[t0 + 32 * k] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) { a += zp(v[k]); bs += uns(v[k]); }
     }
     a = warp_sum(a);
     bs = warp_sum(bs);
@@ -781,18 +815,23 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
     }
     __syncthreads();
     uint64_t ca = s_zp[warp], cs = s_s[warp];
-    for (int64_t t0 = w0; t0 < w1; t0 += 32) {
-        const int64_t t = t0 + lane;
-        const uint64_t v = t < w1 ? L.tile_zsp[t] : 0;
-        const uint64_t x = zp(v), y = uns(v);
-        const uint64_t ix = warp_inclusive_sum(x), iy = warp_inclusive_sum(y);
-        if (t < w1) {
-            const uint64_t ex = ca + ix - x, ey = cs + iy - y;
-            L.tile_excl[t] = make_uint4((uint32_t)(ex >> 32), (uint32_t)ey, (uint32_t)ex, 0);
-            L.tile_z0[t] = (int32_t)(ex >> 32);
+    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
+        uint64_t vv[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.tile_zsp[c0 + 32 * k + lane] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t t = c0 + 32 * k + lane;
+            const uint64_t x = zp(vv[k]), y = uns(vv[k]);
+            const uint64_t ix = warp_inclusive_sum(x), iy = warp_inclusive_sum(y);
+            if (t < w1) {
+                const uint64_t ex = ca + ix - x, ey = cs + iy - y;
+                L.tile_excl[t] = make_uint4((uint32_t)(ex >> 32), (uint32_t)ey, (uint32_t)ex, 0);
+                L.tile_z0[t] = (int32_t)(ex >> 32);
+            }
+            ca += __shfl_sync(0xffffffffu, ix, 31);
+            cs += __shfl_sync(0xffffffffu, iy, 31);
         }
-        ca += __shfl_sync(0xffffffffu, ix, 31);
-        cs += __shfl_sync(0xffffffffu, iy, 31);
     }
 }
 
@@ -1249,11 +1288,10 @@ __global__ void k_rs_pack(const char *__restrict__ rows, int64_t row_bytes, int6
 }
 
 // In-place copy of every zero-count row from its parent.
-// Sources (count >= 2) and destinations (count 0) are disjoint, so
-// no snapshot is needed.  One slot per thread keeps occupancy (and so the
-// number of 32-byte row loads in flight) at the maximum.
+// Rows other than 32 bytes (32-byte rows are copied inside pass C).  Sources (count >= 2)
+// and destinations (count 0) are disjoint, so no snapshot is needed.  One slot
+// per thread keeps occupancy (and so the number of row loads in flight) at the maximum.
 constexpr int CB = 512;
-template <int RB>
 __global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ parents, char *rows, int64_t row_bytes,
                                                 int64_t n, Layout L)
 {
@@ -1262,14 +1300,7 @@ __global__ void __launch_bounds__(CB) k_rs_copy(const int32_t *__restrict__ pare
     const int64_t j = (int64_t)blockIdx.x * CB + threadIdx.x;
     if (j >= n) return;
     const int32_t p = __ldg(parents + j);
-    if (p == j) return;
-    if (RB == 32) {
-        double4 v;
-        ld256((const double *)(rows + (int64_t)p * 32), v);
-        st256((double *)(rows + j * 32), v);
-    } else {
-        copy_row(rows, row_bytes, j, p);
-    }
+    if (p != j) copy_row(rows, row_bytes, j, p);
 }
 
 __global__ void k_rs_export_zsp(Layout L, uint32_t *out)
@@ -1384,7 +1415,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         } else {
             smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
             if (rows)  // other row sizes: one moved row per thread, full occupancy
-                smc_launch(k_rs_copy<0>, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, row_bytes, n, L);
+                smc_launch(k_rs_copy, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, row_bytes, n, L);
         }
     }
     return smc_check_launch("smc_resample");

@@ -214,3 +214,25 @@ def test_multichunk_tile_scans_bit_exact(scheme):
     assert np.array_equal(par, pref)
     if x is not None:
         assert np.array_equal(xg.cpu().numpy(), x[pref])
+
+
+def test_config4_size_2e28_systematic_bit_exact():
+    """BASELINE config 4's whole filter size on one GPU, N = 2^28: systematic counts and the
+    parent map bit-exact with the oracle (the largest size the int32 parent vector is used at
+    in the benchmarks), plus the size-independent invariants."""
+    from paper_1306_5583_b200 import replication_to_parents, resample
+    n = 1 << 28
+    lw = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(28)) * 2.0
+    w = torch.exp(lw - torch.logsumexp(lw, 0))
+    w = w / w.sum()
+    u = torch.tensor([0.3141592653589793], dtype=torch.float64, device="cuda")
+    counts = resample("systematic", w, u=u)
+    parents = replication_to_parents(counts)
+    c = counts.cpu().numpy()
+    p = parents.cpu().numpy()
+    assert c.sum() == n and c.min() >= 0
+    surv = c >= 1
+    assert np.array_equal(p[surv], np.nonzero(surv)[0])
+    ref, _ = O.resample_counts("systematic", w.cpu().numpy(), u=u.cpu().numpy())
+    assert np.array_equal(c, ref)
+    assert np.array_equal(p, O.replication_to_parents(ref))
