@@ -441,21 +441,23 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     }
     if (L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
-    const int64_t base = (int64_t)blockIdx.x * TILE + (int64_t)threadIdx.x * RI;  // blocked
+    __shared__ uint64_t s_io[tile_smem_elems<uint64_t, RT, RI>()];
+    const int64_t tbase = (int64_t)blockIdx.x * TILE;
     uint64_t v[RI];
+    // q (or q') from pass A, scanned in place into Q: blocked per thread, moved as whole
+    // 32-byte sectors (256-bit loads / stores on full tiles, a shared-memory transpose otherwise)
+    load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, v, s_io, 0ull);
     uint64_t loc = 0;
 #pragma unroll
-    for (int j = 0; j < RI; ++j) {  // q (or q') from pass A, scanned in place into Q
-        v[j] = base + j < n ? L.qfull[base + j] : 0;
-        loc += v[j];
-    }
+    for (int j = 0; j < RI; ++j) loc += v[j];
     uint64_t tot;
     uint64_t run = L.tile_pre[blockIdx.x] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         run += v[j];
-        if (base + j < n) L.qfull[base + j] = run;
+        v[j] = run;
     }
+    store_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, v, s_io);
 }
 
 // Multinomial positions P_k = floor(m_k Tm / 2^53) (A.3) are iid over the whole CDF,
@@ -552,8 +554,15 @@ __global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layo
     const int64_t nt = nbins;
     const int64_t C = (nt + NW - 1) / NW;
     const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
+    constexpr int KS = 8;  // warp-rows of bins in flight per round (one round trip per round)
     uint64_t wsum = 0;
-    for (int64_t b = w0 + lane; b < w1; b += 32) wsum += L.mn_cnt[b];
+    for (int64_t b0 = w0 + lane; b0 < w1; b0 += 32 * KS) {
+        uint32_t v[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) v[k] = b0 + 32 * k < w1 ? L.mn_cnt[b0 + 32 * k] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) wsum += v[k];
+    }
     wsum = warp_sum(wsum);
     if (lane == 0) sm64[warp] = wsum;
     __syncthreads();
@@ -564,15 +573,20 @@ __global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layo
     }
     __syncthreads();
     uint64_t carry = sm64[warp];
-    for (int64_t b0 = w0; b0 < w1; b0 += 32) {
-        const int64_t b = b0 + lane;
-        const uint64_t v = b < w1 ? L.mn_cnt[b] : 0;
-        const uint64_t inc = warp_inclusive_sum(v);
-        if (b < w1) {
-            L.mn_off[b] = (uint32_t)(carry + inc - v);
-            L.mn_fill[b] = 0;
+    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
+        uint64_t vv[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.mn_cnt[c0 + 32 * k + lane] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t b = c0 + 32 * k + lane;
+            const uint64_t inc = warp_inclusive_sum(vv[k]);
+            if (b < w1) {
+                L.mn_off[b] = (uint32_t)(carry + inc - vv[k]);
+                L.mn_fill[b] = 0;
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
         }
-        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (warp == NW - 1 && lane == 31) {
         L.mn_off[nt] = (uint32_t)carry;  // total positions in this shard
