@@ -35,7 +35,7 @@ UNIT = "particle-steps/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)  # ~0.3 s timed: several clock samples
+    ap.add_argument("--steps", type=int, default=600)  # ~0.55 s timed: several clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--particles", "--n", dest="n", type=int, default=None,
@@ -84,24 +84,30 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        # one persistent nvidia-smi sampling every 100 ms (the profiling recipe's clocks line)
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        for line in self._p.stdout:
+            if self._stop.is_set():
+                break
+            if line.strip():
+                self.rows.append([c.strip() for c in line.split(",")])
 
     def __enter__(self):
+        self._p = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.15)  # the first sample lands before the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
+        if self._p is not None:
+            self._p.terminate()
         self._t.join(timeout=10)
 
     def summary(self):
