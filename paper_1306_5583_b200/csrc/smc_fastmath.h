@@ -93,8 +93,9 @@ SMC_HD const LogEntry &log_entry(int i)
     return kLogTab[i];
 }
 
-// Natural log of a positive normal finite double (precondition; no check).
-SMC_HD double log_core(double x)
+// Natural log of a positive normal finite double (precondition; no check).  `tab`: an
+// optional shared-memory copy of kLogTab (kernels that stage it), else the global table.
+SMC_HD double log_core(double x, const LogEntry *tab = nullptr)
 {
     const uint64_t ix = bits(x);
     const uint64_t OFF = 0x3fe6000000000000ull;
@@ -103,7 +104,8 @@ SMC_HD double log_core(double x)
     const int64_t k = (int64_t)tmp >> 52;
     const double z = from_bits(ix - (tmp & (0xfffull << 52)));
 #ifdef __CUDA_ARCH__
-    const double2 e = __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]));
+    const double2 e = tab ? reinterpret_cast<const double2 *>(tab)[i]
+                          : __ldg(reinterpret_cast<const double2 *>(&kLogTab[i]));
     const uint64_t w1 = (uint64_t)__double_as_longlong(e.y);
     const double lhi = e.x, invc = (double)__uint_as_float((uint32_t)w1), llo = (double)__uint_as_float((uint32_t)(w1 >> 32));
 #else
@@ -212,7 +214,7 @@ SMC_TABLE CosPoly kCosPoly[4] = {
 #undef SMC_SIN_Q
 SMC_CONSTANT double kCosK[4] = {0x1.45f306dc9c883p-1, 0x1.921fb54442d18p+0, 0x1.1a62633145c07p-54, 0.0};
 
-SMC_HD double cos_bm(double x)
+SMC_HD double cos_bm(double x, const CosPoly *tab = nullptr)  // tab: optional shared-memory copy
 {
     const double SH = 0x1.8p52;
     const double kd = fma_(x, kCosK[0], SH);  // x 2/pi rounded to an integer
@@ -221,8 +223,14 @@ SMC_HD double cos_bm(double x)
     const double r = fma_(-jd, kCosK[2], fma_(-jd, kCosK[1], x));
     const double z = r * r;
 #ifdef __CUDA_ARCH__
-    const double2 *t = reinterpret_cast<const double2 *>(&kCosPoly[j & 3]);
-    const double2 a = __ldg(t), q01 = __ldg(t + 1), q23 = __ldg(t + 2), q45 = __ldg(t + 3), q67 = __ldg(t + 4);
+    double2 a, q01, q23, q45, q67;
+    if (tab) {
+        const double2 *t = reinterpret_cast<const double2 *>(&tab[j & 3]);
+        a = t[0], q01 = t[1], q23 = t[2], q45 = t[3], q67 = t[4];
+    } else {
+        const double2 *t = reinterpret_cast<const double2 *>(&kCosPoly[j & 3]);
+        a = __ldg(t), q01 = __ldg(t + 1), q23 = __ldg(t + 2), q45 = __ldg(t + 3), q67 = __ldg(t + 4);
+    }
 #else
     const CosPoly &e = kCosPoly[j & 3];
     const struct { double x, y; } a{e.a0, e.a1}, q01{e.q[0], e.q[1]}, q23{e.q[2], e.q[3]}, q45{e.q[4], e.q[5]},

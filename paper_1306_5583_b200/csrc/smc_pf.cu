@@ -58,7 +58,7 @@ __device__ __noinline__ double log_sum_cold(double ax, double ay)
     return smc_fm::log(ax) + smc_fm::log(ay);
 }
 
-SMC_DEV double cv_llh(double xp, double yp, double xo, double yo)
+SMC_DEV double cv_llh(double xp, double yp, double xo, double yo, const smc_fm::LogEntry *logtab = nullptr)
 {
     const double scale = 10;
     const double nu = 10;
@@ -67,7 +67,7 @@ SMC_DEV double cv_llh(double xp, double yp, double xo, double yo)
     const double ax = 1 + div_nu(rx * rx);  // 1 + rx^2 / nu
     const double ay = 1 + div_nu(ry * ry);
     const double p = ax * ay;
-    const double s = p < INFINITY ? smc_fm::log_core(p) : log_sum_cold(ax, ay);  // p >= 1
+    const double s = p < INFINITY ? smc_fm::log_core(p, logtab) : log_sum_cold(ax, ay);  // p >= 1
     return -0.5 * (nu + 1) * s;
 }
 
@@ -118,6 +118,24 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // paid once per PPT particles.  The body runs in a non-unrolled loop (code size:
 // the move is ~2.7k SASS); each particle's new log-weight parks in shared memory
 // until the block max is known.
+// The fast-math tables (log 2 KB, cos 320 B, exp 2 KB) staged in shared memory once per
+// block: 32-bit shared addressing instead of a 64-bit global address (constant-bank base +
+// IMAD.WIDE on the FMA pipe, which the Philox multiplies saturate) per lookup.
+struct PfTabs {
+    smc_fm::LogEntry log[128];
+    smc_fm::ExpEntry exp[128];
+    smc_fm::CosPoly cos[4];
+};
+SMC_DEV void stage_tabs(PfTabs &t)
+{
+    for (int k = threadIdx.x; k < 128; k += PB) {
+        t.log[k] = smc_fm::kLogTab[k];
+        t.exp[k] = smc_fm::kExpTab[k];
+    }
+    if (threadIdx.x < 4) t.cos[threadIdx.x] = smc_fm::kCosPoly[threadIdx.x];
+    __syncthreads();
+}
+
 template <bool MON, int PPT>
 __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
@@ -126,6 +144,8 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
                                                    PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
+    __shared__ PfTabs tabs;
+    stage_tabs(tabs);  // constant data: staged before the dependency wait
     SMC_PDL_WAIT();
     __shared__ double s_v[PPT][PB];
     const int64_t base = (int64_t)blockIdx.x * (PB * PPT) + threadIdx.x;
@@ -160,21 +180,21 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             double x0, x1, x2, x3;
             ld_row(x_in + 4 * src, x0, x1, x2, x3);
             if (MON) {
-                const double w = nl.eq ? w_equal : smc_fm::exp(prev, smc_fm::kExpTab);  // 1 / N_total after a resample
+                const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);  // 1 / N_total after a resample
                 h0 += w * x0;
                 h1 += w * x1;
             }
             const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
             double z[4];
-            normals_at(c, si, key, z);
+            normals_at(c, si, key, z, FmTabs{tabs.log, tabs.cos});
             x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
             x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
             x2 = x2 + (0.0 + k.sd_vel * z[2]);
             x3 = x3 + (0.0 + k.sd_vel * z[3]);
             ctrs[i] = c + 8;
             st_row(x_out + 4 * i, x0, x1, x2, x3);
-            const double incw = cv_llh(x0, x1, xo, yo);
+            const double incw = cv_llh(x0, x1, xo, yo, tabs.log);
             if (incw_out) incw_out[i] = incw;
             v = prev + incw;  // add_log_weight(incw)
             if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
@@ -196,7 +216,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
-        const double e = smc_fm::exp(s_v[q][threadIdx.x] - bm, smc_fm::kExpTab);  // -inf -> 0
+        const double e = smc_fm::exp(s_v[q][threadIdx.x] - bm, tabs.exp);  // -inf -> 0
         s1 += e;
         s2 += e * e;
     }

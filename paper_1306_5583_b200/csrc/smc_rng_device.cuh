@@ -87,13 +87,19 @@ SMC_DEV double u01_at(uint64_t ctr, uint64_t stream, const K &key)
 // ulp, 99.6 % bit-identical to glibc), the radius root is sqrt_bm (bit-identical to
 // IEEE sqrt on these inputs) and cos is cos_bm (<= 1.33 ulp, 83 % bit-identical to
 // glibc, never more than 1 ulp away from it): the whole normal is one basic block.
-SMC_DEV double box_muller53(uint64_t m1, uint64_t m2)
+// the fast-math tables a kernel staged in shared memory (null: the global tables)
+struct FmTabs {
+    const smc_fm::LogEntry *log = nullptr;
+    const smc_fm::CosPoly *cos = nullptr;
+};
+
+SMC_DEV double box_muller53(uint64_t m1, uint64_t m2, FmTabs tabs = FmTabs{})
 {
     // 1 - u1 = 1 - m1 2^-53 in [2^-53, 1] (exact, one FMA): a positive normal double, as
     // log_core requires; fl(2 pi u2) = fl((2 pi 2^-53) m2), the power-of-two scale being exact
     const double v1 = __fma_rn(-__ull2double_rn(m1), 1.0 / 9007199254740992.0, 1.0);
     const double x2 = __dmul_rn(__ull2double_rn(m2), (2.0 * 3.141592653589793) / 9007199254740992.0);
-    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(v1)) * smc_fm::cos_bm(x2);
+    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(v1, tabs.log)) * smc_fm::cos_bm(x2, tabs.cos);
 }
 
 template <class K>
@@ -106,13 +112,13 @@ SMC_DEV double normal_at(uint64_t ctr, uint64_t stream, const K &key)
 // block first (2 NZ independent integer chains the scheduler interleaves), then the
 // NZ Box-Muller transforms.  Bit-identical to NZ calls of normal_at.
 template <int NZ, class K>
-SMC_DEV void normals_at(uint64_t ctr, uint64_t stream, const K &key, double (&z)[NZ])
+SMC_DEV void normals_at(uint64_t ctr, uint64_t stream, const K &key, double (&z)[NZ], FmTabs tabs = FmTabs{})
 {
     uint64_t m[2 * NZ];
 #pragma unroll
     for (int j = 0; j < 2 * NZ; ++j) m[j] = draw53(ctr + (uint64_t)j, stream, key);
 #pragma unroll
-    for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1]);
+    for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], tabs);
 }
 
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the
