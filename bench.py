@@ -274,13 +274,18 @@ def run_b200(args):
     move_bytes = n * (32 + 32 + 8 + 8 + 8) + n * 8 * float(np.mean(1 - prev_rs))
     move_gbs = move_bytes / (phase["move"] * 1e-3) / 1e9
     # resample+copy (the metric's second half, SURVEY §8d config 5 at this N): smc_resample with the
-    # parent map AND the explicit in-place row copy on this run's own final weights, timed alone with
-    # CUDA events (inside the PF step the copy is folded into the next move's gather instead).
-    # Algorithmic bytes: W 8 R + counts 4 W + parents 4 W per particle + 64 B per moved 32-byte row.
-    # the weights right after the resample are equal: take one more move (no resample) so the
-    # benchmark resamples the PF's real pre-resample weight distribution
-    s.move_queue[0](s.iteration + 1, s.system)
-    rc = resample_copy_bench(P, s.system, args.scheme)
+    # parent map AND the explicit in-place row copy, timed alone with CUDA events (inside the PF step
+    # the copy is folded into the next move's gather instead).  Algorithmic bytes: W 8 R + counts 4 W
+    # + parents 4 W per particle + 64 B per moved 32-byte row.  The weights are the same whatever
+    # --steps is: a fresh filter (same seed and track) run for the paper's 100 observations, the last
+    # move taken without its resample -- the PF's real pre-resample weight distribution at t = 100.
+    s_rc = P.pf.make_sampler(n, args.scheme, 0.5, seed=1306, shard=shard)
+    s_rc.initialize(obs)
+    s_rc.iterate(98, check=False)
+    s_rc.move_queue[0](s_rc.iteration + 1, s_rc.system)
+    rc = resample_copy_bench(P, s_rc.system, args.scheme)
+    del s_rc
+    torch.cuda.empty_cache()
     frac_moved = rc["moved_frac"]
     dominant = max(("move", "resample", "monitor"), key=lambda k: phase.get(k, 0))
 
@@ -304,7 +309,7 @@ def run_b200(args):
                          "compute": compute_floor(n, phase["move"])},
             "resample_copy": {"achieved": rc["gbs"], "peak": peak, "unit": "GB/s", "frac": rc["gbs"] / peak,
                               "ms": rc["ms"], "algorithmic_bytes": rc["bytes"], "scheme": args.scheme,
-                              "weights": "the PF's pre-resample weights (one extra move after the run)",
+                              "weights": "the PF's pre-resample weights at t = 100 (fresh filter, same seed)",
                               "reps": rc["reps"],
                               "kernels": "k_rs_tiles, k_rs_scan, k_rs_counts, k_rs_zsp_scan, k_rs_ranks, "
                                          "k_rs_assign<copy fused>"},
