@@ -92,13 +92,19 @@ SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, i
             x[j] = __fma_rn(b[j], resid * resid, c[j]);
         }
         double m = x[0];
+        int im = 0;
 #pragma unroll
         // plain compare-select (x is finite or -inf; fmax's NaN handling measured 5 % slower)
-        for (int j = 1; j < R; ++j) m = x[j] > m ? x[j] : m;
+        for (int j = 1; j < R; ++j) {
+            im = x[j] > m ? j : im;
+            m = x[j] > m ? x[j] : m;
+        }
         if (m >= -700.0) {
-            double S = 0.0;
+            // the largest term is exp(0) = 1 exactly: only the R - 1 others need the exp
+            // (selected around the first maximum, in component order)
+            double S = 1.0;
 #pragma unroll
-            for (int j = 0; j < R; ++j) S += smc_fm::exp_nonpos(x[j] - m, tab);
+            for (int j = 0; j + 1 < R; ++j) S += smc_fm::exp_nonpos((j < im ? x[j] : x[j + 1]) - m, tab);
             msum += m;
             prod *= S;  // prod in [1, 2) times S in [1, R]: normal; peel the exponent off
             const uint64_t pb = smc_fm::bits(prod);
