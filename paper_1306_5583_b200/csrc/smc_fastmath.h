@@ -267,6 +267,18 @@ SMC_HD double sqrt_bm(double v)
     return fma_(d, 0.5 * y, s);
 }
 
+// a / 10 rounded to nearest, division-free (Markstein): q = a fl(1/10), the exact residual
+// a - 10 q by FMA, one correction.  Identical to the IEEE quotient for every a whose quotient
+// is normal (tests/test_fastmath.py; below that the PF's t-likelihood only meets it as
+// 1 + q = 1).  a = inf gives inf (the NaN of the correction is discarded), NaN stays NaN.
+SMC_HD double div10(double a)
+{
+    const double q = a * 0.1;
+    const double r = fma_(-q, 10.0, a);
+    const double q1 = fma_(r, 0.1, q);
+    return q1 != q1 ? q : q1;
+}
+
 // exp(x) for the GMM likelihood (smc_gmm.cu).  x = (128 m + j) ln2/128 + r with
 // |r| <= ln2/256; exp(r) - 1 by a degree-5 Taylor polynomial (truncation
 // < 2^-60); 2^(j/128) as hi + lo from kExpTab.  Subnormal results are scaled in

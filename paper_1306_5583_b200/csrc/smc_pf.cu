@@ -38,19 +38,6 @@ struct PfConst {
 // is taken as ONE log of the product (one fewer fp64 log per particle-step;
 // the two-log form only if the product overflows): agrees with the reference's
 // two logs to an absolute 2e-16 in the log-weight.
-// a / 10 rounded to nearest (nu = 10), division-free (Markstein): q = a fl(1/10),
-// the exact residual a - 10 q by FMA, one correction.  Identical to the IEEE
-// quotient for every a whose quotient is normal (host-checked on 4e8 inputs); below
-// that the quotient only ever meets 1 + q = 1.  a = inf gives inf (the NaN of the
-// correction is discarded), NaN stays NaN.
-SMC_DEV double div_nu(double a)
-{
-    const double q = a * 0.1;
-    const double r = __fma_rn(-q, 10.0, a);
-    const double q1 = __fma_rn(r, 0.1, q);
-    return isnan(q1) ? q : q1;
-}
-
 // the reference's two logs, for the (never seen in practice) overflowing product: out of line so
 // the libm fallback's code and registers stay out of the move loop
 __device__ __noinline__ double log_sum_cold(double ax, double ay)
@@ -64,8 +51,8 @@ SMC_DEV double cv_llh(double xp, double yp, double xo, double yo, const smc_fm::
     const double nu = 10;
     const double rx = scale * (xp - xo);
     const double ry = scale * (yp - yo);
-    const double ax = 1 + div_nu(rx * rx);  // 1 + rx^2 / nu
-    const double ay = 1 + div_nu(ry * ry);
+    const double ax = 1 + smc_fm::div10(rx * rx);  // 1 + rx^2 / nu (nu = 10)
+    const double ay = 1 + smc_fm::div10(ry * ry);
     const double p = ax * ay;
     const double s = p < INFINITY ? smc_fm::log_core(p, logtab) : log_sum_cold(ax, ay);  // p >= 1
     return -0.5 * (nu + 1) * s;

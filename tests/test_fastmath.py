@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_cos_bm, lib.fm_sqrt_bm):
+    for f in (lib.fm_log, lib.fm_cos, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_cos_bm, lib.fm_sqrt_bm, lib.fm_div10):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -216,3 +216,19 @@ def test_sqrt_bm(fm):
     assert a[-6] == 0.0
     assert np.max(np.abs(a - b) / np.spacing(np.maximum(b, 1e-300))) <= 1.0
     assert np.mean(a == b) > 0.999
+
+
+def test_div10_matches_ieee_division(fm):
+    """smc_fm::div10 (the t-likelihood's r^2 / nu, nu = 10): bit-identical to a / 10 for every
+    a whose quotient is normal -- random bit patterns over the whole exponent range and the
+    squared residuals the PF produces -- and inf / NaN behave as division does."""
+    rng = np.random.default_rng(15)
+    bitsv = rng.integers(0, 0x7FF0000000000000, 3_000_000, dtype=np.int64)
+    a = bitsv.view(np.float64)
+    a = a[a / 10.0 >= 2.0 ** -1022]
+    r = rng.normal(0, 30, 1_000_000)
+    a = np.concatenate([a, r * r, [0.0, 1.0, 10.0, 1e308, 1.7976931348623157e308, 2.0 ** -1018]])
+    got = fm("fm_div10", a)
+    np.testing.assert_array_equal(got, a / 10.0)
+    edge = fm("fm_div10", np.array([np.inf, np.nan]))
+    assert edge[0] == np.inf and np.isnan(edge[1])
