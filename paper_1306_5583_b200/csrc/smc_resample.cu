@@ -36,6 +36,9 @@ using namespace smc;
 namespace {
 
 constexpr int RT = 256;
+#ifndef RS_COUNTS_MINB
+#define RS_COUNTS_MINB 5  // pass B1 blocks per SM the register allocation must allow (same-box A/B: 5 > 6 > 4)
+#endif
 constexpr int RI = 8;
 constexpr int TILE = RT * RI;  // elements per tile (pass A/B) and ranks per tile (pass C)
 constexpr uint64_t T_LO = (1ull << 63) - (1ull << 43);
@@ -935,7 +938,7 @@ __global__ void __launch_bounds__(RT) k_rs_aggs(const int32_t *__restrict__ cin,
 // Pass B1: counts per particle.  Embarrassingly parallel (no inter-tile wait);
 // the counts go to `counts` (the caller's or the workspace's).
 template <bool RES, bool MULTI, bool SYS>  // scheme family, resolved at compile time
-__global__ void __launch_bounds__(RT) k_rs_counts(int scheme, WSrc src, int64_t n, double m_out, double rscale,
+__global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                   Key key, uint64_t stream, const double *__restrict__ u,
                                                   int32_t *__restrict__ counts, int ranks, Layout L)
 {
