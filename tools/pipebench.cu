@@ -22,6 +22,9 @@ __global__ void __launch_bounds__(256) k(double *out, uint32_t seed)
             if (F == 3) u[j] = u[j] * 0xD2511F53u + v[j];
             if (F == 4) u[j] = (u[j] ^ v[j]) ^ (u[j] >> 3);
             if (F == 5) f[j] = __fmaf_rn(f[j], 0.9999999f, 1e-7f);
+            if (F == 6) { d[j] += (double)(long long)(u[j] + v[j]); u[j] += 3; }            // I2F.F64.S64
+            if (F == 7) { d[j] += (double)(int)(u[j] + v[j]); u[j] += 3; }                  // I2F.F64.S32
+            if (F == 8) { d[j] += (double)((unsigned long long)u[j] << 21 | v[j]); u[j] += 3; }  // I2F.F64.U64
         }
     }
     double s = 0;
@@ -40,8 +43,9 @@ int main()
     int sms, clk;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    const char *names[] = {"DFMA", "DADD", "IMAD.WIDE+LOP3", "IMAD(lo)", "LOP3+SHF", "FFMA"};
-    for (int f = 0; f < 6; ++f) {
+    const char *names[] = {"DFMA", "DADD", "IMAD.WIDE+LOP3", "IMAD(lo)", "LOP3+SHF", "FFMA", "I2F.F64.S64+DADD",
+                           "I2F.F64.S32+DADD", "I2F.F64.U64+DADD"};
+    for (int f = 0; f < 9; ++f) {
         float best = 1e9f;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(a);
@@ -52,6 +56,9 @@ int main()
             case 3: k<3><<<n / 256, 256>>>(d, 7); break;
             case 4: k<4><<<n / 256, 256>>>(d, 7); break;
             case 5: k<5><<<n / 256, 256>>>(d, 7); break;
+            case 6: k<6><<<n / 256, 256>>>(d, 7); break;
+            case 7: k<7><<<n / 256, 256>>>(d, 7); break;
+            case 8: k<8><<<n / 256, 256>>>(d, 7); break;
             }
             cudaEventRecord(b);
             cudaEventSynchronize(b);
