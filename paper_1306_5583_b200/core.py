@@ -330,6 +330,8 @@ class Sampler:
     mcmc = add_mcmc
 
     def set_monitor(self, name, dim, eval_):
+        if int(dim) < 1:
+            raise ValueError("a monitor needs dimension m >= 1")  # SPEC.md:409 (empty monitor disallowed)
         if not isinstance(eval_, MonitorEval):
             eval_ = MonitorEval(eval_, dim)
         self.monitors[name] = MonitorRecord(name, dim, eval_)
