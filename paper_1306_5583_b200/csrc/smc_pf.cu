@@ -140,14 +140,20 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
     const NormLw nl = norm_of(st);
     const bool gathered = parents && (gate == nullptr || *gate != 0);
     const double xo = obs[0], yo = obs[1];
-    // software prefetch: the next particle's counter, parent index and old log-weight are
-    // requested before this particle's normals, so their latency hides behind the Philox work
+    // software prefetch: the next particle's counter and old log-weight are requested before
+    // this particle's normals, so their latency hides behind the Philox work
+    // the block's parent indices (PPT x PB, 4 bytes each) staged in shared memory up front with
+    // coalesced loads: each particle's gathered row load then needs no dependent global load
+    __shared__ int32_t s_src[PPT][PB];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const int64_t i = base + (int64_t)q * PB;
+        s_src[q][threadIdx.x] = gathered && i < n ? __ldg(parents + i) : (int32_t)i;
+    }
     uint64_t c_nx = 0;
-    int64_t src_nx = base;
     double lw_nx = 0.0;
     if (base < n) {
         c_nx = ctrs[base];
-        if (gathered) src_nx = __ldg(parents + base);
         if (nl.needs_raw()) lw_nx = lw_raw[base];
     }
 #pragma unroll kPfUnroll
@@ -155,11 +161,10 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         const int64_t i = base + (int64_t)q * PB;
         double v = -INFINITY;
         const uint64_t c = c_nx;
-        const int64_t src = src_nx;
+        const int64_t src = s_src[q][threadIdx.x];
         const double lw_prev = lw_nx;
         if (q + 1 < PPT && i + PB < n) {
             c_nx = ctrs[i + PB];
-            src_nx = gathered ? (int64_t)__ldg(parents + i + PB) : i + PB;
             if (nl.needs_raw()) lw_nx = lw_raw[i + PB];
         }
         if (i < n) {
