@@ -171,15 +171,15 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             const double prev = nl(lw_prev);  // normalized W_{t-1}; no read if equal
             double x0, x1, x2, x3;
             ld_row(x_in + 4 * src, x0, x1, x2, x3);
+            const uint64_t si = sbase + (uint64_t)i;
+            // PAPER.md:1310-1313, evaluation order pinned (SURVEY R17): x0 += (0 + sd*z) + delta*x2
+            double z[4];
+            normals_at(c, si, key, z, FmTabs{tabs.log, tabs.cos});  // the row load lands meanwhile
             if (MON) {
                 const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);  // 1 / N_total after a resample
                 h0 += w * x0;
                 h1 += w * x1;
             }
-            const uint64_t si = sbase + (uint64_t)i;
-            // PAPER.md:1310-1313, evaluation order pinned (SURVEY R17): x0 += (0 + sd*z) + delta*x2
-            double z[4];
-            normals_at(c, si, key, z, FmTabs{tabs.log, tabs.cos});
             x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
             x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
             x2 = x2 + (0.0 + k.sd_vel * z[2]);
