@@ -870,6 +870,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     __shared__ uint64_t sm[RT / 32 + 1];
     const int64_t b = blockIdx.x;
     int32_t c[RI];
+    const uint4 ex = __ldcg(&L.tile_excl[b]);  // issued before the counts' load and scan: its latency overlaps
     load_blocked<RT, RI, int32_t>(cin, b * TILE, n, c, s_c, 1);  // coalesced; pad: not zero, no surplus
     if (check) {  // caller-provided counts (replication_to_parents)
         bool bad = false;
@@ -887,7 +888,6 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     }
     uint64_t agg;
     const uint64_t tex = block_exclusive_sum<RT, uint64_t>(pack_zsp(0, tp, ts), sm, &agg);
-    const uint4 ex = __ldcg(&L.tile_excl[b]);
     uint32_t sr = ex.y + (uint32_t)uns(tex);
     uint32_t lp = unp(tex);  // tile-local surplus-parent index
     const int32_t base = (int32_t)(b * TILE) + (int32_t)threadIdx.x * RI;  // n < 2^31
@@ -960,6 +960,7 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;  // blocked: thread owns RI consecutive
     int32_t c[RI];
     const bool full = tbase + TILE <= n;  // no per-element bounds checks on full tiles
+    const uint64_t tpre = MULTI ? 0 : L.tile_pre[b];  // issued before the tile's loads and scan
     {
         uint64_t q[RI];
         int32_t f[RI];
@@ -1009,7 +1010,7 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
             for (int j = 0; j < RI; ++j) c[j] = (full || base + j < n) ? f[j] + h4[j] : 1;
         } else {
             uint64_t tot;
-            uint64_t X = L.tile_pre[b] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
+            uint64_t X = tpre + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
             StratCtx sc;
             sc.Tm = h->Tm;
             sc.M = h->M;
