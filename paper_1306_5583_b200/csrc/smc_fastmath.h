@@ -9,9 +9,9 @@
 //
 // log(x) = k ln2 + log(c_i) + log1p(r),  x = 2^k z,  z in [0.6875, 1.375),
 //          k ln2 + log(c_i) exact as a double (table on the 2^-42 grid of LN2_HI),
-//          r = z/c_i - 1 via one FMA (|r| <= 2^-7.5), c_i = 1 exactly around z = 1
-//          so that r = z - 1 is exact there (full relative accuracy near x = 1),
-//          log1p(r) - r by a degree-8 Taylor polynomial (truncation < 2^-59 |r|).
+//          r = z/c_i - 1 via one FMA (|r| <= 2^-10, 512 intervals), c_i = 1 exactly
+//          around z = 1 so that r = z - 1 is exact there (full relative accuracy near
+//          x = 1), log1p(r) - r by a degree-6 Taylor polynomial (truncation < 2^-63 |r|).
 // cos(x), 0 <= x < 8 (x = fl(2 pi u) in Box-Muller): Cody-Waite reduction by
 //          pi/2 in two 33-bit pieces + tail, then fdlibm's __kernel_cos/_sin
 //          polynomials on |r| <= pi/4.
@@ -49,7 +49,7 @@ struct alignas(16) LogEntry {
     float invc, logc_lo;  // 1/c in single precision (exact as a double), the |lo| <= 2^-43 rest
 };                        // 16 bytes: one 128-bit load per lookup
 
-SMC_TABLE LogEntry kLogTab[128] = {
+SMC_TABLE LogEntry kLogTab[512] = {
 #include "smc_logtab.inc"
 };
 
@@ -100,7 +100,7 @@ SMC_HD double log_core(double x, const LogEntry *tab = nullptr)
     const uint64_t ix = bits(x);
     const uint64_t OFF = 0x3fe6000000000000ull;
     const uint64_t tmp = ix - OFF;
-    const int i = (int)((tmp >> 45) & 127);
+    const int i = (int)((tmp >> 43) & 511);
     const int64_t k = (int64_t)tmp >> 52;
     const double z = from_bits(ix - (tmp & (0xfffull << 52)));
 #ifdef __CUDA_ARCH__
@@ -121,10 +121,8 @@ SMC_HD double log_core(double x, const LogEntry *tab = nullptr)
     const double hi = w + r;
     const double he = r - (hi - w);
     const double lo = he + fma_(kd, LN2_LO, llo);
-    // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 + r (-1/6 + r (1/7 - r/8))))))
-    double p = fma_(r, -0.125, kLogK[0]);
-    p = fma_(r, p, kLogK[1]);
-    p = fma_(r, p, kLogK[2]);
+    // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 - r/6)))), |r| <= 2^-10
+    double p = fma_(r, kLogK[1], kLogK[2]);
     p = fma_(r, p, -0.25);
     p = fma_(r, p, kLogK[3]);
     p = fma_(r, p, -0.5);

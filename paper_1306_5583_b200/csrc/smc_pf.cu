@@ -105,20 +105,18 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // paid once per PPT particles.  The body runs in a non-unrolled loop (code size:
 // the move is ~2.7k SASS); each particle's new log-weight parks in shared memory
 // until the block max is known.
-// The fast-math tables (log 2 KB, cos 320 B, exp 2 KB) staged in shared memory once per
+// The fast-math tables (log 8 KB, cos 320 B, exp 2 KB) staged in shared memory once per
 // block: 32-bit shared addressing instead of a 64-bit global address (constant-bank base +
 // IMAD.WIDE on the FMA pipe, which the Philox multiplies saturate) per lookup.
 struct PfTabs {
-    smc_fm::LogEntry log[128];
+    smc_fm::LogEntry log[512];
     smc_fm::ExpEntry exp[128];
     smc_fm::CosPoly cos[4];
 };
 SMC_DEV void stage_tabs(PfTabs &t)
 {
-    for (int k = threadIdx.x; k < 128; k += PB) {
-        t.log[k] = smc_fm::kLogTab[k];
-        t.exp[k] = smc_fm::kExpTab[k];
-    }
+    for (int k = threadIdx.x; k < 512; k += PB) t.log[k] = smc_fm::kLogTab[k];
+    for (int k = threadIdx.x; k < 128; k += PB) t.exp[k] = smc_fm::kExpTab[k];
     if (threadIdx.x < 4) t.cos[threadIdx.x] = smc_fm::kCosPoly[threadIdx.x];
     __syncthreads();
 }
