@@ -275,8 +275,10 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel (the fused move) and of resample+copy ----
     peak, peak_src = measured_peaks()
-    # X 32 R + 32 W, counter 8 R + 8 W, lw 8 W; + the parent index (4 R) after a resample, else lw 8 R
-    move_bytes = n * (32 + 32 + 8 + 8 + 8) + n * (4 * float(np.mean(prev_rs)) + 8 * float(np.mean(1 - prev_rs)))
+    # X 32 R + 32 W, lw 8 W; + the parent index (4 R) after a resample, else lw 8 R; the
+    # counters (8 R + 8 W) only when the streams are not at one uniform count (smc_pf_move_uniform)
+    uni = s.system.rng_set.uniform_count(s.system.size, 16) is not None
+    move_bytes = n * (32 + 32 + 8 + (0 if uni else 16)) + n * (4 * float(np.mean(prev_rs)) + 8 * float(np.mean(1 - prev_rs)))
     move_gbs = move_bytes / (phase["move"] * 1e-3) / 1e9
     # resample+copy (the metric's second half, SURVEY §8d config 5 at this N): smc_resample with the
     # parent map AND the explicit in-place row copy, timed alone with CUDA events (inside the PF step

@@ -250,6 +250,15 @@ int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int
  * sum_i W_i (x_i, y_i) of the state the move CONSUMES -- the previous
  * iteration's estimate -- reduced from registers the move
  * already holds, so the monitor costs no extra pass over the state. */
+/* smc_pf_move when every stream 0..n-1 is known to sit at the same draw count
+ * ctr (the host's RngStreamSet tracks this; SPEC.md:396 own-slot streams):
+ * same results bit for bit, but the counter array is neither read nor written
+ * (the host records the advanced count, ctr + 8) and the Philox blocks share
+ * their stream-only products.  SMC_EINVAL if lo32(ctr) + 15 would carry. */
+int smc_pf_move_uniform(const double *x_in, double *x, const int32_t *parents, const int32_t *gate,
+                        double *lw_raw, int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed,
+                        uint64_t ctr, const double *obs_t, smc_wstate *ws_state, double *incw_out,
+                        double *monitor_prev, double *partial_out, void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* example-gmm kernels -- replace gmm_init / gmm_move_smc / gmm_move_{mu,   */

@@ -96,6 +96,8 @@ _SIGS = {
     "smc_pf_init": ([_vp, _vp, _i64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_pf_move": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _i64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp],
                     C.c_int),
+    "smc_pf_move_uniform": ([_vp, _vp, _vp, _vp, _vp, _i64, _u64, _i64, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp,
+                             _sz, _vp], C.c_int),
 }
 EXPORTS = tuple(_SIGS)
 

@@ -454,6 +454,9 @@ class Sampler:
         pairs = n // 2
         if pairs == 0:
             return n
+        # the captured moves advance the counter array itself: bring it up to date (an eager
+        # move may have advanced the streams by a uniform count only) before capture / replay
+        sysm.rng_set.counters
         t0 = self.iteration
         self._row(t0 + 2 * pairs)  # history capacity first: the graph bakes its address in
         ncols = len(self._cols)

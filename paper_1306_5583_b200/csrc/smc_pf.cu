@@ -5,7 +5,8 @@
 // State: X is N x 4 f64 row-major, one 32-byte row per particle,
 // moved with one 256-bit load and one 256-bit store per thread.
 // Per particle-step HBM traffic: X 32 R + 32 W, lw 8 R (skipped after a
-// resample: equal weights) + 8 W, counter 8 R + 8 W  =  96 B.
+// resample: equal weights) + 8 W  =  80 B, + counter 8 R + 8 W when the
+// streams are not all at one count (smc_pf_move vs smc_pf_move_uniform).
 #include "smc_weights.cuh"
 
 using namespace smc;
@@ -121,12 +122,16 @@ SMC_DEV void stage_tabs(PfTabs &t)
     __syncthreads();
 }
 
-template <bool MON, int PPT>
+// UC: every particle's stream at the same draw count ctr_u (no carry over its 8 draws; the
+// host tracks this, rng.py): the counter array is neither read nor written (16 B per
+// particle-step less traffic) and the Philox blocks use normals_uniform (17 multiplies per
+// draw instead of 20).
+template <bool MON, int PPT, bool UC>
 __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
                                                    const int32_t *__restrict__ parents, const int32_t *gate,
                                                    double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
-                                                   double w_equal, const KeySched key, uint64_t *__restrict__ ctrs, const double *__restrict__ obs,
-                                                   PfConst k, smc_wstate *st, double *__restrict__ incw_out,
+                                                   double w_equal, const KeySched key, uint64_t *__restrict__ ctrs, const UniformCtr ctr_u,
+                                                   const double *__restrict__ obs, PfConst k, smc_wstate *st, double *__restrict__ incw_out,
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
     __shared__ PfTabs tabs;
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
     uint64_t c_nx = 0;
     double lw_nx = 0.0;
     if (base < n) {
-        c_nx = ctrs[base];
+        if (!UC) c_nx = ctrs[base];
         if (nl.needs_raw()) lw_nx = lw_raw[base];
     }
 #pragma unroll kPfUnroll
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         const int64_t src = s_src[q][threadIdx.x];
         const double lw_prev = lw_nx;
         if (q + 1 < PPT && i + PB < n) {
-            c_nx = ctrs[i + PB];
+            if (!UC) c_nx = ctrs[i + PB];
             if (nl.needs_raw()) lw_nx = lw_raw[i + PB];
         }
         if (i < n) {
@@ -172,7 +177,10 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2
             double z[4];
-            normals_at(c, si, key, z, FmTabs{tabs.log, tabs.cos});  // the row load lands meanwhile
+            if (UC)
+                normals_uniform(ctr_u, si, key, z, FmTabs{tabs.log, tabs.cos});
+            else
+                normals_at(c, si, key, z, FmTabs{tabs.log, tabs.cos});  // the row load lands meanwhile
             if (MON) {
                 const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);  // 1 / N_total after a resample
                 h0 += w * x0;
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
             x2 = x2 + (0.0 + k.sd_vel * z[2]);
             x3 = x3 + (0.0 + k.sd_vel * z[3]);
-            ctrs[i] = c + 8;
+            if (!UC) ctrs[i] = c + 8;
             st_row(x_out + 4 * i, x0, x1, x2, x3);
             const double incw = cv_llh(x0, x1, xo, yo, tabs.log);
             if (incw_out) incw_out[i] = incw;
@@ -288,17 +296,20 @@ extern "C" int smc_pf_init(double *x, double *lw_raw, int64_t n, uint64_t stream
     return smc_check_launch("smc_pf_init");
 }
 
-extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
-                           int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed, uint64_t *ctrs,
-                           const double *obs_t, smc_wstate *st, double *incw_out, double *monitor_prev,
-                           double *partial_out, void *ws, size_t ws_bytes, void *stream)
+static int pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
+                   int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed, uint64_t *ctrs, const uint64_t *ctr_u,
+                   const double *obs_t, smc_wstate *st, double *incw_out, double *monitor_prev, double *partial_out,
+                   void *ws, size_t ws_bytes, void *stream, const char *who)
 {
-    int rc = pf_check(x, lw_raw, n, ctrs, obs_t, st, ws, ws_bytes, "smc_pf_move");
+    uint64_t dummy = 0;
+    int rc = pf_check(x, lw_raw, n, ctr_u ? &dummy : ctrs, obs_t, st, ws, ws_bytes, who);
     if (rc) return rc;
+    if (ctr_u && (uint32_t)*ctr_u > 0xFFFFFFFFu - 15u)
+        return smc_set_error(SMC_EINVAL, "%s: uniform counter would carry into its high word", who);
     if (!x_in) x_in = x;
-    if ((uintptr_t)x_in & 31) return smc_set_error(SMC_EINVAL, "smc_pf_move: x_in must be 32-byte aligned");
+    if ((uintptr_t)x_in & 31) return smc_set_error(SMC_EINVAL, "%s: x_in must be 32-byte aligned", who);
     if (parents && x_in == x)
-        return smc_set_error(SMC_EINVAL, "smc_pf_move: a gathering move needs distinct in/out state buffers");
+        return smc_set_error(SMC_EINVAL, "%s: a gathering move needs distinct in/out state buffers", who);
     cudaStream_t s = (cudaStream_t)stream;
     // PF_PPT particles per thread only while the grid still gives every SM >= 4 blocks;
     // below that (e.g. config 1, N = 10^4) one particle per thread spreads the latency
@@ -309,9 +320,16 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
     void *scratch = pf_scratch(ws, nb);
     const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
-#define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                         \
-    smc_launch(k_pf_move<MONV, PPTV>, nb, PB, 0, s, x_in, x, parents, gate, lw_raw, n, stream_base, w_eq, key, ctrs, obs_t, \
-                                            pf_constants(), st, incw_out, parts, MONP)
+    const UniformCtr cu = make_uniform_ctr(ctr_u ? *ctr_u : 0);
+#define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                          \
+    do {                                                                                                       \
+        if (ctr_u)                                                                                             \
+            smc_launch(k_pf_move<MONV, PPTV, true>, nb, PB, 0, s, x_in, x, parents, gate, lw_raw, n, stream_base, \
+                       w_eq, key, ctrs, cu, obs_t, pf_constants(), st, incw_out, parts, MONP);                \
+        else                                                                                                   \
+            smc_launch(k_pf_move<MONV, PPTV, false>, nb, PB, 0, s, x_in, x, parents, gate, lw_raw, n, stream_base, \
+                       w_eq, key, ctrs, cu, obs_t, pf_constants(), st, incw_out, parts, MONP);                \
+    } while (0)
     if (monitor_prev) {
         if (many) SMC_PF_MOVE(true, PF_PPT, mon); else SMC_PF_MOVE(true, 1, mon);
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, mon, monitor_prev, partial_out);
@@ -320,5 +338,23 @@ extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents
         smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     }
 #undef SMC_PF_MOVE
-    return smc_check_launch("smc_pf_move");
+    return smc_check_launch(who);
+}
+
+extern "C" int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int32_t *gate, double *lw_raw,
+                           int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed, uint64_t *ctrs,
+                           const double *obs_t, smc_wstate *st, double *incw_out, double *monitor_prev,
+                           double *partial_out, void *ws, size_t ws_bytes, void *stream)
+{
+    return pf_move(x_in, x, parents, gate, lw_raw, n, stream_base, n_total, seed, ctrs, nullptr, obs_t, st, incw_out,
+                   monitor_prev, partial_out, ws, ws_bytes, stream, "smc_pf_move");
+}
+
+extern "C" int smc_pf_move_uniform(const double *x_in, double *x, const int32_t *parents, const int32_t *gate,
+                                   double *lw_raw, int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed,
+                                   uint64_t ctr, const double *obs_t, smc_wstate *st, double *incw_out,
+                                   double *monitor_prev, double *partial_out, void *ws, size_t ws_bytes, void *stream)
+{
+    return pf_move(x_in, x, parents, gate, lw_raw, n, stream_base, n_total, seed, nullptr, &ctr, obs_t, st, incw_out,
+                   monitor_prev, partial_out, ws, ws_bytes, stream, "smc_pf_move_uniform");
 }

@@ -121,6 +121,66 @@ SMC_DEV void normals_at(uint64_t ctr, uint64_t stream, const K &key, double (&z)
     for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], tabs);
 }
 
+// Rounds R0..9 of philox10 (R0 = 0: the whole block).
+template <int R0, class K>
+SMC_DEV uint4 philox_rounds(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const K &key)
+{
+#pragma unroll
+    for (int r = R0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(PHILOX_M0, c0), lo0 = PHILOX_M0 * c0;
+        const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ key.r0(r);
+        const uint32_t n2 = hi0 ^ c3 ^ key.r1(r);
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// Every stream at the same draw count ctr with no carry into its high word over the next
+// 16 draws (lo32(ctr) <= 2^32 - 16; the host checks): the round-1 M0 products of draw j,
+// M0 * (lo32(ctr) + j), are the same for every stream and come precomputed from the host
+// (a kernel parameter: constant-bank operands).  Per stream, round 1's M1 product and
+// round 2's M0 product are then common to all of its draws, so each draw costs 17
+// multiplies instead of 20.
+struct UniformCtr {
+    uint32_t hi0[16], lo0[16];  // umulhi / mul of M0 by lo32(ctr) + j
+    uint32_t c1;                // hi32(ctr)
+};
+
+#ifndef __CUDACC_RTC__
+inline UniformCtr make_uniform_ctr(uint64_t ctr)
+{
+    UniformCtr u;
+    for (int j = 0; j < 16; ++j) {
+        const uint64_t p = (uint64_t)PHILOX_M0 * (uint32_t)((uint32_t)ctr + (uint32_t)j);
+        u.hi0[j] = (uint32_t)(p >> 32);
+        u.lo0[j] = (uint32_t)p;
+    }
+    u.c1 = (uint32_t)(ctr >> 32);
+    return u;
+}
+#endif
+
+// normals_at(ctr, stream, ...) for the counter `u` describes: bit-identical.
+template <int NZ, class K>
+SMC_DEV void normals_uniform(const UniformCtr &u, uint64_t stream, const K &key, double (&z)[NZ],
+                             FmTabs tabs = FmTabs{})
+{
+    static_assert(2 * NZ <= 16, "UniformCtr holds 16 draws");
+    const uint32_t c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;  // round 1, every draw
+    const uint32_t n0 = hi1 ^ u.c1 ^ key.r0(0);
+    const uint32_t x3 = c3 ^ key.r1(0);
+    uint64_t m[2 * NZ];
+#pragma unroll
+    for (int j = 0; j < 2 * NZ; ++j) {
+        const uint4 w = philox_rounds<1>(n0, lo1, u.hi0[j] ^ x3, u.lo0[j], key);
+        m[j] = ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
+    }
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], tabs);
+}
+
 // rng.py:94-117: Marsaglia-Tsang (+ boost below shape 1); advances *ctr by the
 // variable number of draws it consumes.
 template <class K>

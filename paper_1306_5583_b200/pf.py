@@ -82,9 +82,13 @@ def cv_init(system, param=None):
     w = system.weight_set
     v.pending = None  # the prior draw overwrites every row
     shard = system.shard
-    _abi.call("smc_pf_init", _abi.ptr(v.raw), _abi.ptr(w.lw_raw), n, system.stream_base, system.rng_set.seed,
-              _abi.ptr(system.rng_set.counters), v.obs_ptr(0), w.state_ptr,
+    rs = system.rng_set
+    u = rs.uniform_count(n, 0)
+    _abi.call("smc_pf_init", _abi.ptr(v.raw), _abi.ptr(w.lw_raw), n, system.stream_base, rs.seed,
+              _abi.ptr(rs.counters), v.obs_ptr(0), w.state_ptr,
               None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
+    if u is not None:  # every particle stream drew 8: still uniform (and written)
+        rs.advance_uniform(n, (u + 8) % (1 << 64), True)
     if shard is not None:  # global normalization: allgather the shard partials, combine in rank order
         shard.combine(w, 0, True)  # SMC_W_SET_LOG
     return None  # acceptance "bares no meaning"
@@ -98,16 +102,23 @@ def _cv_move_kernel(iter_, system):
     # a pending fused "pos" monitor of the previous iteration is reduced by this launch
     mon = system.take_pending_monitor("pos")
     shard = system.shard
-    common = (_abi.ptr(w.lw_raw), n, system.stream_base, system.n_total, system.rng_set.seed,
-              _abi.ptr(system.rng_set.counters), v.obs_ptr(iter_), w.state_ptr, None, mon,
-              None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
+    rs = system.rng_set
+    # every particle stream at one draw count (the PF's own streams advance in lockstep):
+    # the kernel takes the count as a scalar and leaves the counter array alone
+    u0 = rs.uniform_count(n, 0)
+    u = rs.uniform_count(n, 16)  # the kernel's precomputed table covers 16 draws without a carry
+    fn, ctr = ("smc_pf_move", _abi.ptr(rs.counters)) if u is None else ("smc_pf_move_uniform", u)
+    common = (_abi.ptr(w.lw_raw), n, system.stream_base, system.n_total, rs.seed, ctr, v.obs_ptr(iter_),
+              w.state_ptr, None, mon, None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
     if v.pending is not None:  # fold the last resample's copy into this move (double buffer)
         parents, gate = v.pending
         v.pending = None
-        _abi.call("smc_pf_move", _abi.ptr(v.raw), _abi.ptr(v.alt()), _abi.ptr(parents), gate, *common)
+        _abi.call(fn, _abi.ptr(v.raw), _abi.ptr(v.alt()), _abi.ptr(parents), gate, *common)
         v.swap()
     else:
-        _abi.call("smc_pf_move", None, _abi.ptr(v.raw), None, None, *common)
+        _abi.call(fn, None, _abi.ptr(v.raw), None, None, *common)
+    if u0 is not None:  # every particle stream drew 8 (the array written iff it was passed)
+        rs.advance_uniform(n, (u0 + 8) % (1 << 64), u is None)
     if shard is not None:  # global add_log_weight + the fused monitor of the previous iteration
         shard.combine(w, 1, True, mon)  # SMC_W_ADD_LOG
     return None

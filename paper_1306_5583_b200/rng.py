@@ -45,7 +45,41 @@ class RngStreamSet:
         self._k0 = seed & 0xFFFFFFFF
         self._k1 = seed >> 32
         self.device = torch.device(device)
-        self.counters = torch.zeros(size, dtype=torch.int64, device=self.device)  # uint64 bit pattern
+        self._ctr = torch.zeros(size, dtype=torch.int64, device=self.device)  # uint64 bit pattern
+        # Uniform-count knowledge: streams [0, _u_n) all sit at draw count _u_val; when
+        # _u_stale the device array lags (a uniform-counter move advanced them without
+        # writing it) and is brought up to date before anyone else sees it.
+        self._u_n, self._u_val, self._u_stale = size, 0, False
+
+    @property
+    def counters(self):
+        """The device counter array (up to date).  The caller may change it, so the
+        uniform-count knowledge is dropped."""
+        self._materialize()
+        self._u_n = 0
+        return self._ctr
+
+    def _materialize(self):
+        if self._u_stale:
+            if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("stream counters are lazily advanced: read them before a graph capture")
+            v = self._u_val - (1 << 64) if self._u_val >= (1 << 63) else self._u_val
+            self._ctr[:self._u_n].fill_(v)
+            self._u_stale = False
+
+    def uniform_count(self, n, draws):
+        """The common draw count of streams [0, n) if known, and if ``draws`` more draws
+        do not carry into the counter's high word (``draws`` = 0: no such check); else None."""
+        if self._u_n < n or (draws and (self._u_val & 0xFFFFFFFF) > 0x100000000 - draws):
+            return None
+        if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+            return None  # a captured graph replays: the count must come from the array
+        return self._u_val
+
+    def advance_uniform(self, n, val, written):
+        """Streams [0, n) now all sit at ``val``; ``written``: the array holds it too."""
+        self._u_n, self._u_val = n, val
+        self._u_stale = not written
 
     @property
     def key(self):
@@ -64,7 +98,11 @@ class RngStreamSet:
 
     def counter_ptr(self, i):
         """Device address of stream i's counter (the resampling kernels advance it in place)."""
-        return ctypes.c_void_p(self.counters.data_ptr() + 8 * int(i))
+        i = int(i)
+        if i < self._u_n:  # streams [i, _u_n) leave the uniform prefix
+            self._materialize()
+            self._u_n = i
+        return ctypes.c_void_p(self._ctr.data_ptr() + 8 * i)
 
     def draw_streams(self, kind, first, n, shape=1.0, mean=0.0, scale=1.0, out=None):
         """One draw from each of streams first..first+n-1 (the per-particle pattern)."""
@@ -91,7 +129,8 @@ class RngStream:
         s = self._set
         m = 1 if n is None else int(n)
         out = torch.empty(m, dtype=torch.float64, device=s.device)
-        _abi.call("smc_rng_fill", kind, s.seed, self.index, _abi.ptr(s.counters), float(shape), float(mean),
+        s.counter_ptr(self.index)  # stream `index` leaves the uniform prefix
+        _abi.call("smc_rng_fill", kind, s.seed, self.index, _abi.ptr(s._ctr), float(shape), float(mean),
                   float(scale), _abi.ptr(out), m, _abi.stream())
         return float(out.item()) if n is None else out
 

@@ -241,3 +241,39 @@ def test_invariants_shift_trapezoid_ais():
     m = llh.max()
     ais = m + np.log(np.mean(np.exp(llh - m)))
     assert abs(s.log_zconst - ais) <= 1e-10 * max(1.0, abs(ais)), (s.log_zconst, ais)
+
+
+def test_pf_uniform_counter_move_is_bit_identical_to_counter_array():
+    """smc_pf_move_uniform (every particle stream at one draw count, the count a kernel
+    parameter) vs smc_pf_move on the counter array: same state, log-weights and counters,
+    also across the 2^32 boundary of the counter's low word (the uniform path declines
+    the step whose 16 draws would carry; smc_pf_move_uniform rejects such a count)."""
+    from paper_1306_5583_b200 import _abi, pf
+    n = 20000
+    obs, _ = _obs(8)
+    a = pf.make_sampler(n, "systematic", threshold=0.5, seed=7)
+    b = pf.make_sampler(n, "systematic", threshold=0.5, seed=7)
+    a.initialize(obs)
+    b.initialize(obs)
+    assert a.system.rng_set.uniform_count(n, 16) == 8
+    start = (1 << 32) - 24  # moves at lo32 = 2^32-24, -16 (uniform), -8 (carry: array), 0, 8 (uniform)
+    for s in (a, b):
+        s.system.rng_set.counters.fill_(start)
+    a.system.rng_set.advance_uniform(n, start, True)
+    used = []
+    for t in range(5):
+        used.append(a.system.rng_set.uniform_count(n, 16) is not None)
+        a.iterate(1)
+        b.system.rng_set.counters  # drop the knowledge: b always runs the counter-array kernel
+        b.iterate(1)
+        assert torch.equal(a.system.value.data, b.system.value.data), t
+        assert torch.equal(a.system.weight_set.read_log_weight(), b.system.weight_set.read_log_weight()), t
+    assert used == [True, True, False, True, True]
+    assert a.system.rng_set.counters_host()[:n] == b.system.rng_set.counters_host()[:n] == [start + 40] * n
+    assert a.log_zconst == b.log_zconst
+    # a count whose 16 draws carry is refused by the entry point itself
+    v, w = a.system.value, a.system.weight_set
+    ws, nb = pf._ws(a.system, n)
+    with pytest.raises(_abi.SmcError):
+        _abi.call("smc_pf_move_uniform", None, _abi.ptr(v.raw), None, None, _abi.ptr(w.lw_raw), n, 0, n, 7,
+                  (1 << 32) - 15, v.obs_ptr(1), w.state_ptr, None, None, None, ws, nb, _abi.stream())
