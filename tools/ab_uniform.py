@@ -1,7 +1,12 @@
 """Same-box A/B of the PF move: smc_pf_move_uniform (streams at one count) vs smc_pf_move
 (counter array), N = 2^24, median of per-launch CUDA-event times over 200 moves each."""
+import os
+import sys
+
 import numpy as np
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_1306_5583_b200 import pf
 
@@ -26,5 +31,4 @@ for rep in range(400):
         s.system.rng_set.advance_uniform(n, v, True)
     if rep >= 20:
         res[mode].append(e0.elapsed_time(e1))
-for k, v in res.items():
-    print(f"{k:8s} move median {np.median(v):.4f} ms  min {np.min(v):.4f} ms  (n={len(v)})")
+print("  ".join(f"{k} median {np.median(v):.4f} ms min {np.min(v):.4f} ms (n={len(v)})" for k, v in res.items()))
