@@ -254,7 +254,8 @@ int smc_pf_move(const double *x_in, double *x, const int32_t *parents, const int
  * ctr (the host's RngStreamSet tracks this; SPEC.md:396 own-slot streams):
  * same results bit for bit, but the counter array is neither read nor written
  * (the host records the advanced count, ctr + 8) and the Philox blocks share
- * their stream-only products.  SMC_EINVAL if lo32(ctr) + 15 would carry. */
+ * their stream-only products.  SMC_EINVAL if lo32(ctr) + 15 would carry or
+ * stream_base + n > 2^32. */
 int smc_pf_move_uniform(const double *x_in, double *x, const int32_t *parents, const int32_t *gate,
                         double *lw_raw, int64_t n, uint64_t stream_base, int64_t n_total, uint64_t seed,
                         uint64_t ctr, const double *obs_t, smc_wstate *ws_state, double *incw_out,

@@ -124,7 +124,7 @@ SMC_DEV void stage_tabs(PfTabs &t)
 
 // UC: every particle's stream at the same draw count ctr_u (no carry over its 8 draws; the
 // host tracks this, rng.py): the counter array is neither read nor written (16 B per
-// particle-step less traffic) and the Philox blocks use normals_uniform (17 multiplies per
+// particle-step less traffic) and the Philox blocks use normals_uniform (16 multiplies per
 // draw instead of 20).
 template <bool MON, int PPT, bool UC>
 __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_in, double *x_out,
@@ -306,6 +306,8 @@ static int pf_move(const double *x_in, double *x, const int32_t *parents, const 
     if (rc) return rc;
     if (ctr_u && (uint32_t)*ctr_u > 0xFFFFFFFFu - 15u)
         return smc_set_error(SMC_EINVAL, "%s: uniform counter would carry into its high word", who);
+    if (ctr_u && stream_base + (uint64_t)n > ((uint64_t)1 << 32))
+        return smc_set_error(SMC_EINVAL, "%s: uniform counts need stream indices below 2^32", who);
     if (!x_in) x_in = x;
     if ((uintptr_t)x_in & 31) return smc_set_error(SMC_EINVAL, "%s: x_in must be 32-byte aligned", who);
     if (parents && x_in == x)
@@ -320,7 +322,7 @@ static int pf_move(const double *x_in, double *x, const int32_t *parents, const 
     void *scratch = pf_scratch(ws, nb);
     const KeySched key = make_key_sched(seed);
     const double w_eq = 1.0 / (double)(n_total > 0 ? n_total : n);
-    const UniformCtr cu = make_uniform_ctr(ctr_u ? *ctr_u : 0);
+    const UniformCtr cu = make_uniform_ctr(ctr_u ? *ctr_u : 0, key);
 #define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                          \
     do {                                                                                                       \
         if (ctr_u)                                                                                             \

@@ -122,13 +122,22 @@ SMC_DEV void normals_at(uint64_t ctr, uint64_t stream, const K &key, double (&z)
 }
 
 // Rounds R0..9 of philox10 (R0 = 0: the whole block).
+// one 32x32 -> 64 product as a single mul.wide (ptxas otherwise may split it into a
+// separate high and low multiply: two issue slots instead of one)
+SMC_DEV void mulwide(uint32_t a, uint32_t m, uint32_t &hi, uint32_t &lo)
+{
+    asm("{\n\t.reg .u64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%1, %0}, p;\n\t}"
+        : "=r"(hi), "=r"(lo) : "r"(a), "r"(m));
+}
+
 template <int R0, class K>
 SMC_DEV uint4 philox_rounds(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const K &key)
 {
 #pragma unroll
     for (int r = R0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(PHILOX_M0, c0), lo0 = PHILOX_M0 * c0;
-        const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;
+        uint32_t hi0, lo0, hi1, lo1;
+        mulwide(c0, PHILOX_M0, hi0, lo0);
+        mulwide(c2, PHILOX_M1, hi1, lo1);
         const uint32_t n0 = hi1 ^ c1 ^ key.r0(r);
         const uint32_t n2 = hi0 ^ c3 ^ key.r1(r);
         c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
@@ -137,44 +146,50 @@ SMC_DEV uint4 philox_rounds(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, 
 }
 
 // Every stream at the same draw count ctr with no carry into its high word over the next
-// 16 draws (lo32(ctr) <= 2^32 - 16; the host checks): the round-1 M0 products of draw j,
-// M0 * (lo32(ctr) + j), are the same for every stream and come precomputed from the host
-// (a kernel parameter: constant-bank operands).  Per stream, round 1's M1 product and
-// round 2's M0 product are then common to all of its draws, so each draw costs 17
-// multiplies instead of 20.
+// 16 draws (lo32(ctr) <= 2^32 - 16), and every stream index below 2^32 (the host checks
+// both).  Then the round-1 M0 product of draw j, M0 * (lo32(ctr) + j), is the same for every
+// stream, and so is round 2's M1 operand (hi of that product ^ round-1 key, the stream's high
+// word being 0): both products come precomputed from the host (kernel-parameter, i.e.
+// constant-bank, operands).  Per stream, round 1's M1 product and round 2's M0 product are
+// common to all of its draws: each draw costs the 16 multiplies of rounds 3-10 instead of 20.
 struct UniformCtr {
-    uint32_t hi0[16], lo0[16];  // umulhi / mul of M0 by lo32(ctr) + j
-    uint32_t c1;                // hi32(ctr)
+    uint32_t c1k;      // hi32(ctr) ^ round-1 key word 0
+    uint32_t a[16];    // round 2: umulhi(M1, n2_j) ^ round-2 key word 0, n2_j = umulhi(M0, c0_j) ^ round-1 key word 1
+    uint32_t b[16];    // round 2: M1 * n2_j (the next c1)
+    uint32_t c[16];    // M0 * c0_j (round 1's next c3) ^ round-2 key word 1
 };
 
 #ifndef __CUDACC_RTC__
-inline UniformCtr make_uniform_ctr(uint64_t ctr)
+inline UniformCtr make_uniform_ctr(uint64_t ctr, const KeySched &ks)
 {
     UniformCtr u;
+    u.c1k = (uint32_t)(ctr >> 32) ^ ks.k0[0];
     for (int j = 0; j < 16; ++j) {
-        const uint64_t p = (uint64_t)PHILOX_M0 * (uint32_t)((uint32_t)ctr + (uint32_t)j);
-        u.hi0[j] = (uint32_t)(p >> 32);
-        u.lo0[j] = (uint32_t)p;
+        const uint64_t p0 = (uint64_t)PHILOX_M0 * (uint32_t)((uint32_t)ctr + (uint32_t)j);
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ ks.k1[0];  // round 1 with stream hi word 0
+        const uint64_t p1 = (uint64_t)PHILOX_M1 * n2;            // round 2's M1 product
+        u.a[j] = (uint32_t)(p1 >> 32) ^ ks.k0[1];
+        u.b[j] = (uint32_t)p1;
+        u.c[j] = (uint32_t)p0 ^ ks.k1[1];
     }
-    u.c1 = (uint32_t)(ctr >> 32);
     return u;
 }
 #endif
 
-// normals_at(ctr, stream, ...) for the counter `u` describes: bit-identical.
+// normals_at(ctr, stream, ...) for the counter `u` describes and stream < 2^32: bit-identical.
 template <int NZ, class K>
 SMC_DEV void normals_uniform(const UniformCtr &u, uint64_t stream, const K &key, double (&z)[NZ],
                              FmTabs tabs = FmTabs{})
 {
     static_assert(2 * NZ <= 16, "UniformCtr holds 16 draws");
-    const uint32_t c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    const uint32_t c2 = (uint32_t)stream;
     const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;  // round 1, every draw
-    const uint32_t n0 = hi1 ^ u.c1 ^ key.r0(0);
-    const uint32_t x3 = c3 ^ key.r1(0);
+    const uint32_t n0 = hi1 ^ u.c1k;
+    const uint32_t hi0b = __umulhi(PHILOX_M0, n0), lo0b = PHILOX_M0 * n0;  // round 2, every draw
     uint64_t m[2 * NZ];
 #pragma unroll
     for (int j = 0; j < 2 * NZ; ++j) {
-        const uint4 w = philox_rounds<1>(n0, lo1, u.hi0[j] ^ x3, u.lo0[j], key);
+        const uint4 w = philox_rounds<2>(u.a[j] ^ lo1, u.b[j], hi0b ^ u.c[j], lo0b, key);
         m[j] = ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
     }
 #pragma unroll

@@ -107,6 +107,8 @@ def _cv_move_kernel(iter_, system):
     # the kernel takes the count as a scalar and leaves the counter array alone
     u0 = rs.uniform_count(n, 0)
     u = rs.uniform_count(n, 16)  # the kernel's precomputed table covers 16 draws without a carry
+    if system.stream_base + n > 1 << 32:  # ... and stream indices below 2^32
+        u = None
     fn, ctr = ("smc_pf_move", _abi.ptr(rs.counters)) if u is None else ("smc_pf_move_uniform", u)
     common = (_abi.ptr(w.lw_raw), n, system.stream_base, system.n_total, rs.seed, ctr, v.obs_ptr(iter_),
               w.state_ptr, None, mon, None if shard is None else _abi.ptr(shard.partial), ws, nb, _abi.stream())
