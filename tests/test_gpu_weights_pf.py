@@ -277,3 +277,27 @@ def test_pf_uniform_counter_move_is_bit_identical_to_counter_array():
     with pytest.raises(_abi.SmcError):
         _abi.call("smc_pf_move_uniform", None, _abi.ptr(v.raw), None, None, _abi.ptr(w.lw_raw), n, 0, n, 7,
                   (1 << 32) - 15, v.obs_ptr(1), w.state_ptr, None, None, None, ws, nb, _abi.stream())
+
+
+def test_lazy_uniform_counts_are_materialized_for_every_consumer():
+    """After uniform-count moves the counter array lags the streams; a scalar draw, the
+    counter readout and the next (counter-array) move all see the true counts."""
+    from paper_1306_5583_b200 import pf
+    from paper_1306_5583_b200.rng import RngStreamSet
+    n = 1000
+    obs, _ = _obs(8)
+    s = pf.make_sampler(n, "systematic", threshold=0.5, seed=3)
+    s.initialize(obs)
+    s.iterate(3)
+    rs = s.system.rng_set
+    assert rs.uniform_count(n, 0) == 32  # init + 3 moves, 8 draws each
+    x = rs.stream(5).uniform01()
+    ref = RngStreamSet(n + 1, 3)
+    ref.counters.fill_(32)
+    assert x == ref.stream(5).uniform01()
+    assert rs.uniform_count(n, 0) is None  # stream 5 left the common count
+    c = rs.counters_host()
+    assert c[5] == 33 and c[:5] == [32] * 5 and c[6:n] == [32] * (n - 6)
+    s.iterate(1)  # the counter-array kernel from here on
+    c = rs.counters_host()
+    assert c[5] == 41 and c[:5] == [40] * 5 and c[6:n] == [40] * (n - 6)
