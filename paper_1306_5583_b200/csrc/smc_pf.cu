@@ -109,16 +109,35 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
 // The fast-math tables (log 8 KB, cos 320 B, exp 2 KB) staged in shared memory once per
 // block: 32-bit shared addressing instead of a 64-bit global address (constant-bank base +
 // IMAD.WIDE on the FMA pipe, which the Philox multiplies saturate) per lookup.
-struct PfTabs {
+struct __align__(16) PfTabs {
     smc_fm::LogEntry log[512];
     smc_fm::ExpEntry exp[128];
     smc_fm::CosPoly cos[4];
 };
-SMC_DEV void stage_tabs(PfTabs &t)
+// The tables are staged in two halves: every 16-byte piece loaded into registers
+// first (tab_load), the shared stores and the barrier only after the block's parent indices
+// and first prefetches are in flight too (tab_store) -- one memory round trip at block start
+// instead of two.
+static_assert(sizeof(smc_fm::LogEntry) == 16 && sizeof(smc_fm::ExpEntry) == 16 && sizeof(PfTabs::cos) == 320,
+              "table layout");
+static_assert(PB >= 128 && 512 % PB == 0, "one pass of 16-byte pieces per table");
+struct TabRegs {
+    double2 log[512 / PB], exp, cos;
+};
+SMC_DEV void tab_load(TabRegs &r)
 {
-    for (int k = threadIdx.x; k < 512; k += PB) t.log[k] = smc_fm::kLogTab[k];
-    for (int k = threadIdx.x; k < 128; k += PB) t.exp[k] = smc_fm::kExpTab[k];
-    if (threadIdx.x < 4) t.cos[threadIdx.x] = smc_fm::kCosPoly[threadIdx.x];
+    const double2 *lg = reinterpret_cast<const double2 *>(smc_fm::kLogTab);
+#pragma unroll
+    for (int k = 0; k < 512 / PB; ++k) r.log[k] = __ldg(lg + threadIdx.x + k * PB);
+    if (threadIdx.x < 128) r.exp = __ldg(reinterpret_cast<const double2 *>(smc_fm::kExpTab) + threadIdx.x);
+    if (threadIdx.x < 20) r.cos = __ldg(reinterpret_cast<const double2 *>(smc_fm::kCosPoly) + threadIdx.x);
+}
+SMC_DEV void tab_store(PfTabs &t, const TabRegs &r)
+{
+#pragma unroll
+    for (int k = 0; k < 512 / PB; ++k) reinterpret_cast<double2 *>(t.log)[threadIdx.x + k * PB] = r.log[k];
+    if (threadIdx.x < 128) reinterpret_cast<double2 *>(t.exp)[threadIdx.x] = r.exp;
+    if (threadIdx.x < 20) reinterpret_cast<double2 *>(t.cos)[threadIdx.x] = r.cos;
     __syncthreads();
 }
 
@@ -135,7 +154,8 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
                                                    LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
     __shared__ PfTabs tabs;
-    stage_tabs(tabs);  // constant data: staged before the dependency wait
+    TabRegs tr;
+    tab_load(tr);  // constant data: requested before the dependency wait
     SMC_PDL_WAIT();
     __shared__ double s_v[PPT][PB];
     const int64_t base = (int64_t)blockIdx.x * (PB * PPT) + threadIdx.x;
@@ -159,6 +179,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         if (!UC) c_nx = ctrs[base];
         if (nl.needs_raw()) lw_nx = lw_raw[base];
     }
+    tab_store(tabs, tr);
 #pragma unroll kPfUnroll
     for (int q = 0; q < PPT; ++q) {
         const int64_t i = base + (int64_t)q * PB;
