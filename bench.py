@@ -379,10 +379,10 @@ def move_traffic(n):
 
 
 def compute_floor(n, move_ms):
-    """Issue floor of k_pf_move: instructions per particle (ncu, profiles/r1_ncu_move_mix.txt) over
+    """Issue floor of k_pf_move: instructions per particle (ncu, profiles/r1_ncu_move_tabstage.txt) over
     148 SMs x 4 schedulers x 32 lanes at the max SM clock -- the compute roofline the move is held to."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_move_mix.txt")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_move_tabstage.txt")) as f:
             head = [l for l in f if "warp-instructions (" in l][0]
         ipp = float(head.split("(")[1].split()[0])
     except (OSError, IndexError, ValueError):
@@ -390,7 +390,7 @@ def compute_floor(n, move_ms):
     floor_ms = n * ipp / (148 * 128 * 1.965e9) * 1e3
     return {"bound": "issue (IMAD.WIDE Philox on the FMA pipe + fp64 Box-Muller)", "instr_per_particle": ipp,
             "issue_floor_ms": floor_ms, "achieved_ms": move_ms, "frac": floor_ms / move_ms,
-            "source": "profiles/r1_ncu_move_mix.txt (ncu --set full, one launch at 2^24)"}
+            "source": "profiles/r1_ncu_move_tabstage.txt (ncu --set full, one launch at 2^24)"}
 
 
 def resample_copy_bench(P, system, scheme, reps=10):
