@@ -241,6 +241,8 @@ def _gmm_sigs():
                              C.c_double, C.c_double, C.c_int]
     L.orc_gmm_run.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_double, _f64, C.c_int, _f64, C.c_int,
                               C.c_double, _f64, C.c_int]
+    L.orc_gmm_run_steps.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_double, _f64, C.c_int, _f64,
+                                    C.c_int, C.c_int, C.c_double, _f64, C.c_int]
     L._gmm_ok = True
     return L
 
@@ -272,13 +274,16 @@ def gmm_mh(block, x, streams, y, h, alpha, sd, r=4, nthreads=1):
                                   _h6(h), alpha, sd, nthreads)
 
 
-def gmm_run(n, seed, scheme, threshold, y, h, T, power, r=4, nthreads=1):
-    """hist (T+1) x 8: ess_over_n resampled acc_mu acc_lambda acc_weight alpha U_t log_zconst."""
+def gmm_run(n, seed, scheme, threshold, y, h, T, power, r=4, nthreads=1, steps=None):
+    """hist (steps+1) x 8: ess_over_n resampled acc_mu acc_lambda acc_weight alpha U_t log_zconst.
+    steps < T: only the first `steps` iterations of the T-iteration schedule."""
     if isinstance(scheme, str):
         scheme = SCHEMES[scheme]
     y = np.ascontiguousarray(y, np.float64)
-    hist = np.zeros((T + 1, 8), np.float64)
-    rc = _gmm_sigs().orc_gmm_run(n, r, seed, scheme, threshold, y, len(y), _h6(h), T, power, hist, nthreads)
+    steps = T if steps is None else int(steps)
+    hist = np.zeros((steps + 1, 8), np.float64)
+    rc = _gmm_sigs().orc_gmm_run_steps(n, r, seed, scheme, threshold, y, len(y), _h6(h), T, steps, power, hist,
+                                       nthreads)
     if rc:
         raise OracleError(f"gmm_run rc={rc}")
     return hist

@@ -670,6 +670,13 @@ int64_t orc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t *ctrs, uint3
 int orc_gmm_run(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
                 const double *h6, int T, double power, double *hist, int nthreads)
 {
+    return orc_gmm_run_steps(n, r, seed, scheme, threshold, y, nd, h6, T, T, power, hist, nthreads);
+}
+
+/* The first `steps` iterations of a T-iteration run (the alpha schedule is T's). */
+int orc_gmm_run_steps(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                      const double *h6, int T, int steps, double power, double *hist, int nthreads)
+{
     double *x = (double *)calloc((size_t)(ORC_GMM_ROW * n), sizeof(double));
     double *lw = (double *)malloc(sizeof(double) * (size_t)n), *w = (double *)malloc(sizeof(double) * (size_t)n);
     double *incw = (double *)malloc(sizeof(double) * (size_t)n);
@@ -681,7 +688,7 @@ int orc_gmm_run(int64_t n, int r, uint64_t seed, int scheme, double threshold, c
     const int use[3] = {1, !(h6[5] > 0), r > 1};
     orc_gmm_init(x, n, r, ctrs, k0, k1, y, nd, h6, nthreads);
     orc_weights_update(ORC_W_EQUAL, lw, w, NULL, n, &ess);
-    for (int t = 0; t <= T && !rc; ++t) {
+    for (int t = 0; t <= steps && t <= T && !rc; ++t) {
         double *hr = hist + 8 * t;
         double acc[3] = {0, 0, 0};
         if (t > 0) {

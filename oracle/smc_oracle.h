@@ -100,6 +100,8 @@ int64_t orc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t *ctrs, uint3
                    const double *y, int nd, const double *h6, double alpha, double sd, int nthreads);
 int orc_gmm_run(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
                 const double *h6, int T, double power, double *hist, int nthreads);
+int orc_gmm_run_steps(int64_t n, int r, uint64_t seed, int scheme, double threshold, const double *y, int nd,
+                      const double *h6, int T, int steps, double power, double *hist, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -39,12 +39,36 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _deps():
+    """Every file the library is compiled from: kernels, device headers, the fast-math tables."""
+    pats = ("*.cu", "*.cuh", "*.h", "*.inc")
+    files = [f for p in pats for f in glob.glob(os.path.join(CSRC, p))]
+    return sorted(files + glob.glob(os.path.join(ROOT, "include", "*.h")))
+
+
+def source_hash():
+    """sha256 over the build flags and every source file (the library's stamp)."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in _deps():
+        h.update(os.path.relpath(f, ROOT).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+STAMP = LIB + ".stamp"
+
+
 def _stale():
     if not os.path.exists(LIB):
         return True
-    t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "smc_abi.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    try:
+        with open(STAMP) as f:
+            return f.read().strip() != source_hash()
+    except OSError:
+        return True
 
 
 def build(force=False, verbose=False, extra=()):
@@ -62,6 +86,9 @@ def build(force=False, verbose=False, extra=()):
     if verbose and (r.stdout or r.stderr):
         print(r.stdout, r.stderr, file=sys.stderr)
     os.replace(LIB + ".tmp", LIB)
+    if not extra:
+        with open(STAMP, "w") as f:
+            f.write(source_hash())
     return LIB
 
 

@@ -452,6 +452,10 @@ class Sampler:
             n -= 1
             self._graph_warm = True
         pairs = n // 2
+        # never replay past the observations: the graph gathers obs[t] by a device index, so an
+        # out-of-range t would be a device-side fault; the eager path raises IndexError instead
+        nobs = v.obs.shape[0] if getattr(v, "obs", None) is not None else 0
+        pairs = max(0, min(pairs, (nobs - 1 - self.iteration) // 2))
         if pairs == 0:
             return n
         # the captured moves advance the counter array itself: bring it up to date (an eager
@@ -482,8 +486,11 @@ class Sampler:
         for name, col in mon.items():
             sysm.pending_monitors[name] = (stage[1].data_ptr() + 8 * col, t0)
         tdev.fill_(t0 + 1)
+        # everything the capture bakes in as a launch argument: buffers, and the sampler's public
+        # knobs (threshold, scheme, RNG seed) -- a changed knob must not replay the old value
         key = (v._cur, v.pending is not None, self._hist.data_ptr(), v.obs.data_ptr(),
-               sysm.weight_set.state.data_ptr())
+               sysm.weight_set.state.data_ptr(), float(sysm.threshold), int(sysm.resample_scheme),
+               int(sysm.rng_set.seed), sysm.rng_set.counters.data_ptr(), v.obs.shape[0])
         g = gb["graphs"].get(key)
         if g is None:
             g = torch.cuda.CUDAGraph()

@@ -12,9 +12,9 @@
 //          r = z/c_i - 1 via one FMA (|r| <= 2^-10, 512 intervals), c_i = 1 exactly
 //          around z = 1 so that r = z - 1 is exact there (full relative accuracy near
 //          x = 1), log1p(r) - r by a degree-6 Taylor polynomial (truncation < 2^-63 |r|).
-// cos(x), 0 <= x < 8 (x = fl(2 pi u) in Box-Muller): Cody-Waite reduction by
-//          pi/2 in two 33-bit pieces + tail, then fdlibm's __kernel_cos/_sin
-//          polynomials on |r| <= pi/4.
+// cos_bm(x), 0 <= x < 8 (x = fl(2 pi u) in Box-Muller): branch-free quadrant
+//          reduction, then minimax polynomials on |r| <= pi/4 (coefficients:
+//          fdlibm's published __kernel_cos/__kernel_sin constants; see cos_bm).
 #pragma once
 #ifdef __CUDACC_RTC__  // run-time compiled user kernels (NVRTC has no libc headers)
 typedef unsigned long long uint64_t;
@@ -134,53 +134,6 @@ SMC_HD double log(double x)
 {
     // positive normal finite: exponent field in [1, 2046]
     return (bits(x) >> 52) - 1u < 2046u ? log_core(x) : ::log(x);
-}
-
-// cos(x) for |x| < 8; larger arguments go to libm.
-SMC_HD double cos(double x)
-{
-    const double ax = fabs(x);
-    if (!(ax < 8.0)) return ::cos(x);
-    const double PIO2_1 = 0x1.921fb54400000p+0;
-    const double PIO2_2 = 0x1.0b4611a600000p-34, PIO2_2T = 0x1.3198a2e037073p-69;
-    const double TWO_OVER_PI = 0x1.45f306dc9c883p-1;
-    const double jd = rint(ax * TWO_OVER_PI);
-    const int j = (int)jd;
-    // r = ax - j pi/2: the first product and difference are exact (j <= 5, 33-bit PIO2_1)
-    const double r1 = ax - jd * PIO2_1;
-    const double w = jd * PIO2_2;
-    double r = r1 - w;
-    const double tail = jd * PIO2_2T - ((r1 - r) - w);
-    const double y0 = r - tail;                 // reduced argument, |y0| <= pi/4 (+tiny)
-    const double y1 = (r - y0) - tail;          // its low part
-    const double z = y0 * y0;
-    double res;
-    if (j & 1) {  // +-sin(y): fdlibm __kernel_sin(y0, y1, 1)
-        const double S1 = -1.66666666666666324348e-01, S2 = 8.33333333332248946124e-03,
-                     S3 = -1.98412698298579493134e-04, S4 = 2.75573137070700676789e-06,
-                     S5 = -2.50507602534068634195e-08, S6 = 1.58969099521155010221e-10;
-        const double v = z * y0;
-        const double rr = S2 + z * (S3 + z * (S4 + z * (S5 + z * S6)));
-        res = y0 - ((z * (0.5 * y1 - v * rr) - y1) - v * S1);
-        if ((j & 3) == 1) res = -res;
-    } else {  // +-cos(y): fdlibm __kernel_cos(y0, y1)
-        const double C1 = 4.16666666666666019037e-02, C2 = -1.38888888888741095749e-03,
-                     C3 = 2.48015872894767294178e-05, C4 = -2.75573143513906633035e-07,
-                     C5 = 2.08757232129817482790e-09, C6 = -1.13596475577881948265e-11;
-        const double rr = z * (C1 + z * (C2 + z * (C3 + z * (C4 + z * (C5 + z * C6)))));
-        const double ay = fabs(y0);
-        if (ay < 0.3) {
-            res = 1.0 - (0.5 * z - (z * rr - y0 * y1));
-        } else {
-            // |y|/4 truncated to 21 bits (fdlibm's INSERT_WORDS): 1 - qx is exact
-            const double qx = ay > 0.78125 ? 0.28125 : from_bits((bits(ay) - 0x0020000000000000ull) & 0xffffffff00000000ull);
-            const double hz = 0.5 * z - qx;
-            const double a = 1.0 - qx;
-            res = a - (hz - (z * rr - y0 * y1));
-        }
-        if ((j & 3) == 2) res = -res;
-    }
-    return res;
 }
 
 // cos(x) for 0 <= x < 8, BRANCH-FREE (the Box-Muller argument x = fl(2 pi u),

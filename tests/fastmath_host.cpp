@@ -1,7 +1,6 @@
 // Host build of paper_1306_5583_b200/csrc/smc_fastmath.h for the accuracy test.
 #include "../paper_1306_5583_b200/csrc/smc_fastmath.h"
 extern "C" void fm_log(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::log(x[i]); }
-extern "C" void fm_cos(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::cos(x[i]); }
 extern "C" void fm_cos_bm(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::cos_bm(x[i]); }
 extern "C" void fm_sqrt_bm(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::sqrt_bm(x[i]); }
 extern "C" void fm_exp(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp(x[i], smc_fm::kExpTab); }

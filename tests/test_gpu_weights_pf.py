@@ -214,6 +214,43 @@ def test_graph_replay_is_bit_identical_to_eager(scheme, n):
     assert np.array_equal(x0, x1) and np.array_equal(w0, w1) and z0 == z1
 
 
+def test_graph_replay_stops_at_the_last_observation():
+    """iterate() past the data with graph='auto': the replayed pairs stop before the last
+    observation and the eager remainder raises IndexError (no device-side fault)."""
+    from paper_1306_5583_b200 import pf
+    obs, _ = _obs(40)
+    s = pf.make_sampler(4096, "systematic", threshold=0.5, seed=5)
+    s.graph_min_steps = 4
+    s.initialize(obs)
+    with pytest.raises(IndexError):
+        s.iterate(45)
+    assert s.iteration == 39  # every observation was used, none past the end
+    torch.cuda.synchronize()  # the context is still healthy
+    assert s._gbuf["graphs"], "graph mode did not engage"
+    h = s.history()
+    assert np.all(np.isfinite(h["pos.0"]))
+
+
+def test_graph_replay_follows_changed_scheme_and_threshold():
+    """A cached graph must not replay an old scheme / threshold after the caller changes them."""
+    from paper_1306_5583_b200 import pf
+    from paper_1306_5583_b200.resample import _scheme
+    obs, _ = _obs(60)
+    runs = []
+    for graph in (False, "auto"):
+        s = pf.make_sampler(4096, "systematic", threshold=0.5, seed=13)
+        s.graph = graph
+        s.graph_min_steps = 4
+        s.initialize(obs)
+        s.iterate(20)
+        s.system.resample_scheme = _scheme("multinomial")
+        s.system.threshold = 0.9
+        s.initialize(obs)
+        s.iterate(30)
+        runs.append((s.history_array(), s.log_zconst))
+    assert np.array_equal(runs[0][0], runs[1][0]) and runs[0][1] == runs[1][1]
+
+
 def test_invariants_shift_trapezoid_ais():
     """SPEC acceptance 8 invariant suites: log-weight shift invariance, trapezoid exactness on
     linear integrands, and AIS/SIS equivalence at threshold <= 0 (no resampling: the running
