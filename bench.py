@@ -42,6 +42,11 @@ def parse():
                     help="particles per GPU (default: 2^24 on one GPU -- config 2 -- and 2^28 / G on G > 1 "
                          "GPUs -- config 4, strong scaling); use --particles under torchrun: it claims --n*")
     ap.add_argument("--scheme", default="systematic")
+    ap.add_argument("--config", type=int, choices=(2, 4), default=None,
+                    help="2: N=2^24 per GPU (default on one GPU); 4: N=2^28 in total, sharded over the GPUs "
+                         "(default on G > 1; --config 4 --gpus 1 runs the whole 2^28 filter on one GPU, the "
+                         "same-config single-GPU point of the strong-scaling curve)")
+    ap.add_argument("--no-schemes", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gmm", action="store_true")
@@ -49,7 +54,8 @@ def parse():
 
 
 def workload(n, world, scheme, strong):
-    """(scaling, config) of the JSON line: config 2 on one GPU, config 4 (2^28 in total) on G > 1."""
+    """(scaling, config) of the JSON line: config 2 on one GPU, config 4 (2^28 in total) on G > 1.
+    Both arms print exactly this config dict (the driver compares them)."""
     if strong:
         name = (f"PF config 4: N=2^{(n * world).bit_length() - 1} particles in total sharded over {world} GPUs "
                 f"(2^{n.bit_length() - 1} per GPU), ")
@@ -59,10 +65,19 @@ def workload(n, world, scheme, strong):
     return ("strong" if strong else "weak"), {"workload": name, "n_particles": n * world, "scheme": scheme}
 
 
+def config_of(args, world):
+    return args.config if args.config is not None else (2 if world == 1 else 4)
+
+
 def particles_per_gpu(args, world):
     if args.n is not None:
         return args.n
-    return N_DEFAULT if world == 1 else N_SHARDED // world
+    return N_DEFAULT if config_of(args, world) == 2 else N_SHARDED // world
+
+
+def is_strong(args, world):
+    """Config 4 fixes the TOTAL work (2^28): strong scaling; config 2 / --particles fix it per GPU."""
+    return args.n is None and config_of(args, world) == 4
 
 
 def dist_env():
@@ -166,36 +181,57 @@ def cpu_baseline_pf(n, steps, scheme, obs, threads):
     return times
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def bench_obs(steps):
+    """The synthetic observation track both arms use (T >= 100 rows: the paper's 100-obs shape)."""
+    import numpy as np
+    return np.cumsum(np.random.default_rng(1306).normal(0, 0.15, (max(100, steps), 2)), 0)
+
+
 def run_reference(args):
-    """--impl reference: the reference algorithm (CPU oracle port) on this host's cores."""
+    """--impl reference: the reference algorithm (C oracle port: OpenMP per-particle loops,
+    sequential normalization / resampling / copy as SPEC.md:99, :185 pin) on this host's cores,
+    on the SAME config as the B200 arm.  Config 2 (N = 2^24) runs at its full N: every timed
+    step is one whole PF step of the workload.  Config 4 (2^28 in total) would take ~25 s per
+    step on the host, so its steps are bounded samples of 2^24 particles (the rate is per
+    particle-step; `sample` says so)."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    import numpy as np
-
     cores = len(os.sched_getaffinity(0))
     n = particles_per_gpu(args, world)
-    # bounded sample: every step runs the full PF step on N_s <= N particles, N_s the largest power of
-    # two with (W + K) N_s <= 4e8 particle-steps (about a minute on a 16-core host, whatever K the
-    # driver passes), and the rate is reported per particle-step
-    ns = n
-    while ns > (1 << 14) and (args.warmup + args.steps) * ns > 4e8:
-        ns >>= 1
-    obs = np.cumsum(np.random.default_rng(1306).normal(0, 0.15, (max(100, args.steps + args.warmup + 2), 2)), 0)
+    n_work = n * world
+    ns = n_work if n_work <= N_DEFAULT else N_DEFAULT
+    obs = bench_obs(args.steps + args.warmup + 2)
     times = cpu_baseline_pf(ns, args.warmup + args.steps, args.scheme, obs, cores)
     t = sum(times[args.warmup:])
     v = ns * args.steps / t
-    scaling, cfg = workload(n, world, args.scheme, world > 1 and args.n is None)
+    scaling, cfg = workload(n, world, args.scheme, is_strong(args, world))
+    full = ns == n_work
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps * (n / ns), "higher_is_better": True,
+            "warmup": args.warmup,
+            # measured per step at N_s; at the full workload N (config 2) this IS the step time
+            "ms_per_step": 1e3 * t / args.steps * (n_work / ns), "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            # the same workload line as the B200 arm (N per GPU x world); each step is a bounded
-            # sample of it: one host runs N_s particles and the rate is per particle-step
-            "config": cfg,
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.steps} full PF steps of the C oracle at N={ns} (of the workload's "
-                                       f"N={n}) on one host (after {args.warmup} warm-up steps), OpenMP "
-                                       "per-particle loops, rate per particle-step"},
+            "config": cfg, "same_config": full,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+                             "sample": (f"{args.steps} full PF steps of the C oracle at the workload's N={ns} "
+                                        if full else
+                                        f"{args.steps} full PF steps of the C oracle at N={ns} of the workload's "
+                                        f"N={n_work} (rate per particle-step) ") +
+                                       f"after {args.warmup} warm-up steps, OpenMP over {cores} threads for the "
+                                       "per-particle loops"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -224,12 +260,18 @@ def run_b200(args):
     n = particles_per_gpu(args, world)
     n_total = n * world
     # one GPU: config 2 (N = 2^24); G > 1: config 4 (N = 2^28 in total, 2^28 / G per GPU: strong
-    # scaling) unless --particles fixes the per-GPU size (then weak)
-    strong = world > 1 and args.n is None
+    # scaling) unless --particles fixes the per-GPU size (then weak); --config 4 on one GPU: 2^28
+    strong = is_strong(args, world)
     T = args.warmup + args.steps + 60  # + the instrumented phase pass
-    rs = np.random.default_rng(1306)
     # synthetic observations of the paper's shape: a smooth track + noise (T x 2)
-    obs = np.cumsum(rs.normal(0, 0.15, (max(100, T), 2)), 0)
+    obs = bench_obs(T)
+    strong_ref = None
+    if strong and world > 1 and rank == 0:
+        # the same config-4 filter (2^28 particles) on this ONE GPU, timed the same way before the
+        # sharded run: the single-GPU point of the strong-scaling curve, inside the same job
+        strong_ref = time_single(P, n_total, args, obs)
+    if world > 1:
+        torch.distributed.barrier()
 
     shard = None
     if world > 1:  # one rank's slice of a G-GPU filter: global streams, NCCL allgathers + row exchange
@@ -251,9 +293,11 @@ def run_b200(args):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        lc0 = P._abi.launch_count()
         e0.record()
         s.iterate(args.steps, check=False)
         e1.record()
+        launches = P._abi.launch_count() - lc0  # the library's own kernels in the timed region
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -301,12 +345,13 @@ def run_b200(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(cfg, l2=f"inputs larger than L2 (state {32 * n >> 20} MiB per GPU), no flush",
-                           parallelism=f"particles sharded over {world} GPU(s)"),
+            "config": cfg,
+            "l2": f"inputs larger than L2 (state {32 * n >> 20} MiB per GPU), no flush",
+            "parallelism": f"particles sharded over {world} GPU(s)",
             "phase_ms": phase, "resampled_frac": float(np.mean(resampled)), "moved_row_frac": frac_moved,
-            # per step: k_pf_move, k_lse_level1, k_lse_finalize, k_ess_decide, 6 resample passes
-            # (device-gated: they launch every step), k_set_equal
-            "gpu_launches": args.steps * 11,
+            # counted by the library (smc_launch_count) around the timed iterate(): per step the move,
+            # the lse combine, the ESS rule, the device-gated resample passes and set_equal_weight
+            "gpu_launches": launches,
             "roofline": {"bound": "hbm", "kernel": "k_pf_move (fused move + add_log_weight + lse/ESS partials)",
                          "achieved": move_gbs, "peak": peak, "unit": "GB/s", "frac": move_gbs / peak,
                          "traffic": move_traffic(n), "peak_source": peak_src,
@@ -330,16 +375,84 @@ def run_b200(args):
                        "h2d_bytes_per_step": e["h2d"], "d2h_bytes_per_step": e["d2h"]}
     if rank == 0 and world == 1 and not args.no_gmm:
         line["gmm"] = gmm_bench(P)
+    if strong_ref is not None:
+        line["strong_baseline"] = dict(strong_ref, note="the same config-4 filter on ONE GPU of this job "
+                                       "(rank 0, before the sharded run): strong-scaling efficiency at "
+                                       f"{world} GPUs = value / (strong_baseline.value * {world})")
+    if rank == 0 and world == 1 and not args.no_schemes and args.n is None and config_of(args, world) == 2:
+        line["schemes"] = schemes_bench(P, n, args, obs)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        cores = len(os.sched_getaffinity(0))
-        ncpu = 1 << 22
-        times = cpu_baseline_pf(ncpu, 3, args.scheme, obs, cores)
-        line["cpu_baseline"] = {"value": ncpu * 3 / sum(times), "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"3 full PF steps of the oracle at N=2^22 (scaled per particle-step)"}
+        line["cpu_baseline"] = cpu_baseline_line(n, args.scheme, obs)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def time_single(P, n, args, obs):
+    """One unsharded filter of n particles on this GPU: ms per step over args.steps (CUDA events)."""
+    import torch
+    s = P.pf.make_sampler(n, args.scheme, 0.5, seed=1306)
+    s.initialize(obs)
+    for _ in range(args.warmup):
+        s.iterate(1, check=False)
+    s.check()
+    s.graph = False
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s.iterate(args.steps, check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    s.check()
+    ms = e0.elapsed_time(e1)
+    del s
+    torch.cuda.empty_cache()
+    return {"value": n * args.steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / args.steps, "n_particles": n,
+            "n_gpus": 1}
+
+
+def schemes_bench(P, n, args, obs, steps=30, warmup=3):
+    """Config 2's sweep: the 2^24 PF step (move + ESS + resample + parent map + fused copy) for
+    every resampling scheme, eager launches timed with CUDA events over `steps` steps."""
+    import numpy as np
+    import torch
+    out = {}
+    for scheme in ("multinomial", "residual", "stratified", "systematic", "residual_stratified",
+                   "residual_systematic"):
+        s = P.pf.make_sampler(n, scheme, 0.5, seed=1306)
+        s.initialize(obs)
+        for _ in range(warmup):
+            s.iterate(1, check=False)
+        s.graph = False
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.iterate(steps, check=False)
+        e1.record()
+        torch.cuda.synchronize()
+        s.check()
+        ms = e0.elapsed_time(e1) / steps
+        h = s.history()
+        out[scheme] = {"ms_per_step": ms, "value": n / (ms * 1e-3), "unit": UNIT,
+                       "resampled_frac": float(np.mean(h["resampled"][-steps:]))}
+        del s
+        torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline_line(n, scheme, obs):
+    """The oracle on this box's host cores at the workload's own N: 3 timed steps with all cores
+    (OpenMP per-particle loops) and 1 timed step on one thread (the sequential figure)."""
+    cores = len(os.sched_getaffinity(0))
+    tm = cpu_baseline_pf(n, 4, scheme, obs, cores)[1:]  # first step untimed (page faults)
+    t1 = cpu_baseline_pf(n, 1, scheme, obs, 1)
+    v = n * len(tm) / sum(tm)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"{len(tm)} full PF steps of the C oracle at the workload's N={n} (after 1 untimed step), "
+                      f"OpenMP over {cores} threads for the per-particle loops",
+            "sequential": {"value": n / t1[0], "unit": UNIT, "cores": 1,
+                           "sample": f"1 full PF step of the C oracle at N={n} on one thread"}}
 
 
 def gmm_bench(P, n=1 << 20, T=100):
@@ -361,36 +474,65 @@ def gmm_bench(P, n=1 << 20, T=100):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"workload": "GMM config 3: N=2^20, 4 components, 1000 points, T=100, prior annealing p=2",
-            "value": n * T / (ms * 1e-3), "unit": "particle-iterations/s", "ms_per_run": ms,
-            "log_zconst_ds": s.log_zconst, "log_zconst_ps": s.path_log_zconst(),
-            "component_evals_per_s": n * (1 + 3 * T) * 1000 * 4 / (ms * 1e-3)}
+    evals = n * 3 * T * 1000 * 4  # (particle, point, component) likelihood terms in the 3T MH blocks
+    out = {"workload": "GMM config 3: N=2^20, 4 components, 1000 points, T=100, prior annealing p=2",
+           "value": n * T / (ms * 1e-3), "unit": "particle-iterations/s", "ms_per_run": ms,
+           "log_zconst_ds": s.log_zconst, "log_zconst_ps": s.path_log_zconst(),
+           "component_evals_per_s": n * (1 + 3 * T) * 1000 * 4 / (ms * 1e-3)}
+    # FP64 roofline: fp64 thread-instructions per likelihood term from the committed ncu capture of
+    # one k_gmm_mh launch (stamped with the kernel sources), times the terms of the whole run, over
+    # the run's time, against the fp64 pipe's issue rate (64 lanes / SM / clk x 148 SMs x max clock)
+    d, src = profile_for("gmm_mh_ncu", n)
+    if d is not None:
+        per = d["fp64_thread_inst"] / (d["n"] * d["nd"] * d["r"])
+        ach = per * evals / (ms * 1e-3)
+        peak = 64 * 148 * 1.965e9
+        out["fp64"] = {"bound": "fp64 pipe", "fp64_inst_per_term": per, "achieved_inst_per_s": ach,
+                       "peak_inst_per_s": peak, "frac": ach / peak,
+                       "ncu_fp64_pipe_pct_one_launch": d.get("fp64_pipe_pct"), "source": src}
+    else:
+        out["fp64"] = {"frac": None, "source": src}
+    return out
+
+
+def source_hash():
+    """The library's source stamp (every csrc/ file + the ABI header + the nvcc flags)."""
+    from paper_1306_5583_b200 import _build
+    return _build.source_hash()
+
+
+def profile_for(name, n):
+    """A committed ncu capture (profiles/<name>.json) -- used only when it was taken at this N AND
+    from the current kernel sources (its `source_hash`): a kernel change never reuses a stale
+    capture silently; the field reads null with the reason instead."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name + ".json")) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None, f"profiles/{name}.json missing"
+    if d.get("n") != n:
+        return None, f"profiles/{name}.json taken at N={d.get('n')}"
+    if d.get("source_hash") != source_hash():
+        return None, f"profiles/{name}.json is from other kernel sources (commit {d.get('commit')}): re-capture"
+    return d, f"profiles/{name}.json (ncu --set full, commit {d.get('commit')}, same source hash)"
 
 
 def move_traffic(n):
-    """DRAM bytes (read + write) per k_pf_move launch from the committed ncu --set full capture
-    (profiles/r1_move_traffic.json), when it was taken at this N; else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_move_traffic.json")) as f:
-            d = json.load(f)
-        return d["dram_bytes_read"] + d["dram_bytes_write"] if d.get("n") == n else None
-    except (OSError, ValueError, KeyError):
-        return None
+    """DRAM bytes (read + write) per k_pf_move launch from the committed ncu capture, or None."""
+    d, _ = profile_for("move_ncu", n)
+    return None if d is None else d["dram_bytes_read"] + d["dram_bytes_write"]
 
 
 def compute_floor(n, move_ms):
-    """Issue floor of k_pf_move: instructions per particle (ncu, profiles/r1_ncu_move_tabstage.txt) over
-    148 SMs x 4 schedulers x 32 lanes at the max SM clock -- the compute roofline the move is held to."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_move_tabstage.txt")) as f:
-            head = [l for l in f if "warp-instructions (" in l][0]
-        ipp = float(head.split("(")[1].split()[0])
-    except (OSError, IndexError, ValueError):
-        return None
+    """Issue floor of k_pf_move: instructions per particle (ncu) over 148 SMs x 4 schedulers x 32
+    lanes at the max SM clock -- the compute roofline the move is held to."""
+    d, src = profile_for("move_ncu", n)
+    if d is None:
+        return {"frac": None, "source": src}
+    ipp = d["warp_inst_per_particle"] * 32.0 if "warp_inst_per_particle" in d else d["inst_per_particle"]
     floor_ms = n * ipp / (148 * 128 * 1.965e9) * 1e3
     return {"bound": "issue (IMAD.WIDE Philox on the FMA pipe + fp64 Box-Muller)", "instr_per_particle": ipp,
-            "issue_floor_ms": floor_ms, "achieved_ms": move_ms, "frac": floor_ms / move_ms,
-            "source": "profiles/r1_ncu_move_tabstage.txt (ncu --set full, one launch at 2^24)"}
+            "issue_floor_ms": floor_ms, "achieved_ms": move_ms, "frac": floor_ms / move_ms, "source": src}
 
 
 def resample_copy_bench(P, system, scheme, reps=10):

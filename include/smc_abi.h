@@ -50,6 +50,10 @@ extern "C" {
 int smc_abi_version(void);
 /* Copies the last host-side error message of the calling thread. */
 int smc_last_error(char *buf, size_t len);
+/* Kernels this library has launched in the process so far (every entry point's launches,
+ * NVRTC user kernels included).  No reference counterpart: instrumentation for the bench's
+ * `gpu_launches` (how many of the library's kernels ran in a timed region). */
+int smc_launch_count(uint64_t *out);
 
 /* ------------------------------------------------------------------------ */
 /* RNG -- replaces pkg/src/smckit/rng.py                                     */

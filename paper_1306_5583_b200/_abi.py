@@ -58,6 +58,7 @@ _vp, _i64, _u64, _i32, _f64, _sz = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C
 _SIGS = {
     "smc_abi_version": ([], C.c_int),
     "smc_last_error": ([C.c_char_p, _sz], C.c_int),
+    "smc_launch_count": ([_vp], C.c_int),
     "smc_philox_blocks": ([_vp, _i64, _u64, _vp, _vp], C.c_int),
     "smc_rng_fill": ([_i32, _u64, _u64, _vp, _f64, _f64, _f64, _vp, _i64, _vp], C.c_int),
     "smc_rng_draw_streams": ([_i32, _u64, _u64, _i64, _vp, _f64, _f64, _f64, _vp, _vp], C.c_int),
@@ -126,6 +127,13 @@ def load(build_if_missing=True):
 
 def lib():
     return _lib if _lib is not None else load()
+
+
+def launch_count():
+    """Kernels the library has launched in this process (smc_launch_count)."""
+    v = C.c_uint64(0)
+    lib().smc_launch_count(C.byref(v))
+    return int(v.value)
 
 
 def last_error():

@@ -32,3 +32,10 @@ extern "C" int smc_last_error(char *buf, size_t len)
     buf[len - 1] = 0;
     return SMC_OK;
 }
+
+extern "C" int smc_launch_count(uint64_t *out)
+{
+    if (!out) return SMC_EINVAL;
+    *out = smc_launch_counter().load(std::memory_order_relaxed);
+    return SMC_OK;
+}

@@ -20,6 +20,16 @@ typedef unsigned __int128 u128;
 // returns at once.
 #define SMC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 
+// Every kernel launch of the library bumps this counter (smc_launch_count in the ABI): the bench
+// reports how many of OUR kernels ran in its timed region from it, not from a guess.
+#include <atomic>
+inline std::atomic<unsigned long long> &smc_launch_counter()
+{
+    static std::atomic<unsigned long long> c{0};
+    return c;
+}
+#define SMC_COUNT_LAUNCH() smc_launch_counter().fetch_add(1, std::memory_order_relaxed)
+
 template <typename... KArgs, typename... Args>
 inline void smc_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
 {
@@ -34,6 +44,7 @@ inline void smc_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    SMC_COUNT_LAUNCH();
 }
 
 namespace smc {

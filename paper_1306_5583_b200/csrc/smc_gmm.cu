@@ -352,6 +352,7 @@ extern "C" int smc_gmm_init(double *x, int64_t n, int r, uint64_t stream_base, u
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
     SMC_GMM_DISPATCH(r, (k_gmm_init<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, stream_base, key, ctrs,
                                                                                        data, nd, h)));
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_gmm_init");
 }
 
@@ -362,6 +363,7 @@ extern "C" int smc_gmm_eval(double *x, int64_t n, int r, const double *data, int
     const Hyper h = make_hyper(hyper, r);
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
     SMC_GMM_DISPATCH(r, (k_gmm_eval<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, data, nd, h)));
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_gmm_eval");
 }
 
@@ -381,6 +383,7 @@ extern "C" int smc_gmm_reweight(const double *x, double *lw_raw, int64_t n, doub
     LsePartial *parts = (LsePartial *)ws;
     void *scratch = (char *)ws + (((size_t)(nb + 1) * sizeof(LsePartial) + 255) & ~(size_t)255);
     k_gmm_reweight<<<nb, 256, 0, s>>>(x, lw_raw, n, dalpha, st, parts);
+    SMC_COUNT_LAUNCH();
     smc_launch_lse_finalize(parts, nb, st, n, SMC_W_ADD_LOG, 1, s, scratch, nullptr, nullptr, partial_out);
     return smc_check_launch("smc_gmm_reweight");
 }
@@ -404,5 +407,6 @@ extern "C" int smc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t strea
     else if (block == 1) { SMC_GMM_MH(1) }
     else { SMC_GMM_MH(2) }
 #undef SMC_GMM_MH
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_gmm_mh");
 }

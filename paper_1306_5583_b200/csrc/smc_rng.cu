@@ -69,6 +69,7 @@ extern "C" int smc_philox_blocks(const uint32_t *ctr4, int64_t n, uint64_t seed,
     k_philox_blocks<<<(unsigned)((n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const uint4 *>(ctr4), n, Key{(uint32_t)seed, (uint32_t)(seed >> 32)},
         reinterpret_cast<uint4 *>(out4));
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_philox_blocks");
 }
 
@@ -87,10 +88,13 @@ extern "C" int smc_rng_fill(int kind, uint64_t seed, uint64_t stream_index, uint
     uint64_t *ctr = ctrs + stream_index;
     if (kind == SMC_DRAW_GAMMA) {
         k_fill_gamma<<<1, 1, 0, s>>>(key, stream_index, ctr, shape, scale, out, n);
+        SMC_COUNT_LAUNCH();
     } else {
         const int bs = 256;
         k_fill_parallel<<<grid_for(n, bs), bs, 0, s>>>(kind, key, stream_index, ctr, mean, scale, out, n);
         k_advance<<<1, 1, 0, s>>>(ctr, (uint64_t)n * (kind == SMC_DRAW_U01 ? 1u : 2u));
+        SMC_COUNT_LAUNCH();
+        SMC_COUNT_LAUNCH();
     }
     return smc_check_launch("smc_rng_fill");
 }
@@ -107,5 +111,6 @@ extern "C" int smc_rng_draw_streams(int kind, uint64_t seed, uint64_t first_stre
     const int bs = 256;
     k_draw_streams<<<(unsigned)((n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
         kind, Key{(uint32_t)seed, (uint32_t)(seed >> 32)}, first_stream, n, ctrs, shape, mean, scale, out);
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_rng_draw_streams");
 }

@@ -179,6 +179,7 @@ extern "C" int smc_user_launch_move(void *module, uint64_t iter, double *x, int6
     const unsigned nb = (unsigned)((n + 255) / 256);
     CUresult_t cr = g_api.LaunchKernel(m->fn, nb, 1, 1, 256, 1, 1, 0, stream, args, nullptr);
     if (cr) return cu_err(cr, "smc_user_launch_move");
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_user_launch_move");
 }
 
@@ -194,5 +195,6 @@ extern "C" int smc_user_launch_eval(void *module, uint64_t iter, const double *x
     const unsigned nb = (unsigned)((n + 255) / 256);
     CUresult_t cr = g_api.LaunchKernel(m->fn, nb, 1, 1, 256, 1, 1, 0, stream, args, nullptr);
     if (cr) return cu_err(cr, "smc_user_launch_eval");
+    SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_user_launch_eval");
 }
