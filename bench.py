@@ -550,7 +550,7 @@ def resample_copy_bench(P, system, scheme, reps=10):
     x = system.value.data.clone()
     counts = torch.empty(n, dtype=torch.int32, device="cuda")
     parents = torch.empty(n, dtype=torch.int32, device="cuda")
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = torch.zeros(3, dtype=torch.int32, device="cuda")  # smc_status
     ws = torch.empty(_abi.lib().smc_resample_workspace_bytes(n), dtype=torch.uint8, device="cuda")
     rng = P.RngStreamSet(n + 1, 1306)
     from paper_1306_5583_b200.resample import _scheme
@@ -569,8 +569,8 @@ def resample_copy_bench(P, system, scheme, reps=10):
         call()
     e1.record()
     torch.cuda.synchronize()
-    if int(status.item()) != 0:
-        raise RuntimeError(f"resample+copy bench: device status {int(status.item())}")
+    if int(status[0].item()) != 0:
+        raise RuntimeError(f"resample+copy bench: device status {int(status[0].item())}")
     ms = e0.elapsed_time(e1) / reps
     moved = int((parents != torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
     byts = n * (8 + 4 + 4) + 64 * moved

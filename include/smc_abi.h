@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SMC_ABI_VERSION 1
+#define SMC_ABI_VERSION 2
 
 #define SMC_OK 0
 #define SMC_EINVAL -1         /* invalid argument                                   */
@@ -98,8 +98,19 @@ typedef struct smc_wstate {
     int32_t equal;     /* 1 after set_equal_weight                              */
     int32_t status;    /* sticky device error (SMC_E*), 0 when healthy          */
     int32_t resample;  /* decision of the last smc_ess_decide     */
-    int32_t iter;      /* free for the host loop                                */
+    int32_t err_index; /* first failing particle of `status`, as INT32_MAX - i  */
 } smc_wstate;
+
+/* Every `int32_t *status` argument of this ABI points at an smc_status record (the
+ * smc_wstate's status / resample / err_index words are one): the sticky error code,
+ * then -- 8 bytes on -- the FIRST (lowest-index) failing particle, stored as
+ * INT32_MAX - index so concurrent kernels keep the minimum with an atomic max; 0 = no
+ * particle named ("first failing particle index reported"). */
+typedef struct smc_status {
+    int32_t code;
+    int32_t reserved;
+    int32_t first_index; /* INT32_MAX - index, 0 = none */
+} smc_status;
 
 enum { SMC_W_SET_LOG = 0, SMC_W_ADD_LOG = 1, SMC_W_SET_LIN = 2, SMC_W_MUL_LIN = 3, SMC_W_EQUAL = 4 };
 enum { SMC_READ_LOG_WEIGHT = 0, SMC_READ_WEIGHT = 1 };

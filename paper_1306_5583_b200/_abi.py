@@ -32,11 +32,20 @@ ERRORS = {
 
 
 class SmcError(RuntimeError):
-    """Raised for every failure the ABI reports (host- or device-detected)."""
+    """Raised for every failure the ABI reports (host- or device-detected).  ``index`` is the
+    first (lowest-index) failing particle when the device named one."""
 
-    def __init__(self, code, msg=""):
+    def __init__(self, code, msg="", index=None):
         self.code = code
-        super().__init__(f"[{code}] {ERRORS.get(code, 'error')}{': ' + msg if msg else ''}")
+        self.index = index
+        where = f" (first failing particle {index})" if index is not None else ""
+        super().__init__(f"[{code}] {ERRORS.get(code, 'error')}{': ' + msg if msg else ''}{where}")
+
+
+def decode_index(v):
+    """smc_status.first_index (INT32_MAX - index, 0 = none) -> index or None."""
+    v = int(v)
+    return None if v <= 0 else 0x7FFFFFFF - v
 
 
 class SmcWState(C.Structure):
@@ -46,7 +55,7 @@ class SmcWState(C.Structure):
         ("lse", C.c_double), ("ess", C.c_double), ("ess_over_n", C.c_double), ("nc_inc", C.c_double),
         ("log_zconst", C.c_double), ("max_raw", C.c_double), ("log_sum", C.c_double), ("w_equal", C.c_double),
         ("equal", C.c_int32), ("status", C.c_int32),
-        ("resample", C.c_int32), ("iter", C.c_int32),
+        ("resample", C.c_int32), ("err_index", C.c_int32),
     ]
 
 

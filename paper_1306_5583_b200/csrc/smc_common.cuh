@@ -72,6 +72,16 @@ SMC_DEV void raise_status(int32_t *status, int32_t code)
     if (status) atomicCAS(reinterpret_cast<int *>(status), 0, code);
 }
 
+// ... and the first (lowest-index) failing particle: a status word is
+// followed, 8 bytes on, by its record of the first failing index, stored as INT32_MAX - index
+// so that an atomicMax keeps the lowest index and 0 means "none" (smc_abi.h, smc_status).
+SMC_DEV void raise_status_at(int32_t *status, int32_t code, int64_t index)
+{
+    if (!status) return;
+    atomicCAS(reinterpret_cast<int *>(status), 0, code);
+    if (index >= 0 && index < 0x7fffffff) atomicMax(reinterpret_cast<int *>(status + 2), 0x7fffffff - (int)index);
+}
+
 // ---------------------------------------------------------------------------
 // Warp / block scans and reductions.
 // ---------------------------------------------------------------------------
@@ -149,6 +159,16 @@ SMC_DEV void st_sector(void *p, const uint64_t (&w)[4])
                  : "memory");
 }
 
+// 64-bit words <-> items (bit casts for double, value casts for the integer types)
+template <typename T>
+SMC_DEV T from_u64(uint64_t w) { return (T)w; }
+template <>
+SMC_DEV double from_u64<double>(uint64_t w) { return __longlong_as_double((long long)w); }
+template <typename T>
+SMC_DEV uint64_t to_u64(T v) { return (uint64_t)v; }
+template <>
+SMC_DEV uint64_t to_u64<double>(double v) { return (uint64_t)__double_as_longlong(v); }
+
 template <int NT, int ITEMS, typename T>
 SMC_DEV bool vector_tile(const T *g, int64_t base, int64_t n)
 {
@@ -168,7 +188,7 @@ SMC_DEV void load_blocked(const T *__restrict__ g, int64_t base, int64_t n, T (&
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (sizeof(T) == 8) {
-                    v[c * 4 + k] = (T)w[k];
+                    v[c * 4 + k] = from_u64<T>(w[k]);
                 } else {
                     v[c * 8 + 2 * k] = (T)(uint32_t)w[k];
                     v[c * 8 + 2 * k + 1] = (T)(uint32_t)(w[k] >> 32);
@@ -199,7 +219,7 @@ SMC_DEV void store_blocked(T *__restrict__ g, int64_t base, int64_t n, const T (
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (sizeof(T) == 8)
-                    w[k] = (uint64_t)v[c * 4 + k];
+                    w[k] = to_u64<T>(v[c * 4 + k]);
                 else
                     w[k] = (uint64_t)(uint32_t)v[c * 8 + 2 * k] | ((uint64_t)(uint32_t)v[c * 8 + 2 * k + 1] << 32);
             }

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) k_gmm_reweight(const double *__restrict__
         const NormLw nl = norm_of(st);
         const double prev = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
         v = prev + dalpha * x[i * W + 13];
-        if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+        if (isnan(v) || v == INFINITY) { raise_status_at(&st->status, SMC_ENORMALIZE, i); v = -INFINITY; }
         lw_raw[i] = v;
     }
     LsePartial p = block_lse_partial<256>(v);

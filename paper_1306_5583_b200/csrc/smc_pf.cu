@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(PB) k_pf_init(double *__restrict__ x, double *
         ctrs[i] = c + 8;
         st_row(x + 4 * i, r0, r1, r2, r3);
         v = cv_llh(r0, r1, obs[0], obs[1]);
-        if (isnan(v)) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+        if (isnan(v)) { raise_status_at(&st->status, SMC_ENORMALIZE, (int64_t)si); v = -INFINITY; }
         lw_raw[i] = v;  // set_log_weight(llh)
     }
     LsePartial p = block_lse_partial<PB>(v);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
             const double incw = cv_llh(x0, x1, xo, yo, tabs.log);
             if (incw_out) incw_out[i] = incw;
             v = prev + incw;  // add_log_weight(incw)
-            if (isnan(v) || v == INFINITY) { raise_status(&st->status, SMC_ENORMALIZE); v = -INFINITY; }
+            if (isnan(v) || v == INFINITY) { raise_status_at(&st->status, SMC_ENORMALIZE, (int64_t)si); v = -INFINITY; }
             lw_raw[i] = v;
         }
         s_v[q][threadIdx.x] = v;

@@ -195,12 +195,13 @@ __global__ void __launch_bounds__(RT, RS_TILES_MINB) k_rs_tiles(int scheme, WSrc
     u128 sq = 0;
     uint64_t sqr = 0;
     int64_t sf = 0;
-    bool bad = false;
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         const int64_t i = base + j * RT + threadIdx.x;
         if (full || i < n) {
+            bool bad = false;
             const Quant qq = quantize(src.weight(r[j], nl), RES, m_out, rscale, bad);
+            if (bad) raise_status_at(status, SMC_EUNNORMALIZED, i);  // the first bad weight is reported
             sq += qq.q;
             if (RES) {
                 sqr += qq.qr;
@@ -210,11 +211,9 @@ __global__ void __launch_bounds__(RT, RS_TILES_MINB) k_rs_tiles(int scheme, WSrc
             if (MULTI) L.cnt[i] = 0;
         }
     }
-    bool badu = false;  // explicit uniforms must lie in [0, 1)
+    // explicit uniforms must lie in [0, 1) (the index reported is the uniform's)
     for (int64_t k = (int64_t)blockIdx.x * RT + threadIdx.x; u && k < n_u; k += (int64_t)gridDim.x * RT)
-        if (!(u[k] >= 0.0 && u[k] < 1.0)) badu = true;
-    if (__syncthreads_or(bad) && threadIdx.x == 0) raise_status(status, SMC_EUNNORMALIZED);
-    if (__syncthreads_or(badu) && threadIdx.x == 0) raise_status(status, SMC_EINVAL);
+        if (!(u[k] >= 0.0 && u[k] < 1.0)) raise_status_at(status, SMC_EINVAL, k);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sq += shfl_xor_u128(sq, o);
@@ -872,12 +871,13 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     int32_t c[RI];
     const uint4 ex = __ldcg(&L.tile_excl[b]);  // issued before the counts' load and scan: its latency overlaps
     load_blocked<RT, RI, int32_t>(cin, b * TILE, n, c, s_c, 1);  // coalesced; pad: not zero, no surplus
-    if (check) {  // caller-provided counts (replication_to_parents)
-        bool bad = false;
+    if (check) {  // caller-provided counts (replication_to_parents): the first negative one is reported
 #pragma unroll
         for (int j = 0; j < RI; ++j)
-            if (c[j] < 0) { bad = true; c[j] = 0; }
-        if (bad) raise_status(status, SMC_ECOUNTS);
+            if (c[j] < 0) {
+                raise_status_at(status, SMC_ECOUNTS, b * TILE + (int64_t)threadIdx.x * RI + j);
+                c[j] = 0;
+            }
     }
     uint32_t tp = 0;
     uint64_t ts = 0;

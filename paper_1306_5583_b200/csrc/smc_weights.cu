@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(WB) k_weights_pass(int mode, double *__restric
         default: v = (x >= 0.0) ? prev + log(x) : NAN; break;  // MUL_LIN
         }
         if (isnan(v) || v == INFINITY) {
-            raise_status(&st->status, SMC_ENORMALIZE);
+            raise_status_at(&st->status, SMC_ENORMALIZE, i);
             v = -INFINITY;
         }
         lw_raw[i] = v;

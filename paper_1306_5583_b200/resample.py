@@ -52,7 +52,7 @@ class Resampler:
         self.size = int(size)
         self.device = torch.device(device)
         self._ws = _abi.Workspace(self.device)
-        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(3, dtype=torch.int32, device=self.device)  # smc_status
 
     def __call__(self, scheme, *, weights=None, weight_set=None, rng=None, stream_index=None, u=None,
                  m_out=None, counts=None, parents=None, rows=None, row_bytes=0, gate=None, status=None):
@@ -81,10 +81,10 @@ class Resampler:
                   status if status is not None else ctypes.c_void_p(self.status.data_ptr()), ws, nb, _abi.stream())
 
     def check(self):
-        code = int(self.status.item())
+        code, _, first = (int(v) for v in self.status.cpu().tolist())
         if code:
             self.status.zero_()
-            raise _abi.SmcError(code, "device-side resampling failure")
+            raise _abi.SmcError(code, "device-side resampling failure", _abi.decode_index(first))
 
 
 _resamplers = {}

@@ -53,9 +53,9 @@ class WeightSet:
     def raise_if_failed(self):
         st = self.host_state()
         if st.status != 0:
-            code = st.status
+            code, idx = st.status, _abi.decode_index(st.err_index)
             self.clear_status()
-            raise _abi.SmcError(code, "device-side weight failure")
+            raise _abi.SmcError(code, "device-side weight failure", idx)
 
     def reset_log_zconst(self):
         """NormalizingConstant::initialize (PAPER.md:1808): log Z accumulator back to 0."""
@@ -63,8 +63,9 @@ class WeightSet:
         self.state[off:off + 8].zero_()
 
     def clear_status(self):
-        off = _abi.WSTATE_OFF["status"]
-        self.state[off:off + 4].zero_()
+        for f in ("status", "err_index"):
+            off = _abi.WSTATE_OFF[f]
+            self.state[off:off + 4].zero_()
 
     # -- collective mutations --------------------------------
     def _update(self, mode, values, accumulate_nc=False, check=None):

@@ -53,3 +53,47 @@ def test_after_resampling_weights_equal():
     s.iterate(2)
     w = s.system.weight_set.read_weight().cpu().numpy()
     assert np.all(w == w[0]) and abs(w.sum() - 1.0) < 1e-12  # after resampling ESS/N = 1
+
+
+def test_first_failing_particle_index_is_reported():
+    """a failing per-particle kernel reports the FIRST failing particle's
+    index (the lowest, whatever order the threads ran in) next to the error code."""
+    from paper_1306_5583_b200 import WeightSet, _abi
+    n = 100000
+    v = torch.zeros(n, dtype=torch.float64, device="cuda")
+    v[[77777, 4242, 99999]] = float("nan")
+    ws = WeightSet(n)
+    ws.set_log_weight(v, check=False)
+    with pytest.raises(_abi.SmcError) as e:
+        ws.raise_if_failed()
+    assert e.value.code == -3 and e.value.index == 4242 and "first failing particle 4242" in str(e.value)
+    ws.set_log_weight(torch.zeros(n, dtype=torch.float64, device="cuda"))  # cleared: healthy again
+
+
+def test_resample_reports_first_bad_weight_and_negative_count():
+    from paper_1306_5583_b200 import _abi, replication_to_parents, resample
+    n = 50000
+    w = torch.full((n,), 1.0 / n, dtype=torch.float64, device="cuda")
+    w[31337] = -1.0 / n
+    w[40000] = float("nan")
+    with pytest.raises(_abi.SmcError) as e:
+        resample("stratified", w, u=torch.rand(n, dtype=torch.float64, device="cuda"))
+    assert e.value.code == -2 and e.value.index == 31337
+    c = torch.ones(n, dtype=torch.int32, device="cuda")
+    c[[12345, 23456]] = -1
+    c[[1, 2]] = 2
+    with pytest.raises(_abi.SmcError) as e:
+        replication_to_parents(c)
+    assert e.value.code == -5 and e.value.index == 12345
+
+
+def test_pf_move_reports_the_particle_whose_weight_failed():
+    """A non-finite observation makes every particle's likelihood NaN: particle 0 is the first."""
+    from paper_1306_5583_b200 import _abi, pf
+    obs, _ = pf.generate_observations(4, 3)
+    obs[2, 0] = float("nan")
+    s = pf.make_sampler(5000, "systematic", 0.5, seed=3)
+    s.initialize(obs)
+    with pytest.raises(_abi.SmcError) as e:
+        s.iterate(2)
+    assert e.value.code == -3 and e.value.index == 0

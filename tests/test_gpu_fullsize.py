@@ -91,6 +91,7 @@ def test_pf_2e24_100_obs_resampling_bit_exact_every_step(scheme):
     from paper_1306_5583_b200 import pf
     obs, _ = pf.generate_observations(100, 1306)
     s = pf.make_sampler(N, scheme, 0.5, seed=1306)
+    s.graph = False  # the hook reads the weights back on the host at every step
     hook = _LockstepResampler(s.system.resampler, scheme)
     s.system.resampler = hook
     s.initialize(obs)

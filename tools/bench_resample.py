@@ -59,7 +59,7 @@ def main():
         counts = torch.empty(n, dtype=torch.int32, device="cuda")
         parents = torch.empty(n, dtype=torch.int32, device="cuda")
         ws = torch.empty(_abi.lib().smc_resample_workspace_bytes(n), dtype=torch.uint8, device="cuda")
-        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        status = torch.zeros(3, dtype=torch.int32, device="cuda")  # smc_status
         rng = P.RngStreamSet(n + 1, 1306)
         kinds = args.kinds.split(",")
         for kind in kinds:
@@ -83,7 +83,7 @@ def main():
                     call()
                 e1.record()
                 torch.cuda.synchronize()
-                assert int(status.item()) == 0
+                assert int(status[0].item()) == 0
                 ms = e0.elapsed_time(e1) / reps
                 moved = int((parents != torch.arange(n, device="cuda", dtype=torch.int32)).sum().item())
                 byts = n * 16 + 64 * moved
