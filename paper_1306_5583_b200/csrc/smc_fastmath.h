@@ -271,6 +271,12 @@ SMC_HD double exp(double x, const ExpEntry *tab)
 // exp(x) for x <= 0 with the table: no overflow side and no subnormal results
 // (below 2^-1022 it flushes to +0) -- for sums whose largest term is exp(0) = 1,
 // where anything that small is far below their rounding (the GMM likelihood).
+// The constants a DFMA cannot take as an immediate (low mantissa word nonzero): as
+// immediates they cost two UMOVs each -- free in a loop that hoists them (the GMM
+// likelihood), not in straight-line code evaluating many items (the resampling weights),
+// which takes them from the constant bank instead (exp_nonpos_cb: same bits).
+SMC_CONSTANT double kExpNpK[8] = {0x1.71547652b82fep+7, 0x1.62e42fefc0000p-8, -0x1.c610ca86c3899p-44,
+                                  1.0 / 120, 1.0 / 24, 1.0 / 6, 0.0, 0.0};
 SMC_HD double exp_nonpos(double x, const ExpEntry *tab)
 {
     const double SH = 0x1.8p52;
@@ -281,6 +287,25 @@ SMC_HD double exp_nonpos(double x, const ExpEntry *tab)
     r = fma_(-kd, -0x1.c610ca86c3899p-44, r);
     double p = fma_(r, 1.0 / 120, 1.0 / 24);
     p = fma_(r, p, 1.0 / 6);
+    p = fma_(r, p, 0.5);
+    p = fma_(r * r, p, r);
+    const ExpEntry t = tab[k & 127];
+    const double m = fma_(t.hi, p, t.lo) + t.hi;
+    const double res = from_bits(bits(m) + ((uint64_t)(k >> 7) << 52));
+    return x < -708.0 ? 0.0 : res;  // -inf included
+}
+
+// exp_nonpos with its non-immediate constants from the constant bank (same bits).
+SMC_HD double exp_nonpos_cb(double x, const ExpEntry *tab)
+{
+    const double SH = 0x1.8p52;
+    double kd = fma_(x, kExpNpK[0], SH);
+    const int64_t k = (int32_t)(uint32_t)bits(kd);
+    kd -= SH;
+    double r = fma_(-kd, kExpNpK[1], x);
+    r = fma_(-kd, kExpNpK[2], r);
+    double p = fma_(r, kExpNpK[3], kExpNpK[4]);
+    p = fma_(r, p, kExpNpK[5]);
     p = fma_(r, p, 0.5);
     p = fma_(r * r, p, r);
     const ExpEntry t = tab[k & 127];

@@ -37,7 +37,7 @@ namespace {
 
 constexpr int RT = 256;
 #ifndef RS_TILES_MINB
-#define RS_TILES_MINB 8  // pass A: 8 blocks/SM (32 registers; same-box A/B 0.227 -> 0.212 ms resample)
+#define RS_TILES_MINB 6  // pass A: 6 blocks/SM (40 registers, no spills of the branch-free item loop)
 #endif
 #ifndef RS_COUNTS_MINB
 #define RS_COUNTS_MINB 5  // pass B1 blocks per SM the register allocation must allow (same-box A/B: 5 > 6 > 4)
@@ -78,6 +78,7 @@ struct Layout {
     uint4 *tile_excl;   // per slot tile: exclusive (Z, S, P) prefix
     int32_t *anchor, *sp_idx, *sp_start;  // anchor[k]: surplus parent covering rank k*ANCHOR
     int32_t *tile_z0;   // per slot tile: its first zero rank (and Z at index nt)
+    uint32_t *zmask;    // zero-count slots, one bit per slot (TILE / 32 words per tile), for pass C
     uint64_t *qfull;
     int32_t *cnt;       // multinomial histogram, then the counts when the caller passes none
     uint32_t *mn_cnt, *mn_off, *mn_fill;  // multinomial: draws per position bin, offsets, fill pointers
@@ -115,6 +116,7 @@ Layout layout(void *ws, int64_t n)
     L.sp_idx = (int32_t *)take(sizeof(int32_t) * (n + 1));  // P <= n even for invalid counts
     L.sp_start = (int32_t *)take(sizeof(int32_t) * (n + 2));
     L.tile_z0 = (int32_t *)take(sizeof(int32_t) * (nt + 2));
+    L.zmask = (uint32_t *)take(sizeof(uint32_t) * nt * (TILE / 32));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
     const int64_t nbins = mn_bins(n);
@@ -139,12 +141,32 @@ struct WSrc {
         if (w) return __ldg(w + i);
         return nl.eq ? 0.0 : __ldg(lw + i);
     }
-    SMC_DEV double weight(double r, const NormLw &nl) const  // the math
+    SMC_DEV double weight(double r, const NormLw &nl, const smc_fm::ExpEntry *tab = smc_fm::kExpTab) const
     {
         if (w) return r;
-        // table-free polynomial exp (<= 1 ulp; no lookups, no branches, coefficients
-        // from the constant bank): 8 independent calls per thread
-        return nl.eq ? nl.weq : smc_fm::exp_weight(nl(r));
+        return weight_of_lw(r, nl, tab);
+    }
+    // W = exp(lw - lse): the table exp (<= 0.52 ulp, 6 fp64 operations fewer than a
+    // table-free polynomial; below 2^-1022 it flushes to +0, which is what floor(W 2^63)
+    // makes of it anyway).  smc_weights_read uses this same function, so the weights a
+    // caller reads are bit for bit the ones the resampler quantizes.
+    SMC_DEV static double weight_of_lw(double r, const NormLw &nl, const smc_fm::ExpEntry *tab)
+    {
+        return nl.eq ? nl.weq : smc_fm::exp_nonpos_cb(nl(r), tab);
+    }
+};
+
+// The exp table (2 KB) staged in shared memory by a block: requested before the
+// dependency wait (constant data), stored, and published by the block's next barrier.
+struct ExpTabStage {
+    double2 v;
+    SMC_DEV void load()
+    {
+        if (threadIdx.x < 128) v = __ldg(reinterpret_cast<const double2 *>(smc_fm::kExpTab) + threadIdx.x);
+    }
+    SMC_DEV void store(smc_fm::ExpEntry *t) const
+    {
+        if (threadIdx.x < 128) reinterpret_cast<double2 *>(t)[threadIdx.x] = v;
     }
 };
 
@@ -176,39 +198,73 @@ SMC_DEV Quant quantize(double W, bool residual, double m_out, double rscale, boo
 }
 
 // ------------------------------------------------------------------ pass A --
-template <bool RES, bool MULTI>  // residual family / multinomial histogram: resolved at compile time
+// LW: the weights come from the raw log weights + the weight record (the sampler's
+// path: the table exp staged in shared memory); otherwise from an explicit W vector.
+template <bool RES, bool MULTI, bool LW>  // scheme family and weight source: resolved at compile time
 __global__ void __launch_bounds__(RT, RS_TILES_MINB) k_rs_tiles(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                  const double *__restrict__ u, int64_t n_u, const int32_t *gate,
                                                  int32_t *status, Layout L)
 {
+    __shared__ smc_fm::ExpEntry s_tab[128];
+    ExpTabStage ts;
+    if (LW) ts.load();
     SMC_PDL_WAIT();
     if (gate && *gate == 0) return;
     const int64_t base = (int64_t)blockIdx.x * TILE;
     const NormLw nl = src.norm();
     const bool full = base + TILE <= n;  // no per-element bounds checks on full tiles
+    const int rem = full ? TILE : (int)(n - base);
+    // 32-bit offsets from the tile's base pointers (no 64-bit index arithmetic per element)
+    const double *g = LW ? (nl.eq ? nullptr : src.lw + base) : src.w + base;
+    uint64_t *qb = L.qfull + base;
     double r[RI];
 #pragma unroll
     for (int j = 0; j < RI; ++j) {  // striped: each warp load is 256 contiguous bytes; all issued up front
-        const int64_t i = base + j * RT + threadIdx.x;
-        r[j] = (full || i < n) ? src.raw(i, nl) : 0.0;
+        const int li = j * RT + threadIdx.x;
+        r[j] = (g && (full || li < rem)) ? __ldg(g + li) : 0.0;
+    }
+    if (LW) {
+        ts.store(s_tab);
+        __syncthreads();
     }
     u128 sq = 0;
     uint64_t sqr = 0;
     int64_t sf = 0;
+    bool anybad = false;
+    // branch-free over the RI items (items past the end: W = 0, q = 0; stores predicated); a bad
+    // weight (NaN, < 0, > 1) fails the call, so what it adds to the sums does not matter
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
-        const int64_t i = base + j * RT + threadIdx.x;
-        if (full || i < n) {
+        const int li = j * RT + threadIdx.x;
+        const bool in = full || li < rem;
+        double W = LW ? WSrc::weight_of_lw(r[j], nl, s_tab) : r[j];
+        W = in ? W : 0.0;
+        const uint64_t wb = smc_fm::bits(W);
+        anybad |= wb > 0x3FF0000000000000ull && wb != 0x8000000000000000ull;
+        const uint64_t q = (uint64_t)(W * 9223372036854775808.0);  // floor(W 2^63), A.1
+        uint64_t qr = 0;
+        sq += q;
+        if (RES) {
+            const double x = m_out * W;  // fl(M W_i), exactly rounded (no FMA: --fmad=false)
+            const double f = floor(x);
+            qr = (uint64_t)((x - f) * rscale);
+            sqr += qr;
+            sf += (int64_t)f;
+        }
+        if (in) {
+            qb[li] = RES ? qr : q;  // the searched quantity, for passes M and B1
+            if (MULTI) L.cnt[base + li] = 0;
+        }
+    }
+    if (__any_sync(0xffffffffu, anybad)) {  // rare: name the first bad weight
+#pragma unroll
+        for (int j = 0; j < RI; ++j) {
+            const int li = j * RT + threadIdx.x;
+            if (!(full || li < rem)) continue;
+            const double rr = g ? __ldg(g + li) : 0.0;  // reloaded: the item registers are not kept live
             bool bad = false;
-            const Quant qq = quantize(src.weight(r[j], nl), RES, m_out, rscale, bad);
-            if (bad) raise_status_at(status, SMC_EUNNORMALIZED, i);  // the first bad weight is reported
-            sq += qq.q;
-            if (RES) {
-                sqr += qq.qr;
-                sf += qq.f;
-            }
-            L.qfull[i] = RES ? qq.qr : qq.q;  // the searched quantity, for passes M and B1
-            if (MULTI) L.cnt[i] = 0;
+            quantize(LW ? WSrc::weight_of_lw(rr, nl, s_tab) : rr, RES, m_out, rscale, bad);
+            if (bad) raise_status_at(status, SMC_EUNNORMALIZED, base + li);
         }
     }
     // explicit uniforms must lie in [0, 1) (the index reported is the uniform's)
@@ -217,8 +273,10 @@ __global__ void __launch_bounds__(RT, RS_TILES_MINB) k_rs_tiles(int scheme, WSrc
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sq += shfl_xor_u128(sq, o);
-        sqr += __shfl_xor_sync(0xffffffffu, sqr, o);
-        sf += __shfl_xor_sync(0xffffffffu, sf, o);
+        if (RES) {
+            sqr += __shfl_xor_sync(0xffffffffu, sqr, o);
+            sf += __shfl_xor_sync(0xffffffffu, sf, o);
+        }
     }
     __shared__ u128 s_q[RT / 32];
     __shared__ uint64_t s_qr[RT / 32];
@@ -242,10 +300,14 @@ inline void launch_tiles(int scheme, unsigned nt, cudaStream_t s, WSrc src, int6
 {
     const bool res = scheme == SMC_RESIDUAL || scheme == SMC_RESIDUAL_STRATIFIED || scheme == SMC_RESIDUAL_SYSTEMATIC;
     const bool multi = scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL;
-    if (res && multi) smc_launch(k_rs_tiles<true, true>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
-    else if (res) smc_launch(k_rs_tiles<true, false>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
-    else if (multi) smc_launch(k_rs_tiles<false, true>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
-    else smc_launch(k_rs_tiles<false, false>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L);
+#define SMC_TILES(R_, M_)                                                                                              \
+    (src.w ? smc_launch(k_rs_tiles<R_, M_, false>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L) \
+           : smc_launch(k_rs_tiles<R_, M_, true>, nt, RT, 0, s, scheme, src, n, mo, rscale, u, n_u, gate, status, L))
+    if (res && multi) SMC_TILES(true, true);
+    else if (res) SMC_TILES(true, false);
+    else if (multi) SMC_TILES(false, true);
+    else SMC_TILES(false, false);
+#undef SMC_TILES
 }
 
 // ------------------------------------------------------------------ pass S --
@@ -745,6 +807,8 @@ SMC_DEV uint64_t F_fast(const StratCtx &c, uint64_t X)
 template <bool SYS>
 SMC_DEV uint64_t F_fast_flag(const StratCtx &c, uint64_t X, bool &ex)
 {
+    // (a conversion-free variant -- X and floor(z) through the 2^52 shifter -- measured slower:
+    // 12 fp64 operations per item instead of 3 conversions, the same pipe time, more issue slots)
     const double z = (double)X * c.ratio;
     const double fl = floor(z);
     const double fr = z - fl;
@@ -786,6 +850,21 @@ SMC_DEV void tile_aggregate(const int32_t (&c)[RI], int64_t b, const Layout &L)
     uint64_t agg;
     block_exclusive_sum<RT, uint64_t>(pack_zsp(tz, tp, ts), sm, &agg);
     if (threadIdx.x == 0) L.tile_zsp[b] = agg;
+}
+
+// The tile's zero-count slots as a bitmask: thread t's RI = 8 slots are byte t, four threads per
+// 32-bit word, 64 words per tile (one coalesced 256-byte store).  Padding slots hold 1: not zero.
+SMC_DEV void zero_mask(const int32_t (&c)[RI], int64_t b, const Layout &L)
+{
+    static_assert(RI == 8, "one byte of zero flags per thread");
+    uint32_t zb = 0;
+#pragma unroll
+    for (int j = 0; j < RI; ++j) zb |= (uint32_t)(c[j] == 0) << j;
+    const int lane = threadIdx.x & 31;
+    uint32_t wv = zb << (8 * (lane & 3));
+    wv |= __shfl_xor_sync(0xffffffffu, wv, 1);
+    wv |= __shfl_xor_sync(0xffffffffu, wv, 2);
+    if ((lane & 3) == 0) L.zmask[b * (TILE / 32) + (threadIdx.x >> 2)] = wv;
 }
 
 // One block: exclusive (Z, S, P) prefix of the tile aggregates, the totals, each
@@ -935,6 +1014,7 @@ __global__ void __launch_bounds__(RT) k_rs_aggs(const int32_t *__restrict__ cin,
     load_blocked<RT, RI, int32_t>(cin, (int64_t)blockIdx.x * TILE, n, c, s_c, 1);
 #pragma unroll
     for (int j = 0; j < RI; ++j) c[j] = c[j] < 0 ? 0 : c[j];  // k_rs_ranks raises ECOUNTS
+    zero_mask(c, blockIdx.x, L);
     tile_aggregate(c, blockIdx.x, L);
 }
 
@@ -1064,7 +1144,10 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
     }
     __syncthreads();  // s_fb may still be read by the residual staging path
     store_blocked<RT, RI, int32_t>(counts, tbase, n, c, s_fb);  // coalesced
-    if (ranks) tile_aggregate(c, b, L);  // the parent map's per-tile (Z, S, P) for k_rs_zsp_scan
+    if (ranks) {
+        zero_mask(c, b, L);   // pass C's zero slots: 1 bit per slot instead of re-reading the counts
+        tile_aggregate(c, b, L);  // the parent map's per-tile (Z, S, P) for k_rs_zsp_scan
+    }
 }
 
 inline void launch_counts(int scheme, unsigned nt, cudaStream_t s, WSrc src, int64_t n, double mo, double rscale,
@@ -1139,28 +1222,33 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
 {
     SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
-    if (!h->active) return;
-    if (h->trivial) {
+    const int64_t t = blockIdx.x;
+    // every load that does not depend on another issued together, before the first branch: the
+    // block's chain of dependent round trips (header / zero ranks -> anchors -> staged slice) is
+    // its whole cost (a latency-bound pass), so the first trip carries all of them
+    const int32_t active = h->active, trivial = h->trivial;
+    const int64_t z0 = __ldcg(&L.tile_z0[t]), z1 = __ldcg(&L.tile_z0[t + 1]);  // local zero ranks
+    const int64_t Zl = h->Z_total, Sl = h->S_total, P = h->P_total;
+    const uint32_t zword = __ldcg(&L.zmask[t * (TILE / 32) + (threadIdx.x >> 2)]);
+    if (!active) return;
+    if (trivial) {
         if (blockIdx.x == 0 && threadIdx.x == 0) parents[0] = 0;
         return;
     }
     __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
     __shared__ int32_t s_io[tile_smem_elems<int32_t, RT, RI>()];
     __shared__ uint32_t sm32[RT / 32 + 1];
-    const int64_t t = blockIdx.x;
     const int64_t tbase = t * TILE;
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;
-    const int64_t z0 = __ldcg(&L.tile_z0[t]), z1 = __ldcg(&L.tile_z0[t + 1]);  // local zero ranks
-    const int64_t Zl = h->Z_total, Sl = h->S_total, P = h->P_total;
     const int64_t s_self = sc.s_self < 0 ? Sl : sc.s_self;
     const int64_t soff = sc.soff, zoff = sc.zoff;
     // length of this shard's local piece [soff, soff+s_self) ∩ [zoff, zoff+Zl) in global ranks
     const int64_t piece = max((int64_t)0, min(zoff + Zl, soff + s_self) - max(zoff, soff));
-    int32_t c[RI];
-    load_blocked<RT, RI, int32_t>(cin, tbase, n, c, s_io, 1);  // coalesced
-    uint32_t nz = 0;
-#pragma unroll
-    for (int j = 0; j < RI; ++j) nz += (c[j] == 0);
+    // this thread's RI slots: one byte of the tile's zero-slot bitmask (pass B1); padding bits are 0
+    (void)cin;
+    const uint32_t zb = (zword >> (8 * (threadIdx.x & 3))) & 0xFFu;
+    auto zero = [&](int j) { return ((zb >> j) & 1u) != 0; };
+    const uint32_t nz = __popc(zb);
     // local surplus ranks this tile needs: [lo_s, hi_s)
     const int64_t lo_s = max(zoff + z0, soff) - soff, hi_s = min(zoff + z1, soff + s_self) - soff;
     uint32_t cnt = 0;
@@ -1224,7 +1312,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
 #pragma unroll
         for (int j = 0; j < RI; ++j) {
             par[j] = b32 + j;  // survivors keep their slot
-            if (c[j] == 0) par[j] = s_par[g++];
+            if (zero(j)) par[j] = s_par[g++];
         }
         if (COPY32) {  // 4 row loads in flight per thread, then their stores
             double *rows = (double *)sc.rows;
@@ -1233,10 +1321,10 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
                 double4 v[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (c[j0 + j] == 0) ld256(rows + (int64_t)par[j0 + j] * 4, v[j]);
+                    if (zero(j0 + j)) ld256(rows + (int64_t)par[j0 + j] * 4, v[j]);
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
-                    if (c[j0 + j] == 0) st256(rows + (base + j0 + j) * 4, v[j]);
+                    if (zero(j0 + j)) st256(rows + (base + j0 + j) * 4, v[j]);
             }
         }
     } else {
@@ -1253,7 +1341,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
 #pragma unroll
         for (int j = 0; j < RI; ++j) {
             par[j] = (int32_t)(base + j);
-            if (c[j] == 0) {
+            if (zero(j)) {
                 if (g >= soff && g < soff + s_self) {
                     const int64_t s = g - soff;
                     while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;

@@ -205,9 +205,9 @@ __global__ void k_weights_read(int what, const double *__restrict__ lw_raw, cons
     const NormLw nl = norm_of(st);
     const double l = nl(nl.needs_raw() ? lw_raw[i] : 0.0);
     // equal weights are exp(-log N): N is the GLOBAL count of a sharded system.  W = exp(lw) by
-    // the same function the resampling kernels use (smc_fm::exp_weight, <= 1 ulp): the weights a
+    // the same function the resampling kernels use (the table exp, <= 0.52 ulp): the weights a
     // caller reads are bit-for-bit the weights smc_resample quantizes
-    out[i] = what == SMC_READ_WEIGHT ? (nl.eq ? nl.weq : smc_fm::exp_weight(l)) : l;
+    out[i] = what == SMC_READ_WEIGHT ? (nl.eq ? nl.weq : smc_fm::exp_nonpos_cb(l, smc_fm::kExpTab)) : l;
 }
 
 // SPEC.md:266 / SURVEY R8: threshold >= 1 always, <= 0 never, else ess/N < threshold.

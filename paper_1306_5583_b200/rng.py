@@ -3,8 +3,9 @@
 Same streams, same numbers: stream ``i`` of ``RngStreamSet(size, seed)`` is
 Philox4x32-10 keyed by the seed, counter (draw_lo, draw_hi, i_lo, i_hi)
 (rng.py:59-82).  Uniforms are bit-identical to the reference; normals and
-gammas use the same algorithms (rng.py:85-117) with CUDA libdevice
-transcendentals, so they agree with glibc to a few ulp.
+gammas use the same algorithms (rng.py:85-117) with the branch-free fp64
+pieces of smc_fastmath.h (table log, cos_bm, sqrt_bm; libdevice pow for the
+gamma boost), so they agree with glibc to a few ulp.
 
 The per-stream draw counters live in device memory (``counters``, uint64
 stored as int64), so particle kernels advance them without host traffic.

@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_cos_bm, lib.fm_sqrt_bm, lib.fm_div10):
+    for f in (lib.fm_log, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_exp_nonpos_cb, lib.fm_cos_bm, lib.fm_sqrt_bm, lib.fm_div10):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -201,3 +201,12 @@ def test_div10_matches_ieee_division(fm):
     np.testing.assert_array_equal(got, a / 10.0)
     edge = fm("fm_div10", np.array([np.inf, np.nan]))
     assert edge[0] == np.inf and np.isnan(edge[1])
+
+
+def test_exp_nonpos_constant_bank_variant_is_bit_identical(fm):
+    """exp_nonpos_cb (resampling weights, read_weight) takes its constants from the constant bank;
+    exp_nonpos (GMM) from immediates: the same bits for every input."""
+    rng = np.random.default_rng(11)
+    x = np.concatenate([-rng.exponential(3, 200000), -rng.uniform(0, 750, 20000), [0.0, -0.0, -708.0, -709, -np.inf]])
+    a, b = fm("fm_exp_nonpos", x), fm("fm_exp_nonpos_cb", x)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))

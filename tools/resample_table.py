@@ -8,7 +8,8 @@ import sys
 
 SCHEMES = ["systematic", "stratified", "multinomial", "residual", "residual_stratified", "residual_systematic"]
 rows = [json.loads(l) for l in open(sys.argv[1]) if l.strip()]
-peak = 6547.8
+import json as _json, os as _os
+peak = _json.load(open(_os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
 print("# Config 5: resample + in-place copy via smc_resample (counts + parents + 32-byte row copy fused into pass C),")
 print("# 1 B200, CUDA events, mean of 20 calls (5 at 2^26+); cell = GB/s | ms, GB/s = algorithmic bytes (N*(8 W +")
 print(f"# 4 counts + 4 parents) + 64 per moved row) / time; HBM peak {peak} GB/s (MEASURED_PEAKS.json).")

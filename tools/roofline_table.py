@@ -7,7 +7,8 @@ with the ncu-measured DRAM traffic beside it.
 import sys
 
 N = 1 << 24
-PEAK = 6547.8  # GB/s, MEASURED_PEAKS.json
+import json as _json, os as _os
+PEAK = _json.load(open(_os.path.join(_os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]  # GB/s
 # algorithmic bytes per launch (DESIGN.md §6 table; the move after a resample: lw is not read)
 ALG = {
     "k_pf_move": N * (32 + 32 + 4 + 8 + 8 + 8),
@@ -42,7 +43,7 @@ for line in open(sys.argv[2]):
     k = key(parts[0] if parts[0] != "void" else parts[1])
     if k:
         ncu[k] = (float(parts[-3]), float(parts[-2]), float(parts[-1]))
-print("# per-kernel HBM roofline, one PF step at N = 2^24 (systematic, resampled every step); peak 6547.8 GB/s")
+print(f"# per-kernel HBM roofline, one PF step at N = 2^24 (systematic, resampled every step); peak {PEAK} GB/s")
 print("# alg = algorithmic bytes per launch (DESIGN.md §6); chain = time in the bench's PF step (launch list, last")
 print("# launch); ncu = cold serialized time and DRAM bytes from the ncu --set full capture")
 print(f"{'kernel':16s} {'alg MB':>8s} {'chain us':>9s} {'GB/s':>7s} {'frac':>6s} {'ncu us':>8s} {'DRAM MB':>8s} {'DRAM GB/s':>9s}")
