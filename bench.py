@@ -251,6 +251,9 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        # NCCL's own INFO log (ranks, rings / NVLS, P2P transport) stays on so the run shows what
+        # the communicator set up (stderr; the JSON line stays the last stdout line)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         if functional:
             dist.init_process_group("gloo")
         else:

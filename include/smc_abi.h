@@ -220,6 +220,18 @@ int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64_t zoff, in
                               const void *recv, void *rows, int64_t row_bytes, int32_t *parents, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* The same assignment with the cross-shard rows read straight from the other ranks' memory
+ * (CUDA-IPC mappings, P2P loads over NVLink/NVSwitch) instead of a packed send/receive:
+ * zsp_all = the allgathered smc_resample_shard_counts outputs (G x {Z, S, P, active}, device),
+ * peer_ws[r] / peer_rows[r] = rank r's resample workspace and current state buffer (host
+ * arrays of G device pointers; the own rank's entries are its own buffers).  Every offset
+ * comes from zsp_all on the device: no host plan and no host synchronization per step.
+ * The allgather that delivered zsp_all orders this call after every peer's counts pass.
+ * Replaces the row-migration step of PAPER.md:1993-2059 (vSMC MPI module). */
+int smc_resample_shard_assign_p2p(const uint32_t *zsp_all, int G, int rank, const void *const *peer_ws,
+                                  const void *const *peer_rows, int64_t n, void *rows, int64_t row_bytes,
+                                  int32_t *parents, int32_t *status, void *ws, size_t ws_bytes, void *stream);
+
 /* replication_to_parents(counts) from a device counts vector. */
 int smc_replication_to_parents(const int32_t *counts, int64_t n, int32_t *parents, int32_t *status, void *ws,
                                size_t ws_bytes, void *stream);

@@ -89,6 +89,7 @@ _SIGS = {
                                    _i64, _vp, _vp, _vp, _vp, _sz, _vp, _vp], C.c_int),
     "smc_resample_shard_pack": ([_vp, _i64, _i64, _vp, _i32, _vp, _vp, _sz, _vp], C.c_int),
     "smc_resample_shard_assign": ([_vp, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp], C.c_int),
+    "smc_resample_shard_assign_p2p": ([_vp, _i32, _i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_replication_to_parents": ([_vp, _i64, _vp, _vp, _vp, _sz, _vp], C.c_int),
     "smc_gather_rows": ([_vp, _vp, _i64, _vp, _i64, _vp], C.c_int),
     "smc_copy_rows_inplace": ([_vp, _i64, _vp, _i64, _vp, _vp], C.c_int),
@@ -127,6 +128,8 @@ def load(build_if_missing=True):
                 raise ImportError(f"{_build.LIB} is missing: the CUDA library is required (no CPU fallback)")
             L = C.CDLL(_build.LIB)
             for name, (args, res) in _SIGS.items():
+                if os.environ.get("SMC_LIB_PATH") and not hasattr(L, name):
+                    continue  # an older A/B variant without a newer entry point
                 f = getattr(L, name)
                 f.argtypes = args
                 f.restype = res

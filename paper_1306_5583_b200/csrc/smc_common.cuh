@@ -19,6 +19,14 @@ typedef unsigned __int128 u128;
 // visible), so stream-order semantics are unchanged.  Without the attribute the wait
 // returns at once.
 #define SMC_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+// ... and a kernel may let its dependent launch before it finishes (the dependent still waits in
+// SMC_PDL_WAIT for this grid's completion and memory): used after a block's main loop, so the
+// next kernel's blocks get rasterized while the last wave finishes its reductions
+#ifndef SMC_NO_PDL_TRIGGER
+#define SMC_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+#else
+#define SMC_PDL_TRIGGER() do { } while (0)
+#endif
 
 // Every kernel launch of the library bumps this counter (smc_launch_count in the ABI): the bench
 // reports how many of OUR kernels ran in its timed region from it, not from a guess.

@@ -277,7 +277,10 @@ SMC_HD double exp(double x, const ExpEntry *tab)
 // which takes them from the constant bank instead (exp_nonpos_cb: same bits).
 SMC_CONSTANT double kExpNpK[8] = {0x1.71547652b82fep+7, 0x1.62e42fefc0000p-8, -0x1.c610ca86c3899p-44,
                                   1.0 / 120, 1.0 / 24, 1.0 / 6, 0.0, 0.0};
-SMC_HD double exp_nonpos(double x, const ExpEntry *tab)
+// (stride, off): the table may be replicated -- entry k of copy `off` at tab[k stride + off]
+// (the GMM kernel keeps 8 copies interleaved so that the 8 lanes of an LDS.128 phase read 8
+// different bank groups: no bank conflicts whatever the indices).  Same bits either way.
+SMC_HD double exp_nonpos(double x, const ExpEntry *tab, int stride = 1, int off = 0)
 {
     const double SH = 0x1.8p52;
     double kd = fma_(x, 0x1.71547652b82fep+7, SH);
@@ -289,7 +292,7 @@ SMC_HD double exp_nonpos(double x, const ExpEntry *tab)
     p = fma_(r, p, 1.0 / 6);
     p = fma_(r, p, 0.5);
     p = fma_(r * r, p, r);
-    const ExpEntry t = tab[k & 127];
+    const ExpEntry t = tab[(k & 127) * stride + off];
     const double m = fma_(t.hi, p, t.lo) + t.hi;
     const double res = from_bits(bits(m) + ((uint64_t)(k >> 7) << 52));
     return x < -708.0 ? 0.0 : res;  // -inf included

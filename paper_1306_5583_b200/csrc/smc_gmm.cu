@@ -67,6 +67,14 @@ SMC_DEV double log_likelihood_direct(const Param<R> &p, const double *__restrict
     return ll;
 }
 
+// The exp table in shared memory as TAB_COPIES interleaved copies (entry k of copy c at
+// k * TAB_COPIES + c; each thread reads copy threadIdx % TAB_COPIES): an LDS.128 serves a
+// warp in phases of 8 lanes, and 8 lanes reading 8 different copies hit 8 different bank
+// groups -- the random exp indices no longer conflict (the single table measured 764 M of
+// 1322 M shared wavefronts as conflicts, profiles/r1_ncu_gmm_mh.txt).
+constexpr int TAB_COPIES = 8;
+constexpr size_t TAB_BYTES = 128 * TAB_COPIES * sizeof(smc_fm::ExpEntry);
+
 template <int R>
 SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, int nd,
                               const smc_fm::ExpEntry *__restrict__ tab)
@@ -104,7 +112,8 @@ SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, i
             // (selected around the first maximum, in component order)
             double S = 1.0;
 #pragma unroll
-            for (int j = 0; j + 1 < R; ++j) S += smc_fm::exp_nonpos((j < im ? x[j] : x[j + 1]) - m, tab);
+            for (int j = 0; j + 1 < R; ++j)
+                S += smc_fm::exp_nonpos((j < im ? x[j] : x[j + 1]) - m, tab, TAB_COPIES, (int)(threadIdx.x % TAB_COPIES));
             msum += m;
             prod *= S;  // prod in [1, 2) times S in [1, R]: normal; peel the exponent off
             const uint64_t pb = smc_fm::bits(prod);
@@ -115,7 +124,7 @@ SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, i
             // rounded into the subnormal range and a zero sum giving -inf, as libm does
             double lli = 0.0;
 #pragma unroll
-            for (int j = 0; j < R; ++j) lli += smc_fm::exp(x[j], tab);
+            for (int j = 0; j < R; ++j) lli += smc_fm::exp(x[j], smc_fm::kExpTab);
             far.add(lli);
         }
     }
@@ -142,11 +151,10 @@ SMC_DEV double log_prior(const Param<R> &p, const Hyper &h)
 }
 
 // Shared memory: the exp table (2 KB) then the data (nd doubles, <= 32 KB).
-constexpr size_t TAB_BYTES = 128 * sizeof(smc_fm::ExpEntry);
 
 SMC_DEV void stage_data(const double *__restrict__ data, int nd, smc_fm::ExpEntry *s_tab, double *s_y)
 {
-    for (int k = threadIdx.x; k < 128; k += blockDim.x) s_tab[k] = smc_fm::kExpTab[k];
+    for (int k = threadIdx.x; k < 128 * TAB_COPIES; k += blockDim.x) s_tab[k] = smc_fm::kExpTab[k / TAB_COPIES];
     for (int k = threadIdx.x; k < nd; k += blockDim.x) s_y[k] = data[k];
     __syncthreads();
 }
@@ -333,6 +341,14 @@ int gmm_check(const double *x, int64_t n, int r, const double *data, int nd, con
 }  // namespace
 
 // r -> template instantiation (r = 1..SMC_GMM_MAX_R)
+// more than 48 KB of dynamic shared memory (4096 data points + the replicated exp table) needs
+// the kernel's opt-in, set on every launch that asks for it (cheap, host-side)
+template <class K>
+inline void allow_smem(K kern, size_t bytes)
+{
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 #define SMC_GMM_DISPATCH(r, CALL)          \
     switch (r) {                            \
     case 1: { constexpr int R = 1; CALL; } break; \
@@ -350,7 +366,7 @@ extern "C" int smc_gmm_init(double *x, int64_t n, int r, uint64_t stream_base, u
     const Key key{(uint32_t)seed, (uint32_t)(seed >> 32)};
     const Hyper h = make_hyper(hyper, r);
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
-    SMC_GMM_DISPATCH(r, (k_gmm_init<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, stream_base, key, ctrs,
+    SMC_GMM_DISPATCH(r, (allow_smem(k_gmm_init<R>, smem_bytes(nd)), k_gmm_init<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, stream_base, key, ctrs,
                                                                                        data, nd, h)));
     SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_gmm_init");
@@ -362,7 +378,7 @@ extern "C" int smc_gmm_eval(double *x, int64_t n, int r, const double *data, int
     if (rc) return rc;
     const Hyper h = make_hyper(hyper, r);
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
-    SMC_GMM_DISPATCH(r, (k_gmm_eval<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, data, nd, h)));
+    SMC_GMM_DISPATCH(r, (allow_smem(k_gmm_eval<R>, smem_bytes(nd)), k_gmm_eval<R><<<nb, GB, smem_bytes(nd), (cudaStream_t)stream>>>(x, n, data, nd, h)));
     SMC_COUNT_LAUNCH();
     return smc_check_launch("smc_gmm_eval");
 }
@@ -402,7 +418,7 @@ extern "C" int smc_gmm_mh(int block, double *x, int64_t n, int r, uint64_t strea
     const unsigned nb = (unsigned)((n + GB - 1) / GB);
     const size_t sm = smem_bytes(nd);
 #define SMC_GMM_MH(B) \
-    SMC_GMM_DISPATCH(r, (k_gmm_mh<B, R><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted)))
+    SMC_GMM_DISPATCH(r, (allow_smem(k_gmm_mh<B, R>, sm), k_gmm_mh<B, R><<<nb, GB, sm, s>>>(x, n, stream_base, key, ctrs, data, nd, h, alpha, sd, accepted)))
     if (block == 0) { SMC_GMM_MH(0) }
     else if (block == 1) { SMC_GMM_MH(1) }
     else { SMC_GMM_MH(2) }

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         }
         s_v[q][threadIdx.x] = v;
     }
+    SMC_PDL_TRIGGER();  // the lse combine's blocks may launch now (they wait for this grid)
     // block (max, sum e, sum e^2), e = exp(v - max): one pass over the parked values
     __shared__ double s_red[3][PB / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

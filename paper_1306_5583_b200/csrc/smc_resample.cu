@@ -65,11 +65,13 @@ struct RsHeader {
     int32_t trivial;  // N == 1
     uint32_t Z_total, S_total, P_total;
     uint64_t qoff;    // this shard's CDF offset (0 on one GPU)
-    int32_t mn_direct;  // multinomial: too many positions for the buckets -> direct search
+    int32_t mn_direct;  // multinomial: a position bin overflowed its capacity -> direct search
+    double mn_rb;       // multinomial: 2^kb / Tm (bin-boundary estimate, exact fix-up)
 };
 
 struct Layout {
     RsHeader *hdr;
+    SMC_DEV RsHeader *hdr_w() const { return hdr; }
     u128 *tile_q;
     int64_t *tile_f;
     uint64_t *tile_qr;
@@ -81,21 +83,35 @@ struct Layout {
     uint32_t *zmask;    // zero-count slots, one bit per slot (TILE / 32 words per tile), for pass C
     uint64_t *qfull;
     int32_t *cnt;       // multinomial histogram, then the counts when the caller passes none
-    uint32_t *mn_cnt, *mn_off, *mn_fill;  // multinomial: draws per position bin, offsets, fill pointers
-    uint64_t *mn_pos;   // multinomial: positions bucketed by bin
-    uint32_t *mn_start; // multinomial: first particle of every bin
+    uint32_t *mn_fill;  // multinomial: positions per bin (reserved runs)
+    uint64_t *mn_pos;   // multinomial: positions by bin, `cap` slots per bin
+    uint32_t *mn_start; // multinomial: first particle reached by every bin's positions (B + 1)
     size_t bytes;
 };
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// multinomial position bins: ~256 particles each, at most 2^17 (the one-block bin scan
-// stays ~40 us at any N; bins get wider, the bin-local searches a few levels deeper)
-constexpr int64_t MN_MAX_BINS = 1 << 17;
-__host__ __device__ inline int64_t mn_bins(int64_t n)
+// Multinomial position bins: B = 2^kb bins by the top kb bits of the 53-bit draw m (the
+// position P = floor(m Tm / 2^53) is monotone in m, so bin b holds exactly the positions
+// [floor(b Tm / 2^kb), ~floor((b+1) Tm / 2^kb)] -- no division, no search), ~8192
+// positions per bin (at most 4096 bins), and a fixed capacity of cap slots per bin (the
+// draws' bins are Binomial(M, 2^-kb) whatever the weights: mean + 8 sd + 64; an overflow --
+// adversarial explicit uniforms -- falls back to the direct search).
+struct MnGeom {
+    int kb;
+    int64_t nb, cap;
+};
+__host__ __device__ inline MnGeom mn_geom(int64_t n)
 {
-    const int64_t b = (n + 255) / 256;
-    return b < MN_MAX_BINS ? b : MN_MAX_BINS;
+    MnGeom g;
+    g.kb = 0;
+    while (g.kb < 12 && (n >> g.kb) > 8192) ++g.kb;
+    g.nb = (int64_t)1 << g.kb;
+    const int64_t per = (n + g.nb - 1) / g.nb;
+    int64_t sd = (int64_t)sqrt((double)per);  // ceil(sqrt(per)): correctly rounded sqrt, one fix-up
+    while (sd * sd < per) ++sd;
+    g.cap = per + 8 * sd + 64;
+    return g;
 }
 
 Layout layout(void *ws, int64_t n)
@@ -119,12 +135,10 @@ Layout layout(void *ws, int64_t n)
     L.zmask = (uint32_t *)take(sizeof(uint32_t) * nt * (TILE / 32));
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
-    const int64_t nbins = mn_bins(n);
-    L.mn_cnt = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
-    L.mn_off = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
-    L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (nbins + 1));
-    L.mn_pos = (uint64_t *)take(sizeof(uint64_t) * n);  // bucket capacity n positions
-    L.mn_start = (uint32_t *)take(sizeof(uint32_t) * (nbins + 2));
+    const MnGeom mg = mn_geom(n);
+    L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (mg.nb + 1));
+    L.mn_pos = (uint64_t *)take(sizeof(uint64_t) * mg.nb * mg.cap);
+    L.mn_start = (uint32_t *)take(sizeof(uint32_t) * (mg.nb + 2));
     L.bytes = o;
     return L;
 }
@@ -449,7 +463,16 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
                 h->m_sys = draws ? (u ? (uint64_t)(u[0] * TWO53) : draw53(c0, stream, key)) : 0;
         }
         h->active = ok;
+        h->mn_direct = 0;
+        h->mn_rb = Tm ? ldexp(1.0, mn_geom(n).kb) / (double)Tm : 0.0;
         s_ok = ok;
+    }
+    if (is_multinomial(scheme)) {  // the multinomial bins: empty, every start at the last particle
+        const MnGeom g = mn_geom(n);
+        for (int64_t b = threadIdx.x; b <= g.nb; b += SB) {
+            L.mn_fill[b] = 0;
+            L.mn_start[b] = (uint32_t)(n - 1);
+        }
     }
     __syncthreads();
     if (!s_ok) return;
@@ -502,10 +525,6 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
 {
     SMC_PDL_WAIT();
     if (!L.hdr->active || L.hdr->trivial) return;
-    {  // zero the multinomial bin counters (nbins <= n / 256 + 1 <= nt * RT)
-        const int64_t b = (int64_t)blockIdx.x * RT + threadIdx.x;
-        if (b <= mn_bins(n)) L.mn_cnt[b] = 0;
-    }
     if (L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
     __shared__ uint64_t s_io[tile_smem_elems<uint64_t, RT, RI>()];
@@ -519,211 +538,294 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     for (int j = 0; j < RI; ++j) loc += v[j];
     uint64_t tot;
     uint64_t run = L.tile_pre[blockIdx.x] + block_exclusive_sum<RT, uint64_t>(loc, sm, &tot);
+    // the multinomial bins' first particles: particle i is the first reached by bin b's
+    // positions iff lo_b = floor(b Tm / 2^kb) lies in [Q_{i-1}, Q_i) -- found from the two
+    // ends of each particle's interval (ceil bin boundaries are monotone: usually no bin)
+    const RsHeader *h = L.hdr;
+    const MnGeom g = mn_geom(n);
+    auto ceil_bin = [&](uint64_t X) {  // min b with floor(b Tm / 2^kb) >= X
+        int64_t b = (int64_t)ceil((double)X * h->mn_rb);
+        b = b < 0 ? 0 : (b > g.nb ? g.nb : b);
+        while (b > 0 && (uint64_t)(((u128)(b - 1) * h->Tm) >> g.kb) >= X) --b;
+        while (b < g.nb && (uint64_t)(((u128)b * h->Tm) >> g.kb) < X) ++b;
+        return b;
+    };
+    const int64_t i0 = tbase + (int64_t)threadIdx.x * RI;
+    const uint64_t q0 = run;  // Q before this thread's first particle
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         run += v[j];
         v[j] = run;
     }
+    if (i0 == 0 && h->qoff > 0) {  // the bin straddling this shard's start reaches particle 0 first
+        const int64_t bq = ceil_bin(h->qoff) - 1;
+        if (bq >= 0) L.mn_start[bq] = 0;
+    }
+    if (i0 < n) {
+        // a bin boundary inside this thread's 8 intervals is rare (~8 per 8192 particles): two
+        // boundary evaluations per thread, the per-particle walk only when they differ
+        int64_t bprev = ceil_bin(q0);
+        if (ceil_bin(run) > bprev) {
+            uint64_t qprev = q0;
+#pragma unroll
+            for (int j = 0; j < RI; ++j) {
+                if (v[j] > qprev && i0 + j < n) {
+                    const int64_t bj = ceil_bin(v[j]);
+                    for (int64_t b = bprev; b < bj; ++b) L.mn_start[b] = (uint32_t)(i0 + j);
+                    bprev = bj;
+                }
+                qprev = v[j];
+            }
+        }
+    }
     store_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, v, s_io);
 }
 
-// Multinomial positions P_k = floor(m_k Tm / 2^53) (A.3) are iid over the whole CDF,
-// so a per-draw binary search over Q diverges across a warp at every level (32
-// cache lines per load).  Instead the draws are first COUNTING-SORTED into NB
-// equal-width position bins (bin = an arithmetic, monotone function of P: no
-// search), regenerating each draw from its counter rather than storing it
-// twice; then the bucketed positions, now nearly sorted, are searched: a warp's
-// 32 searches share their paths down to the last few levels, so those loads
-// broadcast.  Counts are order-independent integer sums: bit-identical to any
-// other evaluation order.
-constexpr int MN_BIN = 256;  // particles per position bin (on average)
+// Multinomial positions P_k = floor(m_k Tm / 2^53) (A.3) are iid over the whole CDF: a
+// per-draw search over Q diverges across a warp at every level, and a per-draw scatter
+// or histogram increment costs a random 32-byte sector each.  Instead:
+//  k_mn2_scatter: a block draws 12288 positions into shared memory, counting-sorts them
+//      by bin there (bin = the draw's top kb bits), reserves one run per bin in the bin's
+//      fixed-capacity region (one global atomic per bin per block), and writes the runs
+//      out coalesced (~12 positions = 96 B per bin per block at 2^24);
+//  k_mn2_count: one block per bin: the bin's positions reach only the particles
+//      [start_b, start_{b+1}] (k_rs_prefix), so their counts accumulate in shared memory
+//      (each position found by a search over that slice of Q) and go out with plain
+//      coalesced stores -- atomics only for the two end particles a neighbouring bin can
+//      share.
+// Counts are order-independent integer sums: bit-identical to any other evaluation order.
+constexpr int MT = 1024;          // threads of the multinomial kernels
+constexpr int MDPT = 12;          // draws per thread in k_mn2_scatter
+constexpr int MCH = MT * MDPT;    // draws per scatter block
 
-
-struct MnCtx {
-    uint64_t M, Tm, c0, lo, hi;  // [lo, hi): this shard's slice of the CDF
-    uint32_t nb;
-    uint64_t W;                  // bin width: bin b = positions [lo + b W, lo + (b+1) W)
-    double invW;
-    SMC_DEV uint32_t bin(uint64_t P) const  // exact floor((P - lo) / W)
-    {
-        const uint64_t d = P - lo;
-        uint64_t b = (uint64_t)((double)d * invW);
-        while (b && b * W > d) --b;
-        while ((b + 1) * W <= d) ++b;
-        return (uint32_t)(b < nb ? b : nb - 1);
-    }
-};
-
-SMC_DEV MnCtx mn_ctx(const Layout &L, int64_t n)
+inline size_t mn2_scatter_smem(int64_t n)
 {
-    const RsHeader *h = L.hdr;
-    MnCtx c;
-    c.M = h->M;
-    c.Tm = h->Tm;
-    c.c0 = h->c0;
-    c.lo = h->qoff;
-    c.hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
-    c.nb = (uint32_t)mn_bins(n);
-    const uint64_t span = c.hi > c.lo ? c.hi - c.lo : 1;
-    c.W = span / c.nb + 1;  // nb W > span: every position has a bin
-    c.invW = 1.0 / (double)c.W;
-    return c;
+    return (size_t)MCH * (8 + 2 + 2) + (size_t)mn_geom(n).nb * 12 + 64;
 }
 
-SMC_DEV uint64_t mn_position(const MnCtx &c, uint64_t k, const Key &key, uint64_t stream, const double *u)
+SMC_DEV uint64_t mn_m(uint64_t k, uint64_t c0, const Key &key, uint64_t stream, const double *u)
 {
-    const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c.c0 + k, stream, key);
-    return (uint64_t)(((u128)m * c.Tm) >> 53);
+    return u ? (uint64_t)(u[k] * TWO53) : draw53(c0 + k, stream, key);
 }
 
-// atomicAdd(&a[key], 1) for a warp, one atomic when every active lane shares the key
-// (degenerate weights send every draw to one bin / one particle: without this the
-// same-address atomics serialize).  Returns the lane's slot (old value + rank).
-SMC_DEV uint32_t agg_inc(uint32_t *a, uint32_t key, bool active)
-{
-    const unsigned act = __ballot_sync(0xffffffffu, active);
-    if (!act) return 0;
-    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
-    const uint32_t k0 = __shfl_sync(0xffffffffu, key, leader);
-    if (__all_sync(0xffffffffu, !active || key == k0)) {  // the whole warp hits one counter
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&a[k0], (uint32_t)__popc(act));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        return base + __popc(act & ((1u << lane) - 1));
-    }
-    return active ? atomicAdd(&a[key], 1u) : 0;
-}
-
-__global__ void k_mn_count(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+__global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u,
+                                                    Layout L)
 {
     SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial) return;
-    const MnCtx c = mn_ctx(L, n);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t kend = (c.M + stride - 1) / stride * stride;  // whole warps iterate together
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
-        const uint64_t P = k < c.M ? mn_position(c, k, key, stream, u) : c.lo;
-        const bool in = k < c.M && P >= c.lo && P < c.hi;  // else: past the end, or on another shard
-        agg_inc(L.mn_cnt, in ? c.bin(P) : 0u, in);
-    }
-}
-
-// one block: exclusive bucket offsets; fill pointers back to zero
-__global__ void __launch_bounds__(SB) k_mn_scan(int64_t nbins, int64_t cap, Layout L)
-{
-    SMC_PDL_WAIT();
-    const RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
-    __shared__ uint64_t sm64[SB / 32 + 1];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr int NW = SB / 32;
-    const int64_t nt = nbins;
-    const int64_t C = (nt + NW - 1) / NW;
-    const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
-    constexpr int KS = 8;  // warp-rows of bins in flight per round (one round trip per round)
-    uint64_t wsum = 0;
-    for (int64_t b0 = w0 + lane; b0 < w1; b0 += 32 * KS) {
-        uint32_t v[KS];
-#pragma unroll
-        for (int k = 0; k < KS; ++k) v[k] = b0 + 32 * k < w1 ? L.mn_cnt[b0 + 32 * k] : 0;
-#pragma unroll
-        for (int k = 0; k < KS; ++k) wsum += v[k];
-    }
-    wsum = warp_sum(wsum);
-    if (lane == 0) sm64[warp] = wsum;
+    const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0, lo = h->qoff;
+    const uint64_t hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
+    const MnGeom g = mn_geom(n);
+    const uint64_t k0 = (uint64_t)blockIdx.x * MCH;
+    if (k0 >= M) return;
+    extern __shared__ __align__(16) unsigned char mn_sm[];
+    uint64_t *P_s = reinterpret_cast<uint64_t *>(mn_sm);
+    uint16_t *bin_s = reinterpret_cast<uint16_t *>(P_s + MCH);
+    uint16_t *perm_s = bin_s + MCH;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(perm_s + MCH);  // counts, then the sorting cursors
+    uint32_t *base = hist + g.nb;                                  // reserved run start per bin
+    uint32_t *lofs = base + g.nb;                                  // bin's offset in the block's sorted order
+    __shared__ uint32_t s_w[MT / 32 + 1];
+    __shared__ int s_over;
+    for (int64_t b = threadIdx.x; b < g.nb; b += MT) hist[b] = 0;
+    if (threadIdx.x == 0) s_over = 0;
     __syncthreads();
-    if (warp == 0) {
-        const uint64_t x = sm64[lane];
-        const uint64_t inc = warp_inclusive_sum(x);
-        sm64[lane] = inc - x;
-    }
-    __syncthreads();
-    uint64_t carry = sm64[warp];
-    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
-        uint64_t vv[KS];
-#pragma unroll
-        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.mn_cnt[c0 + 32 * k + lane] : 0;
-#pragma unroll
-        for (int k = 0; k < KS; ++k) {
-            const int64_t b = c0 + 32 * k + lane;
-            const uint64_t inc = warp_inclusive_sum(vv[k]);
-            if (b < w1) {
-                L.mn_off[b] = (uint32_t)(carry + inc - vv[k]);
-                L.mn_fill[b] = 0;
+    const int sh = 53 - g.kb;
+#pragma unroll 4
+    for (int d = 0; d < MDPT; ++d) {
+        const int idx = d * MT + threadIdx.x;
+        const uint64_t k = k0 + idx;
+        uint16_t bb = 0xFFFF;  // not in this shard's slice / past the last draw
+        uint64_t P = 0;
+        if (k < M) {
+            const uint64_t m = mn_m(k, c0, key, stream, u);
+            P = (uint64_t)(((u128)m * Tm) >> 53);
+            if (P >= lo && P < hi) {
+                bb = (uint16_t)(m >> sh);
+                atomicAdd(&hist[bb], 1u);
             }
-            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        P_s[idx] = P;
+        bin_s[idx] = bb;
+    }
+    __syncthreads();
+    // per bin: the block's run in the bin's region (one global atomic), and the bins' offsets in
+    // the block's sorted order (exclusive scan over the nb <= 4096 bins, 4 per thread)
+    constexpr int BPT = 4;
+    uint32_t loc[BPT], sum = 0;
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int64_t b = (int64_t)threadIdx.x * BPT + q;
+        loc[q] = b < g.nb ? hist[b] : 0;
+        sum += loc[q];
+        if (b < g.nb && loc[q]) {
+            const uint32_t r = atomicAdd(&L.mn_fill[b], loc[q]);
+            base[b] = r;
+            if (r + loc[q] > (uint64_t)g.cap) s_over = 1;
         }
     }
-    if (warp == NW - 1 && lane == 31) {
-        L.mn_off[nt] = (uint32_t)carry;  // total positions in this shard
-        L.hdr->mn_direct = carry > (uint64_t)cap;  // buckets hold `cap` positions
+    uint32_t tot;
+    uint32_t ex = block_exclusive_sum<MT, uint32_t>(sum, s_w, &tot);
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int64_t b = (int64_t)threadIdx.x * BPT + q;
+        if (b < g.nb) { lofs[b] = ex; hist[b] = 0; }
+        ex += loc[q];
+    }
+    __syncthreads();
+    if (s_over) {  // a bin overflowed (adversarial uniforms): the direct search handles the call
+        if (threadIdx.x == 0) L.hdr_w()->mn_direct = 1;
+        return;
+    }
+    for (int d = 0; d < MDPT; ++d) {  // counting sort in shared memory: the block's draws by bin
+        const int idx = d * MT + threadIdx.x;
+        const uint16_t bb = bin_s[idx];
+        if (bb != 0xFFFF) perm_s[lofs[bb] + atomicAdd(&hist[bb], 1u)] = (uint16_t)idx;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tot; j += MT) {  // consecutive j: consecutive slots of a bin's run
+        const int idx = perm_s[j];
+        const uint32_t bb = bin_s[idx];
+        L.mn_pos[(int64_t)bb * g.cap + base[bb] + (j - lofs[bb])] = P_s[idx];
     }
 }
 
-// first particle of every bin: mn_start[b] = first i with Q_i > lo + b W (b = 0..nb)
-__global__ void k_mn_starts(int64_t n, Layout L)
+// One block per bin: the bin's positions [lo_b, hi_b] are counting-sorted in shared memory
+// into NSB sub-buckets of equal width (~1 position each), and every particle of the bin's range
+// [start_b, start_{b+1}] counts the positions in its interval [Q_{i-1}, Q_i): whole sub-buckets
+// from the sub-bucket prefix, the two end sub-buckets element by element -- O(1) per particle
+// and per position, no search.  Interior particles are reached by this bin only (plain
+// coalesced stores); the two end particles may be shared with a neighbour (atomics).
+constexpr int NSB = 8192;
+inline size_t mn2_count_smem(int64_t n) { return (size_t)mn_geom(n).cap * 8 + (size_t)(NSB + 1) * 4 * 2 + 64; }
+
+__global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
 {
     SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
     if (!h->active || h->trivial || h->mn_direct) return;
-    const MnCtx c = mn_ctx(L, n);
-    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= c.nb; b += gridDim.x * blockDim.x) {
-        const uint64_t X = c.lo + (uint64_t)b * c.W;
-        int64_t lo = 0, hi = n - 1;
-        if (X >= c.hi) lo = n - 1;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (__ldg(&L.qfull[mid]) > X) hi = mid; else lo = mid + 1;
+    const MnGeom g = mn_geom(n);
+    const int64_t b = blockIdx.x;
+    const int64_t cnt = min((int64_t)__ldg(&L.mn_fill[b]), g.cap);
+    if (cnt == 0) return;
+    const uint64_t Tm = h->Tm;
+    const uint64_t lo_b = (uint64_t)(((u128)b * Tm) >> g.kb);
+    const uint64_t mmax = ((uint64_t)(b + 1) << (53 - g.kb)) - 1;
+    const uint64_t hi_b = (uint64_t)(((u128)mmax * Tm) >> 53);  // the bin's largest position
+    const uint64_t span = hi_b - lo_b;
+    // smallest sh2 with span >> sh2 < NSB (one clz, not a loop)
+    int sh2 = span ? max(0, 64 - __clzll((long long)span) - 13) : 0;  // NSB = 2^13
+    while ((span >> sh2) >= (uint64_t)NSB) ++sh2;
+    const int nsb = (int)(span >> sh2) + 1;
+    extern __shared__ __align__(16) unsigned char c_sm[];
+    uint64_t *Ps = reinterpret_cast<uint64_t *>(c_sm);                 // positions sorted by sub-bucket
+    uint32_t *offs = reinterpret_cast<uint32_t *>(Ps + g.cap);         // sub-bucket starts (nsb + 1)
+    uint32_t *cur = offs + NSB + 1;                                    // counts, then cursors
+    __shared__ uint32_t s_w[MT / 32 + 1];
+    for (int k = threadIdx.x; k <= nsb; k += MT) cur[k] = 0;
+    __syncthreads();
+    const uint64_t *pos = L.mn_pos + b * g.cap;
+    // up to KPT positions per thread stay in registers with their rank in their sub-bucket (the
+    // counting atomic's return value): one read of the bin and no second atomic; larger bins
+    // (N > 2^25: wider bins) read their positions twice
+    constexpr int KPT = 12;
+    const bool inreg = cnt <= (int64_t)MT * KPT;
+    uint64_t Pr[KPT];
+    uint32_t sbr[KPT];
+    if (inreg) {
+#pragma unroll
+        for (int k = 0; k < KPT; ++k) {
+            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            Pr[k] = j < cnt ? pos[j] : 0;
         }
-        L.mn_start[b] = (uint32_t)lo;
-    }
-}
-
-__global__ void k_mn_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
-{
-    SMC_PDL_WAIT();
-    const RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
-    if (h->mn_direct) return;  // more positions than bucket capacity (a shard): k_rs_multinomial
-    const MnCtx c = mn_ctx(L, n);
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint64_t kend = (c.M + stride - 1) / stride * stride;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
-        const uint64_t P = k < c.M ? mn_position(c, k, key, stream, u) : c.lo;
-        const bool in = k < c.M && P >= c.lo && P < c.hi;
-        const uint32_t b = in ? c.bin(P) : 0u;
-        const uint32_t r = agg_inc(L.mn_fill, b, in);
-        if (in) L.mn_pos[__ldg(&L.mn_off[b]) + r] = P;
-    }
-}
-
-// per bucketed position: first i with Q_i > P (Q inclusive, materialized by k_rs_prefix),
-// searched only between its bin's first particles
-__global__ void k_mn_assign(int64_t n, Layout L)
-{
-    SMC_PDL_WAIT();
-    const RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
-    if (h->mn_direct) return;
-    const MnCtx c = mn_ctx(L, n);
-    const uint32_t total = __ldg(&L.mn_off[mn_bins(n)]);
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t jend = (total + stride - 1) / stride * stride;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jend; j += stride) {
-        const bool in = j < total;
-        int64_t lo = 0;
-        if (in) {
-            const uint64_t P = L.mn_pos[j];
-            const uint32_t b = c.bin(P);
-            lo = __ldg(&L.mn_start[b]);
-            int64_t hi = __ldg(&L.mn_start[b + 1]);
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (__ldg(&L.qfull[mid]) > P) hi = mid; else lo = mid + 1;
+#pragma unroll
+        for (int k = 0; k < KPT; ++k) {
+            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            if (j < cnt) {
+                const uint32_t sb = (uint32_t)((Pr[k] - lo_b) >> sh2);
+                sbr[k] = (sb << 16) | atomicAdd(&cur[sb], 1u);  // rank < 2^16: cnt <= MT * KPT
             }
         }
-        agg_inc(reinterpret_cast<uint32_t *>(L.cnt), (uint32_t)lo, in);
+    } else {
+        for (int64_t j = threadIdx.x; j < cnt; j += MT) atomicAdd(&cur[(pos[j] - lo_b) >> sh2], 1u);
+    }
+    __syncthreads();
+    {  // exclusive scan of the nsb <= 8192 sub-bucket counts, 8 per thread
+        constexpr int SPT = NSB / MT;
+        uint32_t c8[SPT], sum = 0;
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) {
+            const int k = threadIdx.x * SPT + q;
+            c8[q] = k < nsb ? cur[k] : 0;
+            sum += c8[q];
+        }
+        uint32_t tot;
+        uint32_t ex = block_exclusive_sum<MT, uint32_t>(sum, s_w, &tot);
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) {
+            const int k = threadIdx.x * SPT + q;
+            if (k < nsb) { offs[k] = ex; cur[k] = ex; }
+            ex += c8[q];
+        }
+        if (threadIdx.x == 0) offs[nsb] = tot;
+    }
+    __syncthreads();
+    if (inreg) {
+#pragma unroll
+        for (int k = 0; k < KPT; ++k) {
+            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            if (j < cnt) Ps[offs[sbr[k] >> 16] + (sbr[k] & 0xFFFFu)] = Pr[k];
+        }
+    } else {
+        for (int64_t j = threadIdx.x; j < cnt; j += MT) {  // the bin's positions again (L2-hot): placed
+            const uint64_t P = pos[j];
+            Ps[atomicAdd(&cur[(P - lo_b) >> sh2], 1u)] = P;
+        }
+    }
+    __syncthreads();
+    const uint64_t *Q = L.qfull;
+    const uint64_t qoff = h->qoff;
+    const int64_t s = __ldg(&L.mn_start[b]);
+    int64_t e = max(s, (int64_t)__ldg(&L.mn_start[b + 1]));
+    if (e == n - 1) {  // the start sentinel (the last bin, or zero-weight particles to the end):
+        __shared__ int64_t s_e;  // the particle of the bin's largest position instead, by search
+        if (threadIdx.x == 0) {
+            const uint64_t Pm = min(hi_b, __ldg(&Q[n - 1]) - 1);
+            int64_t lo = s, hi = n - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(&Q[mid]) > Pm) hi = mid; else lo = mid + 1;
+            }
+            s_e = lo;
+        }
+        __syncthreads();
+        e = s_e;
+    }
+    // F(X) = #{bin positions < X}: the sub-bucket prefix plus the few positions of X's own
+    // sub-bucket below X; particle i's count is F(Q_i) - F(Q_{i-1}), the second term being the
+    // previous particle's first (the neighbouring lane's, by shuffle)
+    auto F = [&](uint64_t X) -> uint32_t {
+        if (X <= lo_b) return 0;
+        if (X > hi_b) return offs[nsb];
+        const int sb = (int)((X - lo_b) >> sh2);
+        uint32_t c = offs[sb];
+        for (uint32_t k = offs[sb]; k < offs[sb + 1]; ++k) c += (Ps[k] < X);
+        return c;
+    };
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = s + (threadIdx.x & ~31); i0 <= e; i0 += MT) {  // a warp: 32 consecutive particles
+        const int64_t i = i0 + lane;
+        const uint32_t Fi = i <= e ? F(__ldg(&Q[i])) : 0;
+        uint32_t Fp = __shfl_up_sync(0xffffffffu, Fi, 1);
+        if (lane == 0) Fp = F(i ? __ldg(&Q[i - 1]) : qoff);
+        if (i > e) continue;
+        const uint32_t c = Fi - Fp;
+        if (i == s || i == e) {  // a neighbouring bin may reach it too
+            if (c) atomicAdd(&L.cnt[i], (int)c);
+        } else {
+            L.cnt[i] = (int32_t)c;  // only this bin reaches it
+        }
     }
 }
 
@@ -1205,12 +1307,48 @@ constexpr int CSTAGE = TILE + 2 * ANCHOR + 2;
 // zoff + local rank; global surplus ranks [soff, soff + s_self) are this
 // shard's own surplus children (local pairs, gathered by the next move); the
 // rest arrive as rows in `recv`, ordered by global rank.
+// Peer memory of the other shards (P2P over NVLink: CUDA-IPC mappings of their resample
+// workspaces and state buffers).  The workspaces share one layout (same n), so one set of
+// offsets locates a peer's surplus-parent list, surplus starts and rank anchors.
+constexpr int SMC_MAX_SHARDS = 16;
+struct PeerTab {
+    const char *ws[SMC_MAX_SHARDS];    // each rank's resample workspace
+    const char *rows[SMC_MAX_SHARDS];  // each rank's current state buffer
+    int64_t off_sp_idx, off_sp_start, off_anchor;
+};
+
 struct ShardC {
     int64_t zoff, soff, s_self;  // s_self < 0: single GPU (all pairs local)
     const char *recv;
     char *rows;
     int64_t row_bytes;
+    // P2P exchange (zsp_all != null): the offsets above come from the allgathered per-rank
+    // (Z, S, P, active) on the device, and a surplus child on another rank is read from that
+    // rank's memory directly -- no host plan, no host sync, no packed send / receive
+    const uint32_t *zsp_all;
+    int G, rank;
+    PeerTab peers;
+    int32_t *status;
 };
+
+// The surplus parent owning local surplus rank r of a shard: its rank anchors where they
+// exist, a walk of at most ANCHOR starts from there; beyond them, binary search.
+SMC_DEV int64_t surplus_owner(const int32_t *anchor, const int32_t *sp_start, int64_t n, int64_t P, int64_t r)
+{
+    int64_t p;
+    if (r / ANCHOR < n / ANCHOR + 2) {
+        p = __ldcg(&anchor[r / ANCHOR]);
+        while (p + 1 < P && (int64_t)__ldcg(&sp_start[p + 1]) <= r) ++p;
+    } else {
+        int64_t lo = 0, hi = P;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)__ldcg(&sp_start[mid]) <= r) lo = mid; else hi = mid;
+        }
+        p = lo;
+    }
+    return p;
+}
 
 // COPY32 (one GPU, 32-byte rows): the value collection's in-place copy fused in -- every zero
 // slot's row is overwritten by its parent's as soon as the parent is known (sources have
@@ -1238,8 +1376,28 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
     __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
     __shared__ int32_t s_io[tile_smem_elems<int32_t, RT, RI>()];
     __shared__ uint32_t sm32[RT / 32 + 1];
+    __shared__ int64_t s_soffs[SMC_MAX_SHARDS + 1], s_zs[3];
     const int64_t tbase = t * TILE;
     const int64_t base = tbase + (int64_t)threadIdx.x * RI;
+    if (SHARD && sc.zsp_all) {  // this rank's zero / surplus offsets from the allgathered counts
+        if (threadIdx.x == 0) {
+            int64_t zo = 0, so = 0;
+            for (int r = 0; r < sc.G; ++r) {
+                const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(sc.zsp_all) + r);
+                s_soffs[r] = so;
+                if (r == sc.rank) { s_zs[0] = zo; s_zs[1] = so; s_zs[2] = v.y; }
+                zo += v.x;
+                so += v.y;
+            }
+            s_soffs[sc.G] = so;
+            // sum(counts) != N over all ranks: zero slots and surplus children do not pair up
+            if (blockIdx.x == 0 && zo != so) raise_status(sc.status, SMC_ECOUNTS);
+        }
+        __syncthreads();
+        sc.zoff = s_zs[0];
+        sc.soff = s_zs[1];
+        sc.s_self = s_zs[2];
+    }
     const int64_t s_self = sc.s_self < 0 ? Sl : sc.s_self;
     const int64_t soff = sc.soff, zoff = sc.zoff;
     // length of this shard's local piece [soff, soff+s_self) ∩ [zoff, zoff+Zl) in global ranks
@@ -1346,6 +1504,20 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
                     const int64_t s = g - soff;
                     while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
                     par[j] = s_idx[lo];
+                } else if (sc.zsp_all) {  // surplus child on another shard: read from its memory (P2P)
+                    int h = 0;
+                    while (h + 1 < sc.G && s_soffs[h + 1] <= g) ++h;
+                    const int64_t r = g - s_soffs[h];  // rank h's local surplus rank
+                    const char *wh = sc.peers.ws[h];
+                    const uint4 zh = __ldcg(reinterpret_cast<const uint4 *>(sc.zsp_all) + h);
+                    const int64_t p = surplus_owner(reinterpret_cast<const int32_t *>(wh + sc.peers.off_anchor),
+                                                    reinterpret_cast<const int32_t *>(wh + sc.peers.off_sp_start), n,
+                                                    zh.z, r);
+                    const int64_t src = __ldcg(reinterpret_cast<const int32_t *>(wh + sc.peers.off_sp_idx) + p);
+                    const char *srow = sc.peers.rows[h] + src * sc.row_bytes;
+                    char *dst = sc.rows + (base + j) * sc.row_bytes;
+                    for (int64_t b = 0; b < sc.row_bytes; b += 8)
+                        *(int64_t *)(dst + b) = __ldcg((const long long *)(srow + b));
                 } else if (sc.recv) {  // surplus child on another shard: its row arrived in recv
                     const int64_t k = g < soff ? g - zoff : g - zoff - piece;
                     const char *src = sc.recv + k * sc.row_bytes;
@@ -1455,6 +1627,26 @@ __global__ void __launch_bounds__(RT) k_gather(char *__restrict__ dst, const cha
     }
 }
 
+// The multinomial draws' two kernels (m: the largest draw count; blocks past the call's
+// own count exit at once).
+inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L)
+{
+    const size_t sm = mn2_scatter_smem(n);
+    static size_t s_set = 0;  // opt in to > 48 KB of dynamic shared memory once (per size)
+    if (sm > s_set) {
+        cudaFuncSetAttribute(k_mn2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        s_set = sm;
+    }
+    smc_launch(k_mn2_scatter, (unsigned)((m + MCH - 1) / MCH), MT, sm, s, n, key, stream, u, L);
+    const size_t sc = mn2_count_smem(n);
+    static size_t c_set = 0;
+    if (sc > c_set) {
+        cudaFuncSetAttribute(k_mn2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+        c_set = sc;
+    }
+    smc_launch(k_mn2_count, (unsigned)mn_geom(n).nb, MT, sc, s, n, L);
+}
+
 inline int grid_cap(int64_t blocks)
 {
     return (int)(blocks < 1 ? 1 : (blocks > 148 * 16 ? 148 * 16 : blocks));
@@ -1506,11 +1698,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        smc_launch(k_mn_count, gm, RT, 0, s, n, key, stream_index, u, L);
-        smc_launch(k_mn_scan, 1, SB, 0, s, mn_bins(n), n, L);
-        smc_launch(k_mn_starts, (unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s, n, L);
-        smc_launch(k_mn_scatter, gm, RT, 0, s, n, key, stream_index, u, L);
-        smc_launch(k_mn_assign, gm, RT, 0, s, n, L);
+        launch_mn2(s, n, m_out, key, stream_index, u, L);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
@@ -1520,9 +1708,9 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
         smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, cout, n, status, 0, L);
         if (rows && row_bytes == 32) {  // the value collection's copy fused into pass C
             smc_launch(k_rs_assign<false, true>, (unsigned)nt, RT, 0, s, cout, n, parents,
-                       ShardC{0, 0, -1, nullptr, (char *)rows, 32}, L);
+                       ShardC{0, 0, -1, nullptr, (char *)rows, 32, nullptr, 0, 0, {}, nullptr}, L);
         } else {
-            smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+            smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, cout, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0, nullptr, 0, 0, {}, nullptr}, L);
             if (rows)  // other row sizes: one moved row per thread, full occupancy
                 smc_launch(k_rs_copy, (unsigned)((n + CB - 1) / CB), CB, 0, s, parents, (char *)rows, row_bytes, n, L);
         }
@@ -1545,7 +1733,7 @@ extern "C" int smc_replication_to_parents(const int32_t *counts, int64_t n, int3
     smc_launch(k_rs_aggs, (unsigned)nt, RT, 0, s, counts, n, L);
     smc_launch(k_rs_zsp_scan, 1, SB, 0, s, nt, 1, status, L);
     smc_launch(k_rs_ranks, (unsigned)nt, RT, 0, s, counts, n, status, 1, L);
-    smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0}, L);
+    smc_launch(k_rs_assign<false>, (unsigned)nt, RT, 0, s, counts, n, parents, ShardC{0, 0, -1, nullptr, nullptr, 0, nullptr, 0, 0, {}, nullptr}, L);
     return smc_check_launch("smc_replication_to_parents");
 }
 
@@ -1640,11 +1828,7 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_total + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        smc_launch(k_mn_count, gm, RT, 0, s, n, key, stream_index, u, L);
-        smc_launch(k_mn_scan, 1, SB, 0, s, mn_bins(n), n, L);
-        smc_launch(k_mn_starts, (unsigned)((mn_bins(n) + 1 + RT - 1) / RT), RT, 0, s, n, L);
-        smc_launch(k_mn_scatter, gm, RT, 0, s, n, key, stream_index, u, L);
-        smc_launch(k_mn_assign, gm, RT, 0, s, n, L);
+        launch_mn2(s, n, m_total, key, stream_index, u, L);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
@@ -1690,6 +1874,31 @@ extern "C" int smc_resample_shard_assign(const int32_t *counts, int64_t n, int64
     Layout L = layout(ws, n);
     const int32_t *cin = counts ? counts : L.cnt;
     smc_launch(k_rs_assign<true>, (unsigned)nt, RT, 0, (cudaStream_t)stream, 
-        cin, n, parents, ShardC{zoff, soff, s_self, (const char *)recv, (char *)rows, row_bytes}, L);
+        cin, n, parents, ShardC{zoff, soff, s_self, (const char *)recv, (char *)rows, row_bytes, nullptr, 0, 0, {}, nullptr}, L);
     return smc_check_launch("smc_resample_shard_assign");
+}
+
+extern "C" int smc_resample_shard_assign_p2p(const uint32_t *zsp_all, int G, int rank, const void *const *peer_ws,
+                                             const void *const *peer_rows, int64_t n, void *rows, int64_t row_bytes,
+                                             int32_t *parents, int32_t *status, void *ws, size_t ws_bytes,
+                                             void *stream)
+{
+    if (n < 1 || !parents || !ws || ws_bytes < smc_resample_workspace_bytes(n) || !zsp_all || G < 1 ||
+        G > SMC_MAX_SHARDS || rank < 0 || rank >= G || !peer_ws || !peer_rows || !rows || row_bytes < 8 ||
+        (row_bytes & 7))
+        return smc_set_error(SMC_EINVAL, "smc_resample_shard_assign_p2p: bad args");
+    for (int r = 0; r < G; ++r)
+        if (!peer_ws[r] || !peer_rows[r]) return smc_set_error(SMC_EINVAL, "smc_resample_shard_assign_p2p: peer %d", r);
+    const int64_t nt = (n + TILE - 1) / TILE;
+    Layout L = layout(ws, n);
+    ShardC sc{0, 0, 0, nullptr, (char *)rows, row_bytes, zsp_all, G, rank, {}, status};
+    for (int r = 0; r < G; ++r) {
+        sc.peers.ws[r] = (const char *)peer_ws[r];
+        sc.peers.rows[r] = (const char *)peer_rows[r];
+    }
+    sc.peers.off_sp_idx = (const char *)L.sp_idx - (const char *)ws;
+    sc.peers.off_sp_start = (const char *)L.sp_start - (const char *)ws;
+    sc.peers.off_anchor = (const char *)L.anchor - (const char *)ws;
+    smc_launch(k_rs_assign<true>, (unsigned)nt, RT, 0, (cudaStream_t)stream, nullptr, n, parents, sc, L);
+    return smc_check_launch("smc_resample_shard_assign_p2p");
 }

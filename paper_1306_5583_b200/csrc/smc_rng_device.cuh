@@ -67,11 +67,15 @@ SMC_DEV uint4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const
 
 // 53-bit integer of draw `ctr` of stream `stream` (rng.py:81-82):
 // ((w0 >> 5) << 26) | (w1 >> 6); the uniform is this times 2^-53, exactly.
+template <int R0, class K>
+SMC_DEV uint4 philox_rounds(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const K &key);
+
 template <class K>
 SMC_DEV uint64_t draw53(uint64_t ctr, uint64_t stream, const K &key)
 {
-    const uint4 w = philox10((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream,
-                             (uint32_t)(stream >> 32), key);
+    // the ten rounds with one mul.wide per product (philox_rounds): same bits as philox10
+    const uint4 w = philox_rounds<0>((uint32_t)ctr, (uint32_t)(ctr >> 32), (uint32_t)stream,
+                                     (uint32_t)(stream >> 32), key);
     return ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
 }
 

@@ -103,6 +103,27 @@ class TorchComm:
         self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
         return out
 
+    def peer_pointers(self, tensors):
+        """Device addresses of every rank's `tensors` (same list on every rank), mapped into this
+        process with CUDA IPC: rank r's entries are P2P-readable over NVLink (same-device
+        processes work too).  Returns [rank][k] -> int address; the own rank's are its own."""
+        mine = [(t.untyped_storage()._share_cuda_(), t.storage_offset() * t.element_size()) for t in tensors]
+        allv = [None] * self.world
+        self.dist.all_gather_object(allv, mine, group=self.group)
+        self._ipc = getattr(self, "_ipc", [])
+        out = []
+        for r, entries in enumerate(allv):
+            if r == self.rank:
+                out.append([t.data_ptr() for t in tensors])
+                continue
+            row = []
+            for handle, off in entries:
+                st = torch.UntypedStorage._new_shared_cuda(*handle)
+                self._ipc.append(st)  # keep the mapping alive
+                row.append(st.data_ptr() + off)
+            out.append(row)
+        return out
+
     def exchange(self, sends, recvs):
         """sends: [(peer, tensor)], recvs: [(peer, tensor)] -- one grouped send/recv round."""
         if self.staged:
@@ -145,8 +166,27 @@ class Shard:
                   int(bool(accumulate_nc)), monitor_out, _abi.stream())
 
     # -- resampling ----------------------------------------------------------
+    # p2p: cross-shard rows are read straight from the peers' memory by the assignment kernel
+    # (CUDA IPC + NVLink loads; every offset from the allgathered counts on the device): no host
+    # plan, no host synchronization and no send / receive per step.  None = decide on first use
+    # (the communicator must offer peer_pointers); False = the host-planned send / receive path.
+    p2p = None
+
+    def _peer_table(self, system, buf):
+        """IPC mappings of every rank's resample workspace and both state buffers (set up once;
+        again only if a buffer moved)."""
+        value = system.value
+        value.alt()  # both halves of the double buffer exist before they are shared
+        tensors = [system.resampler._ws.buf, value._bufs[0], value._bufs[1]]
+        key = tuple(t.data_ptr() for t in tensors)
+        if getattr(self, "_peer_key", None) != key:
+            self._peers = self.comm.peer_pointers(tensors)
+            self._peer_key = key
+        return self._peers
+
     def resample(self, system, scheme, gate, status, rows, row_bytes):
-        """Global resample of this shard's particles; returns True when it ran."""
+        """Global resample of this shard's particles; returns True when it ran (host-planned
+        path) or None (P2P path: whether it ran is decided on the device)."""
         ws_set = system.weight_set
         r = system.resampler
         n = self.n
@@ -159,7 +199,19 @@ class Shard:
         _abi.call("smc_resample_shard_counts", int(scheme), None, lw, st, n, self.n_total, self.n_total, self.world,
                   self.rank, _abi.ptr(totals_all), system.rng_set.seed, self.n_total, ctr, None, 0, None, gate,
                   status, buf, nb, _abi.ptr(self.zsp), _abi.stream())
-        zsp_all = self.comm.allgather(self.zsp).cpu().numpy().reshape(self.world, 4)  # the one host sync
+        zsp_dev = self.comm.allgather(self.zsp)  # (G, 4) {zero slots, surplus children, surplus parents, active}
+        if self.p2p is None:
+            self.p2p = hasattr(self.comm, "peer_pointers") and self.world <= 16
+        if self.p2p:
+            peers = self._peer_table(system, buf)
+            cur = system.value._cur
+            ws_arr = (ctypes.c_void_p * self.world)(*[peers[g][0] for g in range(self.world)])
+            rows_arr = (ctypes.c_void_p * self.world)(*[peers[g][1 + cur] for g in range(self.world)])
+            _abi.call("smc_resample_shard_assign_p2p", _abi.ptr(zsp_dev.contiguous()), self.world, self.rank, ws_arr,
+                      rows_arr, n, rows, row_bytes, _abi.ptr(system.parents), status, buf, nb, _abi.stream())
+            self.last_plan = None
+            return None
+        zsp_all = zsp_dev.cpu().numpy().reshape(self.world, 4)  # the host-planned path's one host sync
         if not zsp_all[self.rank, 3]:
             return False
         plan = exchange_plan(zsp_all[:, 0], zsp_all[:, 1])[self.rank]

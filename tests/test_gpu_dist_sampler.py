@@ -34,6 +34,15 @@ class RankComm:
         s.bar.wait()
         return out
 
+    def peer_pointers(self, tensors):
+        """Threads of one process on one device: every rank's raw addresses are directly usable."""
+        s = self.s
+        s.slots[self.rank] = [t.data_ptr() for t in tensors]
+        s.bar.wait()
+        out = list(s.slots)
+        s.bar.wait()
+        return out
+
     def exchange(self, sends, recvs):
         s = self.s
         for peer, t in sends:
@@ -47,11 +56,13 @@ class RankComm:
         s.bar.wait()
 
 
-def _run_rank(shared, rank, n, obs, steps, scheme, out, errs):
+def _run_rank(shared, rank, n, obs, steps, scheme, out, errs, p2p=None):
     try:
         from paper_1306_5583_b200 import pf
         from paper_1306_5583_b200.dist import Shard
         shard = Shard(n, RankComm(shared, rank))
+        if p2p is not None:
+            shard.p2p = p2p
         s = pf.make_sampler(n, scheme, 0.5, seed=1306, shard=shard)
         s.initialize(obs)
         s.iterate(steps)
@@ -62,8 +73,11 @@ def _run_rank(shared, rank, n, obs, steps, scheme, out, errs):
         shared.bar.abort()
 
 
-@pytest.mark.parametrize("G,scheme", [(2, "systematic"), (4, "stratified"), (3, "residual"), (2, "multinomial")])
-def test_sharded_pf_matches_single_gpu(G, scheme):
+@pytest.mark.parametrize("G,scheme,p2p", [(2, "systematic", None), (4, "stratified", None), (3, "residual", None),
+                                          (2, "multinomial", None), (3, "systematic", False), (4, "residual", False)])
+def test_sharded_pf_matches_single_gpu(G, scheme, p2p):
+    """p2p None: cross-shard rows read from the peers' memory by the assignment kernel (no host
+    plan); False: the host-planned packed send / receive path."""
     from paper_1306_5583_b200 import pf
     n, steps = 2048, 29
     obs, _ = pf.generate_observations(steps + 1, 1306)
@@ -74,7 +88,8 @@ def test_sharded_pf_matches_single_gpu(G, scheme):
     xref = ref.system.value.data.cpu().numpy()
     shared = ThreadComm(G)
     out, errs = [None] * G, []
-    th = [threading.Thread(target=_run_rank, args=(shared, r, n, obs, steps, scheme, out, errs)) for r in range(G)]
+    th = [threading.Thread(target=_run_rank, args=(shared, r, n, obs, steps, scheme, out, errs, p2p))
+          for r in range(G)]
     for t in th:
         t.start()
     for t in th:
