@@ -317,7 +317,11 @@ def run_b200(args):
     s.timing = {}
     s.iterate(min(args.steps, 50), check=False)
     torch.cuda.synchronize()
-    phase = {k: sum(a.elapsed_time(b) for a, b in v) / len(v) for k, v in s.timing.items()}
+    # per-phase medians over the instrumented steps (robust to a stray slow step, e.g. a clock
+    # ramp right after the timed region); the full lists go to stderr for inspection
+    phase_lists = {k: sorted(a.elapsed_time(b) for a, b in v) for k, v in s.timing.items()}
+    phase = {k: v[len(v) // 2] for k, v in phase_lists.items()}
+    print(json.dumps({"phase_ms_sorted": phase_lists}), file=sys.stderr)
     s.timing = None
 
     # ---- roofline of the dominant kernel (the fused move) and of resample+copy ----
