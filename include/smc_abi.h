@@ -184,6 +184,10 @@ int smc_resample(int scheme, const double *w, const double *lw_raw, const smc_ws
 /* Test hook: SMC_DEBUG_FORCE_EXACT_F = 1 makes the stratified/systematic count
  * kernel always take its exact 128-bit path instead of the fp64 fast path
  * with guard band (the two are bit-identical by construction; tests check). */
+/* SMC_DEBUG_MOVE_WS = 0 / 1 selects the PF move kernel: the single-role k_pf_move or the
+ * warp-specialized k_pf_move_ws (Philox producer warps, Box-Muller consumer warps); the two
+ * are bit-identical (tests/test_gpu_weights_pf.py). */
+#define SMC_DEBUG_MOVE_WS 2
 #define SMC_DEBUG_FORCE_EXACT_F 1
 int smc_debug_set(int key, int value);
 

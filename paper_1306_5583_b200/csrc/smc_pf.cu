@@ -28,6 +28,9 @@ constexpr int PB = PF_PB;
 #endif
 constexpr int kPfUnroll = PF_UNROLL;
 constexpr int MB = PB * PF_PPT;  // particles per move block
+#ifndef SMC_MOVE_WS_DEFAULT
+#define SMC_MOVE_WS_DEFAULT 1  // the warp-specialized move (k_pf_move_ws) for N >= 4 blocks per SM
+#endif
 
 struct PfConst {
     double sd_pos0, sd_vel0;  // init: 2, 1
@@ -266,6 +269,170 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialized move (same arithmetic, bit-identical results): a block of 8 warps, 4
+// PRODUCER warps computing the Philox draws (IMAD.WIDE + LOP3: the FMA / ALU pipes) and 4
+// CONSUMER warps doing Box-Muller, the move, the likelihood and the lse/ESS partials (the fp64
+// pipe), so that at any moment the warps of a scheduler mix both instruction streams instead of
+// every warp alternating between a Philox phase and an fp64 phase.  The draws of a stage (one
+// particle per consumer thread) pass through a 2-slot shared-memory ring, [slot][draw][thread]
+// (consecutive threads, consecutive words: conflict-free), handed over with named barriers:
+// FULL (producers arrive, consumers wait) and EMPTY (consumers arrive, producers wait).
+constexpr int WSC = 128;  // consumer threads
+constexpr int WSP = 128;  // producer threads
+constexpr int WST = WSC + WSP;
+SMC_DEV void nbar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+SMC_DEV void nbar_arrive(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+enum { BAR_CONS = 1, BAR_FULL = 2, BAR_EMPTY = 4 };  // FULL / EMPTY: 2 ids each (ring slots)
+
+template <bool MON, int PPT, bool UC>
+__global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, double *x_out,
+                                                  const int32_t *__restrict__ parents, const int32_t *gate,
+                                                  double *__restrict__ lw_raw, int64_t n, uint64_t sbase,
+                                                  double w_equal, const KeySched key, uint64_t *__restrict__ ctrs, const UniformCtr ctr_u,
+                                                  const double *__restrict__ obs, PfConst k, smc_wstate *st, double *__restrict__ incw_out,
+                                                  LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
+{
+    __shared__ PfTabs tabs;
+    __shared__ uint64_t ring[2][8][WSC];
+    __shared__ double s_v[PPT][WSC];
+    __shared__ int32_t s_src[PPT][WSC];
+    const int64_t blk = (int64_t)blockIdx.x * (WSC * PPT);
+    if (threadIdx.x >= WSC) {  // ---------------- producers: the draws ----------------
+        SMC_PDL_WAIT();
+        const int p = threadIdx.x - WSC;
+        for (int q = 0; q < PPT; ++q) {
+            const int slot = q & 1;
+            const int64_t i = blk + (int64_t)q * WSC + p;
+            uint64_t m[8];
+            if (i < n) {
+                const uint64_t si = sbase + (uint64_t)i;
+                if (UC) {
+                    draws_uniform<8>(ctr_u, si, key, m);
+                } else {
+                    const uint64_t c = ctrs[i];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) m[j] = draw53(c + (uint64_t)j, si, key);
+                    ctrs[i] = c + 8;
+                }
+            }
+            if (q >= 2) nbar_sync(BAR_EMPTY + slot, WST);  // the consumers are done with this slot
+            if (i < n) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ring[slot][j][p] = m[j];
+            }
+            nbar_arrive(BAR_FULL + slot, WST);
+        }
+        return;
+    }
+    // ---------------- consumers: Box-Muller, move, likelihood, weights ----------------
+    TabRegs tr;
+    tab_load(tr);  // constant data: requested before the dependency wait
+    SMC_PDL_WAIT();
+    const int64_t base = blk + threadIdx.x;
+    double h0 = 0.0, h1 = 0.0;
+    const NormLw nl = norm_of(st);
+    const bool gathered = parents && (gate == nullptr || *gate != 0);
+    const double xo = obs[0], yo = obs[1];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const int64_t i = base + (int64_t)q * WSC;
+        s_src[q][threadIdx.x] = gathered && i < n ? __ldg(parents + i) : (int32_t)i;
+    }
+    double lw_nx = 0.0;
+    if (base < n && nl.needs_raw()) lw_nx = lw_raw[base];
+#pragma unroll
+    for (int k2 = 0; k2 < 512 / WSC; ++k2) reinterpret_cast<double2 *>(tabs.log)[threadIdx.x + k2 * WSC] = tr.log[k2];
+    reinterpret_cast<double2 *>(tabs.exp)[threadIdx.x] = tr.exp;
+    if (threadIdx.x < 20) reinterpret_cast<double2 *>(tabs.cos)[threadIdx.x] = tr.cos;
+    nbar_sync(BAR_CONS, WSC);
+#pragma unroll 1
+    for (int q = 0; q < PPT; ++q) {
+        const int slot = q & 1;
+        const int64_t i = base + (int64_t)q * WSC;
+        double v = -INFINITY;
+        const int64_t src = s_src[q][threadIdx.x];
+        const double lw_prev = lw_nx;
+        if (q + 1 < PPT && i + WSC < n && nl.needs_raw()) lw_nx = lw_raw[i + WSC];
+        double x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+        if (i < n) ld_row(x_in + 4 * src, x0, x1, x2, x3);  // requested before the wait for the draws
+        nbar_sync(BAR_FULL + slot, WST);
+        uint64_t m[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = ring[slot][j][threadIdx.x];
+        if (q + 2 < PPT) nbar_arrive(BAR_EMPTY + slot, WST);
+        if (i < n) {
+            const double prev = nl(lw_prev);
+            double z[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], FmTabs{tabs.log, tabs.cos});
+            if (MON) {
+                const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);
+                h0 += w * x0;
+                h1 += w * x1;
+            }
+            x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
+            x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
+            x2 = x2 + (0.0 + k.sd_vel * z[2]);
+            x3 = x3 + (0.0 + k.sd_vel * z[3]);
+            st_row(x_out + 4 * i, x0, x1, x2, x3);
+            const double incw = cv_llh(x0, x1, xo, yo, tabs.log);
+            if (incw_out) incw_out[i] = incw;
+            v = prev + incw;
+            if (isnan(v) || v == INFINITY) {
+                raise_status_at(&st->status, SMC_ENORMALIZE, (int64_t)(sbase + (uint64_t)i));
+                v = -INFINITY;
+            }
+            lw_raw[i] = v;
+        }
+        s_v[q][threadIdx.x] = v;
+    }
+    SMC_PDL_TRIGGER();
+    __shared__ double s_red[3][WSC / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double tm = s_v[0][threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < PPT; ++q) tm = fmax(tm, s_v[q][threadIdx.x]);
+    tm = warp_max(tm);
+    if (lane == 0) s_red[0][warp] = tm;
+    nbar_sync(BAR_CONS, WSC);
+    double bm = lane < WSC / 32 ? s_red[0][lane] : -INFINITY;
+    bm = warp_max(bm);
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        const double e = smc_fm::exp(s_v[q][threadIdx.x] - bm, tabs.exp);
+        s1 += e;
+        s2 += e * e;
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (MON) {
+        h0 = warp_sum(h0);
+        h1 = warp_sum(h1);
+    }
+    nbar_sync(BAR_CONS, WSC);
+    if (lane == 0) {
+        s_red[1][warp] = s1;
+        s_red[2][warp] = s2;
+        if (MON) { s_v[0][warp] = h0; s_v[1 % PPT][WSC / 32 + warp] = h1; }
+    }
+    nbar_sync(BAR_CONS, WSC);
+    if (threadIdx.x == 0) {
+        LsePartial pp{bm, 0.0, 0.0};
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < WSC / 32; ++w) {
+            pp.s1 += s_red[1][w];
+            pp.s2 += s_red[2][w];
+            if (MON) { a += s_v[0][w]; b += s_v[1 % PPT][WSC / 32 + w]; }
+        }
+        parts[blockIdx.x] = pp;
+        if (MON) mon_parts[blockIdx.x] = make_double2(a, b);
+    }
+}
+
+int h_move_ws = SMC_MOVE_WS_DEFAULT;  // which move kernel runs (smc_debug_set SMC_DEBUG_MOVE_WS)
+
 PfConst pf_constants()
 {
     PfConst k;
@@ -347,7 +514,14 @@ static int pf_move(const double *x_in, double *x, const int32_t *parents, const 
     const UniformCtr cu = make_uniform_ctr(ctr_u ? *ctr_u : 0, key);
 #define SMC_PF_MOVE(MONV, PPTV, MONP)                                                                          \
     do {                                                                                                       \
-        if (ctr_u)                                                                                             \
+        if (h_move_ws && PPTV == PF_PPT && PB == WSC) {                                                        \
+            if (ctr_u)                                                                                         \
+                smc_launch(k_pf_move_ws<MONV, PF_PPT, true>, nb, WST, 0, s, x_in, x, parents, gate, lw_raw, n,  \
+                           stream_base, w_eq, key, ctrs, cu, obs_t, pf_constants(), st, incw_out, parts, MONP); \
+            else                                                                                               \
+                smc_launch(k_pf_move_ws<MONV, PF_PPT, false>, nb, WST, 0, s, x_in, x, parents, gate, lw_raw, n, \
+                           stream_base, w_eq, key, ctrs, cu, obs_t, pf_constants(), st, incw_out, parts, MONP); \
+        } else if (ctr_u)                                                                                      \
             smc_launch(k_pf_move<MONV, PPTV, true>, nb, PB, 0, s, x_in, x, parents, gate, lw_raw, n, stream_base, \
                        w_eq, key, ctrs, cu, obs_t, pf_constants(), st, incw_out, parts, MONP);                \
         else                                                                                                   \
@@ -381,4 +555,10 @@ extern "C" int smc_pf_move_uniform(const double *x_in, double *x, const int32_t 
 {
     return pf_move(x_in, x, parents, gate, lw_raw, n, stream_base, n_total, seed, nullptr, &ctr, obs_t, st, incw_out,
                    monitor_prev, partial_out, ws, ws_bytes, stream, "smc_pf_move_uniform");
+}
+
+int smc_pf_set_move_ws(int on)  // smc_debug_set(SMC_DEBUG_MOVE_WS, on) (A/B and the bit-identity test)
+{
+    h_move_ws = on;
+    return SMC_OK;
 }

@@ -1758,8 +1758,11 @@ extern "C" int smc_gather_rows(void *dst, const void *src, int64_t row_bytes, co
     return smc_check_launch("smc_gather_rows");
 }
 
+int smc_pf_set_move_ws(int on);  // smc_pf.cu
+
 extern "C" int smc_debug_set(int key, int value)
 {
+    if (key == SMC_DEBUG_MOVE_WS) return smc_pf_set_move_ws(value);
     if (key != SMC_DEBUG_FORCE_EXACT_F) return smc_set_error(SMC_EINVAL, "smc_debug_set: unknown key %d", key);
     cudaError_t e = cudaMemcpyToSymbol(g_force_exact, &value, sizeof(int));
     return e == cudaSuccess ? SMC_OK : smc_set_error(SMC_ECUDA, "smc_debug_set: %s", cudaGetErrorString(e));

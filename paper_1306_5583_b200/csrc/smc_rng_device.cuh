@@ -180,22 +180,30 @@ inline UniformCtr make_uniform_ctr(uint64_t ctr, const KeySched &ks)
 }
 #endif
 
+// The 53-bit draw integers of draws ctr .. ctr + ND - 1 of one stream, for the counter `u`
+// describes and stream < 2^32 (bit-identical to draw53).
+template <int ND, class K>
+SMC_DEV void draws_uniform(const UniformCtr &u, uint64_t stream, const K &key, uint64_t (&m)[ND])
+{
+    static_assert(ND <= 16, "UniformCtr holds 16 draws");
+    const uint32_t c2 = (uint32_t)stream;
+    const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;  // round 1, every draw
+    const uint32_t n0 = hi1 ^ u.c1k;
+    const uint32_t hi0b = __umulhi(PHILOX_M0, n0), lo0b = PHILOX_M0 * n0;  // round 2, every draw
+#pragma unroll
+    for (int j = 0; j < ND; ++j) {
+        const uint4 w = philox_rounds<2>(u.a[j] ^ lo1, u.b[j], hi0b ^ u.c[j], lo0b, key);
+        m[j] = ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
+    }
+}
+
 // normals_at(ctr, stream, ...) for the counter `u` describes and stream < 2^32: bit-identical.
 template <int NZ, class K>
 SMC_DEV void normals_uniform(const UniformCtr &u, uint64_t stream, const K &key, double (&z)[NZ],
                              FmTabs tabs = FmTabs{})
 {
-    static_assert(2 * NZ <= 16, "UniformCtr holds 16 draws");
-    const uint32_t c2 = (uint32_t)stream;
-    const uint32_t hi1 = __umulhi(PHILOX_M1, c2), lo1 = PHILOX_M1 * c2;  // round 1, every draw
-    const uint32_t n0 = hi1 ^ u.c1k;
-    const uint32_t hi0b = __umulhi(PHILOX_M0, n0), lo0b = PHILOX_M0 * n0;  // round 2, every draw
     uint64_t m[2 * NZ];
-#pragma unroll
-    for (int j = 0; j < 2 * NZ; ++j) {
-        const uint4 w = philox_rounds<2>(u.a[j] ^ lo1, u.b[j], hi0b ^ u.c[j], lo0b, key);
-        m[j] = ((uint64_t)(w.x >> 5) << 26) | (uint64_t)(w.y >> 6);
-    }
+    draws_uniform<2 * NZ>(u, stream, key, m);
 #pragma unroll
     for (int j = 0; j < NZ; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], tabs);
 }

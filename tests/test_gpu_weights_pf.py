@@ -338,3 +338,30 @@ def test_lazy_uniform_counts_are_materialized_for_every_consumer():
     s.iterate(1)  # the counter-array kernel from here on
     c = rs.counters_host()
     assert c[5] == 41 and c[:5] == [40] * 5 and c[6:n] == [40] * (n - 6)
+
+
+@pytest.mark.parametrize("uniform", [True, False])
+def test_warp_specialized_move_is_bit_identical(uniform):
+    """k_pf_move_ws (Philox producer warps + Box-Muller consumer warps, draws handed over through a
+    shared-memory ring) and the single-role k_pf_move compute the same arithmetic: identical state,
+    log-weights, history and log Z, for the uniform-count and the counter-array move."""
+    from paper_1306_5583_b200 import _abi, pf
+    obs, _ = _obs(12)
+    n = (1 << 20) + 77  # >= 4 blocks per SM (the path both kernels serve) and a partial last block
+    runs = []
+    for ws in (0, 1):
+        _abi.call("smc_debug_set", 2, ws)  # SMC_DEBUG_MOVE_WS
+        try:
+            s = pf.make_sampler(n, "systematic", 0.5, seed=21)
+            s.graph = False
+            s.initialize(obs)
+            if not uniform:
+                _ = s.system.rng_set.counters  # materialized: the counter-array kernel from here on
+            s.iterate(11)
+            runs.append((s.history_array(), s.system.value.data.cpu().numpy(),
+                         s.system.weight_set.read_log_weight().cpu().numpy(), s.log_zconst,
+                         s.system.rng_set.counters_host()[:5]))
+        finally:
+            _abi.call("smc_debug_set", 2, 1)
+    (h0, x0, w0, z0, c0), (h1, x1, w1, z1, c1) = runs
+    assert np.array_equal(h0, h1) and np.array_equal(x0, x1) and np.array_equal(w0, w1) and z0 == z1 and c0 == c1
