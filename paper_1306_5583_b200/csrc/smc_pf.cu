@@ -29,7 +29,7 @@ constexpr int PB = PF_PB;
 constexpr int kPfUnroll = PF_UNROLL;
 constexpr int MB = PB * PF_PPT;  // particles per move block
 #ifndef SMC_MOVE_WS_DEFAULT
-#define SMC_MOVE_WS_DEFAULT 1  // the warp-specialized move (k_pf_move_ws) for N >= 4 blocks per SM
+#define SMC_MOVE_WS_DEFAULT 0  // the single-role move; the warp-specialized k_pf_move_ws measured slower (profiles/r2_move_ws_ab.txt)
 #endif
 
 struct PfConst {
@@ -283,7 +283,8 @@ constexpr int WSP = 128;  // producer threads
 constexpr int WST = WSC + WSP;
 SMC_DEV void nbar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 SMC_DEV void nbar_arrive(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
-enum { BAR_CONS = 1, BAR_FULL = 2, BAR_EMPTY = 4 };  // FULL / EMPTY: 2 ids each (ring slots)
+constexpr int WS_SLOTS = 3;  // ring slots: the producers may run up to 3 stages ahead (48 KB static shared)
+enum { BAR_CONS = 1, BAR_FULL = 2, BAR_EMPTY = 2 + WS_SLOTS };  // FULL / EMPTY: one id per ring slot
 
 template <bool MON, int PPT, bool UC>
 __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, double *x_out,
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, doubl
                                                   LsePartial *__restrict__ parts, double2 *__restrict__ mon_parts)
 {
     __shared__ PfTabs tabs;
-    __shared__ uint64_t ring[2][8][WSC];
+    __shared__ double2 ring[WS_SLOTS][4][WSC];  // Box-Muller arguments (1 - u1, 2 pi u2) per normal
     __shared__ double s_v[PPT][WSC];
     __shared__ int32_t s_src[PPT][WSC];
     const int64_t blk = (int64_t)blockIdx.x * (WSC * PPT);
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, doubl
         SMC_PDL_WAIT();
         const int p = threadIdx.x - WSC;
         for (int q = 0; q < PPT; ++q) {
-            const int slot = q & 1;
+            const int slot = q % WS_SLOTS;
             const int64_t i = blk + (int64_t)q * WSC + p;
             uint64_t m[8];
             if (i < n) {
@@ -316,10 +317,13 @@ __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, doubl
                     ctrs[i] = c + 8;
                 }
             }
-            if (q >= 2) nbar_sync(BAR_EMPTY + slot, WST);  // the consumers are done with this slot
+            double2 a[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[j] = box_muller_args(m[2 * j], m[2 * j + 1]);  // conversions here too
+            if (q >= WS_SLOTS) nbar_sync(BAR_EMPTY + slot, WST);  // the consumers are done with this slot
             if (i < n) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) ring[slot][j][p] = m[j];
+                for (int j = 0; j < 4; ++j) ring[slot][j][p] = a[j];  // 128-bit stores, conflict-free
             }
             nbar_arrive(BAR_FULL + slot, WST);
         }
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, doubl
     nbar_sync(BAR_CONS, WSC);
 #pragma unroll 1
     for (int q = 0; q < PPT; ++q) {
-        const int slot = q & 1;
+        const int slot = q % WS_SLOTS;
         const int64_t i = base + (int64_t)q * WSC;
         double v = -INFINITY;
         const int64_t src = s_src[q][threadIdx.x];
@@ -357,15 +361,15 @@ __global__ void __launch_bounds__(WST, 4) k_pf_move_ws(const double *x_in, doubl
         double x0 = 0, x1 = 0, x2 = 0, x3 = 0;
         if (i < n) ld_row(x_in + 4 * src, x0, x1, x2, x3);  // requested before the wait for the draws
         nbar_sync(BAR_FULL + slot, WST);
-        uint64_t m[8];
+        double2 a[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m[j] = ring[slot][j][threadIdx.x];
-        if (q + 2 < PPT) nbar_arrive(BAR_EMPTY + slot, WST);
+        for (int j = 0; j < 4; ++j) a[j] = ring[slot][j][threadIdx.x];
+        if (q + WS_SLOTS < PPT) nbar_arrive(BAR_EMPTY + slot, WST);
         if (i < n) {
             const double prev = nl(lw_prev);
             double z[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) z[j] = box_muller53(m[2 * j], m[2 * j + 1], FmTabs{tabs.log, tabs.cos});
+            for (int j = 0; j < 4; ++j) z[j] = box_muller_from(a[j], FmTabs{tabs.log, tabs.cos});
             if (MON) {
                 const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);
                 h0 += w * x0;

@@ -97,13 +97,21 @@ struct FmTabs {
     const smc_fm::CosPoly *cos = nullptr;
 };
 
+// Box-Muller's two arguments from the draw integers: 1 - u1 = 1 - m1 2^-53 in [2^-53, 1]
+// (exact, one FMA): a positive normal double, as log_core requires; fl(2 pi u2) =
+// fl((2 pi 2^-53) m2), the power-of-two scale being exact
+SMC_DEV double2 box_muller_args(uint64_t m1, uint64_t m2)
+{
+    return make_double2(__fma_rn(-__ull2double_rn(m1), 1.0 / 9007199254740992.0, 1.0),
+                        __dmul_rn(__ull2double_rn(m2), (2.0 * 3.141592653589793) / 9007199254740992.0));
+}
+SMC_DEV double box_muller_from(double2 a, FmTabs tabs = FmTabs{})
+{
+    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(a.x, tabs.log)) * smc_fm::cos_bm(a.y, tabs.cos);
+}
 SMC_DEV double box_muller53(uint64_t m1, uint64_t m2, FmTabs tabs = FmTabs{})
 {
-    // 1 - u1 = 1 - m1 2^-53 in [2^-53, 1] (exact, one FMA): a positive normal double, as
-    // log_core requires; fl(2 pi u2) = fl((2 pi 2^-53) m2), the power-of-two scale being exact
-    const double v1 = __fma_rn(-__ull2double_rn(m1), 1.0 / 9007199254740992.0, 1.0);
-    const double x2 = __dmul_rn(__ull2double_rn(m2), (2.0 * 3.141592653589793) / 9007199254740992.0);
-    return smc_fm::sqrt_bm(-2.0 * smc_fm::log_core(v1, tabs.log)) * smc_fm::cos_bm(x2, tabs.cos);
+    return box_muller_from(box_muller_args(m1, m2), tabs);
 }
 
 template <class K>

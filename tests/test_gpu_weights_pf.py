@@ -362,6 +362,6 @@ def test_warp_specialized_move_is_bit_identical(uniform):
                          s.system.weight_set.read_log_weight().cpu().numpy(), s.log_zconst,
                          s.system.rng_set.counters_host()[:5]))
         finally:
-            _abi.call("smc_debug_set", 2, 1)
+            _abi.call("smc_debug_set", 2, 0)  # back to the default (single-role) move
     (h0, x0, w0, z0, c0), (h1, x1, w1, z1, c1) = runs
     assert np.array_equal(h0, h1) and np.array_equal(x0, x1) and np.array_equal(w0, w1) and z0 == z1 and c0 == c1
