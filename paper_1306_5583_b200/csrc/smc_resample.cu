@@ -518,6 +518,133 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
     }
 }
 
+// One GPU, nt <= 8 SB tiles (N <= 2^24): the same results as k_rs_scan in ONE pass over the
+// tile sums -- each lane keeps its <= 8 tiles (the chunked layout the scan needs) in registers
+// for both the totals and the scan, the block reduction ends in warp shuffles instead of a
+// serial loop, and the header's dependent loads (status, stream counter) are issued at entry.
+template <bool RES>
+__global__ void __launch_bounds__(SB) k_rs_scan1(int scheme, int64_t n, int64_t nt, uint64_t m_out, Key key,
+                                                 uint64_t stream, uint64_t *ctr, const double *__restrict__ u,
+                                                 int64_t n_u, const int32_t *gate, int32_t *status, Layout L)
+{
+    SMC_PDL_WAIT();
+    RsHeader *h = L.hdr;
+    if (gate && *gate == 0) {
+        if (threadIdx.x == 0) h->active = 0;
+        return;
+    }
+    __shared__ u128 s_q[SB / 32];
+    __shared__ uint64_t s_qr[SB / 32], s_w[SB / 32];
+    __shared__ int64_t s_f[SB / 32];
+    __shared__ int s_ok;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t st0 = 0;
+    uint64_t c00 = 0;
+    if (threadIdx.x == 0) {  // the header's own loads, in flight while the tiles are summed
+        st0 = status ? *status : 0;
+        c00 = u ? 0 : *ctr;
+    }
+    constexpr int NW = SB / 32, KS = 8;
+    const int64_t C = (nt + NW - 1) / NW;  // <= 8 * 32: warp w owns tiles [w C, (w+1) C)
+    const int64_t w0 = min((int64_t)warp * C, nt), w1 = min(w0 + C, nt);
+    uint64_t v[KS];
+    u128 tq = 0;
+    uint64_t tqr = 0, wsum = 0;
+    int64_t tf = 0;
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+        const int64_t b = w0 + 32 * k + lane;
+        const bool in = b < w1;
+        const u128 q = in ? L.tile_q[b] : (u128)0;
+        const uint64_t qr = RES && in ? L.tile_qr[b] : 0;
+        tq += q;
+        if (RES) {
+            tqr += qr;
+            tf += in ? L.tile_f[b] : 0;
+        }
+        v[k] = RES ? qr : (uint64_t)q;
+        wsum += v[k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        tq += shfl_xor_u128(tq, o);
+        wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+        if (RES) {
+            tqr += __shfl_xor_sync(0xffffffffu, tqr, o);
+            tf += __shfl_xor_sync(0xffffffffu, tf, o);
+        }
+    }
+    if (lane == 0) { s_q[warp] = tq; s_qr[warp] = tqr; s_f[warp] = tf; s_w[warp] = wsum; }
+    __syncthreads();
+    if (warp == 0) {  // the totals by shuffles; thread 0 then builds the header
+        u128 T = s_q[lane];
+        uint64_t Tr = RES ? s_qr[lane] : 0;
+        int64_t F = RES ? s_f[lane] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            T += shfl_xor_u128(T, o);
+            if (RES) {
+                Tr += __shfl_xor_sync(0xffffffffu, Tr, o);
+                F += __shfl_xor_sync(0xffffffffu, F, o);
+            }
+        }
+        const uint64_t x = s_w[lane];  // exclusive prefix of the warps' chunks
+        const uint64_t inc = warp_inclusive_sum(x);
+        s_w[lane] = inc - x;
+        if (lane == 0) {
+            h->qoff = 0;
+            int ok = (st0 == 0);
+            if (T < (u128)T_LO || T > (u128)T_HI) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+            int64_t M = (int64_t)m_out;
+            uint64_t Tm = (uint64_t)T;
+            if (ok && RES && n > 1) {
+                M = (int64_t)m_out - F;
+                if (M < 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+                if (M > 0 && Tr == 0) { raise_status(status, SMC_EUNNORMALIZED); ok = 0; }
+                Tm = Tr;
+            }
+            int64_t draws = 0;
+            if (n > 1 && M > 0) draws = is_systematic(scheme) ? 1 : M;
+            if (ok && u && n_u < draws) { raise_status(status, SMC_EUNIFORMS); ok = 0; }
+            h->T = (uint64_t)T;
+            h->Tm = Tm;
+            h->M = (uint64_t)(M > 0 ? M : 0);
+            h->ratio = Tm ? (double)(M > 0 ? M : 0) / (double)Tm : 0.0;
+            h->guard = (double)(M > 0 ? M : 1) * 7.105427357601002e-15;
+            h->draws = draws;
+            h->trivial = (n == 1);
+            h->Z_total = h->S_total = h->P_total = 0;
+            if (ok) {
+                h->c0 = c00;
+                if (!u) *ctr = c00 + (uint64_t)draws;
+                if (is_systematic(scheme))
+                    h->m_sys = draws ? (u ? (uint64_t)(u[0] * TWO53) : draw53(c00, stream, key)) : 0;
+            }
+            h->active = ok;
+            h->mn_direct = 0;
+            h->mn_rb = Tm ? ldexp(1.0, mn_geom(n).kb) / (double)Tm : 0.0;
+            s_ok = ok;
+        }
+    }
+    if (is_multinomial(scheme)) {  // the multinomial bins: empty, every start at the last particle
+        const MnGeom g = mn_geom(n);
+        for (int64_t b = threadIdx.x; b <= g.nb; b += SB) {
+            L.mn_fill[b] = 0;
+            L.mn_start[b] = (uint32_t)(n - 1);
+        }
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    uint64_t carry = s_w[warp];  // (qoff = 0 on one GPU)
+#pragma unroll
+    for (int k = 0; k < KS; ++k) {
+        const int64_t b = w0 + 32 * k + lane;
+        const uint64_t inc = warp_inclusive_sum(v[k]);
+        if (b < w1) L.tile_pre[b] = carry + inc - v[k];
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+}
+
 // ---------------------------------------------- multinomial / residual (M) --
 // Materialize the inclusive CDF Q (or Q') so each draw can binary-search it.
 __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t n, double m_out, double rscale,
@@ -975,7 +1102,6 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
 {
     SMC_PDL_WAIT();
     RsHeader *h = L.hdr;
-    if (!h->active || h->trivial) return;
     __shared__ uint64_t s_zp[SB / 32 + 1], s_s[SB / 32 + 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = SB / 32;
@@ -984,8 +1110,17 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
     // (Z, P) as two 32-bit halves of one u64 (totals < 2^31 never carry), S as u64
     auto zp = [&](uint64_t v) { return ((uint64_t)unz(v) << 32) | unp(v); };
     constexpr int KS = 8;  // warp-rows of tiles in flight per round (one round trip per round)
+    // nt <= 8 SB (N <= 2^24): the first round's loads are all of them, kept for the scan; they are
+    // issued together with the header's flags (the aggregates are valid workspace either way)
+    const bool one = C <= 32 * KS;
+    uint64_t v0[KS];
+#pragma unroll
+    for (int k = 0; k < KS; ++k) v0[k] = w0 + lane + 32 * k < w1 ? L.tile_zsp[w0 + lane + 32 * k] : 0;
+    if (!h->active || h->trivial) return;
     uint64_t a = 0, bs = 0;
-    for (int64_t t0 = w0 + lane; t0 < w1; t0 += 32 * KS) {
+#pragma unroll
+    for (int k = 0; k < KS; ++k) { a += zp(v0[k]); bs += uns(v0[k]); }
+    for (int64_t t0 = w0 + lane + 32 * KS; t0 < w1; t0 += 32 * KS) {
         uint64_t v[KS];
 #pragma unroll
         for (int k = 0; k < KS; ++k) v[k] = t0 + 32 * k < w1 ? L.tile_zsp[t0 + 32 * k] : 0;
@@ -1015,10 +1150,7 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
     }
     __syncthreads();
     uint64_t ca = s_zp[warp], cs = s_s[warp];
-    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
-        uint64_t vv[KS];
-#pragma unroll
-        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.tile_zsp[c0 + 32 * k + lane] : 0;
+    auto emit = [&](int64_t c0, const uint64_t(&vv)[KS]) {
 #pragma unroll
         for (int k = 0; k < KS; ++k) {
             const int64_t t = c0 + 32 * k + lane;
@@ -1032,6 +1164,16 @@ __global__ void __launch_bounds__(SB) k_rs_zsp_scan(int64_t nt, int whole, int32
             ca += __shfl_sync(0xffffffffu, ix, 31);
             cs += __shfl_sync(0xffffffffu, iy, 31);
         }
+    };
+    if (one) {
+        emit(w0, v0);
+        return;
+    }
+    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
+        uint64_t vv[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.tile_zsp[c0 + 32 * k + lane] : 0;
+        emit(c0, vv);
     }
 }
 
@@ -1693,8 +1835,18 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     const double mo = (double)m_out;
 
     launch_tiles(scheme, (unsigned)nt, s, src, n, mo, rscale, u, n_u, gate, status, L);
-    smc_launch(k_rs_scan, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status, L,
-                               nullptr, 1, 0, n);
+    if (nt <= (int64_t)SB * 8 / 32 * 32) {  // one pass with the tile sums in registers (N <= 2^24)
+        const bool res = scheme == SMC_RESIDUAL || scheme == SMC_RESIDUAL_STRATIFIED || scheme == SMC_RESIDUAL_SYSTEMATIC;
+        if (res)
+            smc_launch(k_rs_scan1<true>, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u,
+                       gate, status, L);
+        else
+            smc_launch(k_rs_scan1<false>, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u,
+                       gate, status, L);
+    } else {
+        smc_launch(k_rs_scan, 1, SB, 0, s, scheme, n, nt, (uint64_t)m_out, key, stream_index, ctr, u, n_u, gate, status,
+                   L, nullptr, 1, 0, n);
+    }
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
