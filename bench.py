@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gmm", action="store_true")
+    ap.add_argument("--no-config1", action="store_true")
     return ap.parse_args()
 
 
@@ -179,6 +180,38 @@ def cpu_baseline_pf(n, steps, scheme, obs, threads):
         times.append(time.perf_counter() - t0)
         assert rc == 0
     return times
+
+
+def config1_gpu(P):
+    """BASELINE config 1 (the reference's own CPU-runnable case): the paper's PF at N = 10^4,
+    100 observations, systematic at ESS < N/2 -- initialize + 99 iterations through the Sampler
+    API (CUDA-graph replay on), wall time with a device synchronize on both sides, best of 3
+    after one untimed run (which includes the graph capture).  Launch-latency bound."""
+    import torch
+    obs = bench_obs(100)
+    s = P.pf.make_sampler(10000, "systematic", 0.5, seed=1306)
+    best = None
+    for rep in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.initialize(obs)
+        s.iterate(99)
+        s.flush()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if rep:
+            best = dt if best is None else min(best, dt)
+    return {"workload": "PF config 1: N=10^4, 100 observations, systematic, ESS < N/2 (initialize + 99 "
+                        "iterations, CUDA graphs on)", "value": 10000 * 100 / best, "unit": UNIT,
+            "us_per_step": best / 100 * 1e6}
+
+
+def config1_cpu(threads):
+    """The C oracle on the same config-1 run: initialize + 99 steps, seconds (wall)."""
+    obs = bench_obs(100)
+    t0 = time.perf_counter()
+    times = cpu_baseline_pf(10000, 99, "systematic", obs, threads)
+    return time.perf_counter() - t0, times
 
 
 def cpu_model():
@@ -388,6 +421,8 @@ def run_b200(args):
                                        f"{world} GPUs = value / (strong_baseline.value * {world})")
     if rank == 0 and world == 1 and not args.no_schemes and args.n is None and config_of(args, world) == 2:
         line["schemes"] = schemes_bench(P, n, args, obs)
+    if rank == 0 and world == 1 and not args.no_config1:
+        line["config1"] = config1_gpu(P)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_line(n, args.scheme, obs)
     if rank == 0:
@@ -459,7 +494,10 @@ def cpu_baseline_line(n, scheme, obs):
             "sample": f"{len(tm)} full PF steps of the C oracle at the workload's N={n} (after 1 untimed step), "
                       f"OpenMP over {cores} threads for the per-particle loops",
             "sequential": {"value": n / t1[0], "unit": UNIT, "cores": 1,
-                           "sample": f"1 full PF step of the C oracle at N={n} on one thread"}}
+                           "sample": f"1 full PF step of the C oracle at N={n} on one thread"},
+            "config1": {f"cores_{c}": {"value": 10000 * 100 / config1_cpu(c)[0], "unit": UNIT, "cores": c}
+                        for c in sorted({1, cores})} | {
+                "sample": "config 1 in full: the C oracle's initialize + 99 PF steps at N=10^4 (wall)"}}
 
 
 def gmm_bench(P, n=1 << 20, T=100):

@@ -36,6 +36,9 @@ using namespace smc;
 namespace {
 
 constexpr int RT = 256;
+#ifndef RS_TILES_MINB_W
+#define RS_TILES_MINB_W 8  // pass A from an explicit W vector, not residual: 8 blocks/SM (32 registers)
+#endif
 #ifndef RS_TILES_MINB
 #define RS_TILES_MINB 6  // pass A: 6 blocks/SM (40 registers, no spills of the branch-free item loop)
 #endif
@@ -86,6 +89,7 @@ struct Layout {
     uint32_t *mn_fill;  // multinomial: positions per bin (reserved runs)
     uint64_t *mn_pos;   // multinomial: positions by bin, `cap` slots per bin
     uint32_t *mn_start; // multinomial: first particle reached by every bin's positions (B + 1)
+    uint32_t *mn_cnt, *mn_off;  // MN1: draws per position bin, bin offsets in mn_pos
     size_t bytes;
 };
 
@@ -114,6 +118,34 @@ __host__ __device__ inline MnGeom mn_geom(int64_t n)
     return g;
 }
 
+// The binned kernels' shared memory (k_mn2_scatter: a block's 12288 draws + 3 words per bin;
+// k_mn2_count: a bin's `cap` positions + 2 x 8193 sub-bucket words).  Past N ~ 2^26 a bin no
+// longer fits one block's shared memory: those N take the global-memory bucket path (MN1).
+constexpr int MT = 1024;          // threads of the multinomial kernels
+constexpr int MDPT = 12;          // draws per thread in k_mn2_scatter
+constexpr int MCH = MT * MDPT;    // draws per scatter block
+constexpr int NSB = 4096;         // most sub-buckets of a bin in k_mn2_count (~2 positions each)
+constexpr size_t MN_SMEM_MAX = 232448;  // 227 KB: the sm_100 per-block opt-in maximum
+__host__ __device__ inline size_t mn2_scatter_smem(int64_t n)
+{
+    return (size_t)MCH * (8 + 2 + 2) + (size_t)mn_geom(n).nb * 12 + 64;
+}
+__host__ __device__ inline size_t mn2_count_smem(int64_t n)
+{
+    return (size_t)mn_geom(n).cap * 8 + (size_t)(NSB + 1) * 4 * 2 + 64;
+}
+__host__ __device__ inline bool mn2_fits(int64_t n)
+{
+    return mn2_scatter_smem(n) <= MN_SMEM_MAX && mn2_count_smem(n) <= MN_SMEM_MAX;
+}
+// MN1 (N past mn2_fits): ~256 particles per position bin, at most 2^17 bins
+constexpr int64_t MN1_MAX_BINS = 1 << 17;
+__host__ __device__ inline int64_t mn1_bins(int64_t n)
+{
+    const int64_t b = (n + 255) / 256;
+    return b < MN1_MAX_BINS ? b : MN1_MAX_BINS;
+}
+
 Layout layout(void *ws, int64_t n)
 {
     const int64_t nt = (n + TILE - 1) / TILE;
@@ -136,9 +168,13 @@ Layout layout(void *ws, int64_t n)
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
     const MnGeom mg = mn_geom(n);
-    L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (mg.nb + 1));
-    L.mn_pos = (uint64_t *)take(sizeof(uint64_t) * mg.nb * mg.cap);
-    L.mn_start = (uint32_t *)take(sizeof(uint32_t) * (mg.nb + 2));
+    const bool mn2 = mn2_fits(n);
+    const int64_t nb1 = mn2 ? 0 : mn1_bins(n), nbm = mg.nb > nb1 ? mg.nb : nb1;
+    L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (nbm + 1));
+    L.mn_pos = (uint64_t *)take(sizeof(uint64_t) * (mn2 ? mg.nb * mg.cap : n));  // MN1: capacity n positions
+    L.mn_start = (uint32_t *)take(sizeof(uint32_t) * (nbm + 2));
+    L.mn_cnt = (uint32_t *)take(sizeof(uint32_t) * (nb1 + 1));
+    L.mn_off = (uint32_t *)take(sizeof(uint32_t) * (nb1 + 1));
     L.bytes = o;
     return L;
 }
@@ -215,7 +251,7 @@ SMC_DEV Quant quantize(double W, bool residual, double m_out, double rscale, boo
 // LW: the weights come from the raw log weights + the weight record (the sampler's
 // path: the table exp staged in shared memory); otherwise from an explicit W vector.
 template <bool RES, bool MULTI, bool LW>  // scheme family and weight source: resolved at compile time
-__global__ void __launch_bounds__(RT, RS_TILES_MINB) k_rs_tiles(int scheme, WSrc src, int64_t n, double m_out, double rscale,
+__global__ void __launch_bounds__(RT, LW || RES ? RS_TILES_MINB : RS_TILES_MINB_W) k_rs_tiles(int scheme, WSrc src, int64_t n, double m_out, double rscale,
                                                  const double *__restrict__ u, int64_t n_u, const int32_t *gate,
                                                  int32_t *status, Layout L)
 {
@@ -652,6 +688,10 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
 {
     SMC_PDL_WAIT();
     if (!L.hdr->active || L.hdr->trivial) return;
+    if (!mn2_fits(n)) {  // MN1: zero the bin counters (mn1_bins <= n / 256 + 1 <= nt * RT)
+        const int64_t b = (int64_t)blockIdx.x * RT + threadIdx.x;
+        if (b <= mn1_bins(n)) L.mn_cnt[b] = 0;
+    }
     if (L.hdr->M == 0) return;
     __shared__ uint64_t sm[RT / 32 + 1];
     __shared__ uint64_t s_io[tile_smem_elems<uint64_t, RT, RI>()];
@@ -721,14 +761,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
 //      coalesced stores -- atomics only for the two end particles a neighbouring bin can
 //      share.
 // Counts are order-independent integer sums: bit-identical to any other evaluation order.
-constexpr int MT = 1024;          // threads of the multinomial kernels
-constexpr int MDPT = 12;          // draws per thread in k_mn2_scatter
-constexpr int MCH = MT * MDPT;    // draws per scatter block
 
-inline size_t mn2_scatter_smem(int64_t n)
-{
-    return (size_t)MCH * (8 + 2 + 2) + (size_t)mn_geom(n).nb * 12 + 64;
-}
 
 SMC_DEV uint64_t mn_m(uint64_t k, uint64_t c0, const Key &key, uint64_t stream, const double *u)
 {
@@ -824,8 +857,6 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
 // from the sub-bucket prefix, the two end sub-buckets element by element -- O(1) per particle
 // and per position, no search.  Interior particles are reached by this bin only (plain
 // coalesced stores); the two end particles may be shared with a neighbour (atomics).
-constexpr int NSB = 8192;
-inline size_t mn2_count_smem(int64_t n) { return (size_t)mn_geom(n).cap * 8 + (size_t)(NSB + 1) * 4 * 2 + 64; }
 
 __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
 {
@@ -841,9 +872,13 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
     const uint64_t mmax = ((uint64_t)(b + 1) << (53 - g.kb)) - 1;
     const uint64_t hi_b = (uint64_t)(((u128)mmax * Tm) >> 53);  // the bin's largest position
     const uint64_t span = hi_b - lo_b;
-    // smallest sh2 with span >> sh2 < NSB (one clz, not a loop)
-    int sh2 = span ? max(0, 64 - __clzll((long long)span) - 13) : 0;  // NSB = 2^13
-    while ((span >> sh2) >= (uint64_t)NSB) ++sh2;
+    // sub-buckets: a power of two 2^lt >= cnt / 2 (64 .. NSB), so ~2 positions each whatever the
+    // draw count (a residual's few remainder draws scan a short prefix); the smallest sh2 with
+    // span >> sh2 < 2^lt (one clz, not a loop)
+    const int lt = min(12, max(6, 32 - __clz((int)max((int64_t)1, cnt / 2) - 1)));
+    static_assert(NSB == 1 << 12, "lt <= 12");
+    int sh2 = span ? max(0, 64 - __clzll((long long)span) - lt) : 0;
+    while ((span >> sh2) >= ((uint64_t)1 << lt)) ++sh2;
     const int nsb = (int)(span >> sh2) + 1;
     extern __shared__ __align__(16) unsigned char c_sm[];
     uint64_t *Ps = reinterpret_cast<uint64_t *>(c_sm);                 // positions sorted by sub-bucket
@@ -878,7 +913,7 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
         for (int64_t j = threadIdx.x; j < cnt; j += MT) atomicAdd(&cur[(pos[j] - lo_b) >> sh2], 1u);
     }
     __syncthreads();
-    {  // exclusive scan of the nsb <= 8192 sub-bucket counts, 8 per thread
+    {  // exclusive scan of the nsb <= NSB sub-bucket counts, 4 per thread
         constexpr int SPT = NSB / MT;
         uint32_t c8[SPT], sum = 0;
 #pragma unroll
@@ -953,6 +988,199 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
         } else {
             L.cnt[i] = (int32_t)c;  // only this bin reaches it
         }
+    }
+}
+
+// ---- MN1: the multinomial path for N past mn2_fits (round 1's; every draw regenerated from its
+// counter in two passes).  Draws COUNTED then SCATTERED into ~256-particle position bins in
+// global memory (bin = an arithmetic, monotone function of P), each bucketed position then
+// searched between its bin's first particles: a warp's 32 searches share their paths down to
+// the last few levels.  Counts are order-independent integer sums: bit-identical to MN2.
+struct Mn1Ctx {
+    uint64_t M, Tm, c0, lo, hi;  // [lo, hi): this shard's slice of the CDF
+    uint32_t nb;
+    uint64_t W;                  // bin width: bin b = positions [lo + b W, lo + (b+1) W)
+    double invW;
+    SMC_DEV uint32_t bin(uint64_t P) const  // exact floor((P - lo) / W)
+    {
+        const uint64_t d = P - lo;
+        uint64_t b = (uint64_t)((double)d * invW);
+        while (b && b * W > d) --b;
+        while ((b + 1) * W <= d) ++b;
+        return (uint32_t)(b < nb ? b : nb - 1);
+    }
+};
+
+SMC_DEV Mn1Ctx mn1_ctx(const Layout &L, int64_t n)
+{
+    const RsHeader *h = L.hdr;
+    Mn1Ctx c;
+    c.M = h->M;
+    c.Tm = h->Tm;
+    c.c0 = h->c0;
+    c.lo = h->qoff;
+    c.hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
+    c.nb = (uint32_t)mn1_bins(n);
+    const uint64_t span = c.hi > c.lo ? c.hi - c.lo : 1;
+    c.W = span / c.nb + 1;  // nb W > span: every position has a bin
+    c.invW = 1.0 / (double)c.W;
+    return c;
+}
+
+SMC_DEV uint64_t mn1_position(const Mn1Ctx &c, uint64_t k, const Key &key, uint64_t stream, const double *u)
+{
+    const uint64_t m = u ? (uint64_t)(u[k] * TWO53) : draw53(c.c0 + k, stream, key);
+    return (uint64_t)(((u128)m * c.Tm) >> 53);
+}
+
+// atomicAdd(&a[key], 1) for a warp, one atomic when every active lane shares the key
+// (degenerate weights send every draw to one bin / one particle: without this the
+// same-address atomics serialize).  Returns the lane's slot (old value + rank).
+SMC_DEV uint32_t agg_inc(uint32_t *a, uint32_t key, bool active)
+{
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!act) return 0;
+    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+    const uint32_t k0 = __shfl_sync(0xffffffffu, key, leader);
+    if (__all_sync(0xffffffffu, !active || key == k0)) {  // the whole warp hits one counter
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&a[k0], (uint32_t)__popc(act));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        return base + __popc(act & ((1u << lane) - 1));
+    }
+    return active ? atomicAdd(&a[key], 1u) : 0;
+}
+
+__global__ void k_mn1_count(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+{
+    SMC_PDL_WAIT();
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    const Mn1Ctx c = mn1_ctx(L, n);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t kend = (c.M + stride - 1) / stride * stride;  // whole warps iterate together
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
+        const uint64_t P = k < c.M ? mn1_position(c, k, key, stream, u) : c.lo;
+        const bool in = k < c.M && P >= c.lo && P < c.hi;  // else: past the end, or on another shard
+        agg_inc(L.mn_cnt, in ? c.bin(P) : 0u, in);
+    }
+}
+
+// one block: exclusive bucket offsets; fill pointers back to zero
+__global__ void __launch_bounds__(SB) k_mn1_scan(int64_t nbins, int64_t cap, Layout L)
+{
+    SMC_PDL_WAIT();
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    __shared__ uint64_t sm64[SB / 32 + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = SB / 32;
+    const int64_t nt = nbins;
+    const int64_t C = (nt + NW - 1) / NW;
+    const int64_t w0 = warp * C < nt ? warp * C : nt, w1 = w0 + C < nt ? w0 + C : nt;
+    constexpr int KS = 8;  // warp-rows of bins in flight per round (one round trip per round)
+    uint64_t wsum = 0;
+    for (int64_t b0 = w0 + lane; b0 < w1; b0 += 32 * KS) {
+        uint32_t v[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) v[k] = b0 + 32 * k < w1 ? L.mn_cnt[b0 + 32 * k] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) wsum += v[k];
+    }
+    wsum = warp_sum(wsum);
+    if (lane == 0) sm64[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+        const uint64_t x = sm64[lane];
+        const uint64_t inc = warp_inclusive_sum(x);
+        sm64[lane] = inc - x;
+    }
+    __syncthreads();
+    uint64_t carry = sm64[warp];
+    for (int64_t c0 = w0; c0 < w1; c0 += 32 * KS) {
+        uint64_t vv[KS];
+#pragma unroll
+        for (int k = 0; k < KS; ++k) vv[k] = c0 + 32 * k + lane < w1 ? L.mn_cnt[c0 + 32 * k + lane] : 0;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) {
+            const int64_t b = c0 + 32 * k + lane;
+            const uint64_t inc = warp_inclusive_sum(vv[k]);
+            if (b < w1) {
+                L.mn_off[b] = (uint32_t)(carry + inc - vv[k]);
+                L.mn_fill[b] = 0;
+            }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    if (warp == NW - 1 && lane == 31) {
+        L.mn_off[nt] = (uint32_t)carry;  // total positions in this shard
+        L.hdr->mn_direct = carry > (uint64_t)cap;  // buckets hold `cap` positions
+    }
+}
+
+// first particle of every bin: mn_start[b] = first i with Q_i > lo + b W (b = 0..nb)
+__global__ void k_mn1_starts(int64_t n, Layout L)
+{
+    SMC_PDL_WAIT();
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial || h->mn_direct) return;
+    const Mn1Ctx c = mn1_ctx(L, n);
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= c.nb; b += gridDim.x * blockDim.x) {
+        const uint64_t X = c.lo + (uint64_t)b * c.W;
+        int64_t lo = 0, hi = n - 1;
+        if (X >= c.hi) lo = n - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(&L.qfull[mid]) > X) hi = mid; else lo = mid + 1;
+        }
+        L.mn_start[b] = (uint32_t)lo;
+    }
+}
+
+__global__ void k_mn1_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u, Layout L)
+{
+    SMC_PDL_WAIT();
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    if (h->mn_direct) return;  // more positions than bucket capacity (a shard): k_rs_multinomial
+    const Mn1Ctx c = mn1_ctx(L, n);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t kend = (c.M + stride - 1) / stride * stride;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < kend; k += stride) {
+        const uint64_t P = k < c.M ? mn1_position(c, k, key, stream, u) : c.lo;
+        const bool in = k < c.M && P >= c.lo && P < c.hi;
+        const uint32_t b = in ? c.bin(P) : 0u;
+        const uint32_t r = agg_inc(L.mn_fill, b, in);
+        if (in) L.mn_pos[__ldg(&L.mn_off[b]) + r] = P;
+    }
+}
+
+// per bucketed position: first i with Q_i > P (Q inclusive, materialized by k_rs_prefix),
+// searched only between its bin's first particles
+__global__ void k_mn1_assign(int64_t n, Layout L)
+{
+    SMC_PDL_WAIT();
+    const RsHeader *h = L.hdr;
+    if (!h->active || h->trivial) return;
+    if (h->mn_direct) return;
+    const Mn1Ctx c = mn1_ctx(L, n);
+    const uint32_t total = __ldg(&L.mn_off[mn1_bins(n)]);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t jend = (total + stride - 1) / stride * stride;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jend; j += stride) {
+        const bool in = j < total;
+        int64_t lo = 0;
+        if (in) {
+            const uint64_t P = L.mn_pos[j];
+            const uint32_t b = c.bin(P);
+            lo = __ldg(&L.mn_start[b]);
+            int64_t hi = __ldg(&L.mn_start[b + 1]);
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(&L.qfull[mid]) > P) hi = mid; else lo = mid + 1;
+            }
+        }
+        agg_inc(reinterpret_cast<uint32_t *>(L.cnt), (uint32_t)lo, in);
     }
 }
 
@@ -1789,6 +2017,21 @@ inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t s
     smc_launch(k_mn2_count, (unsigned)mn_geom(n).nb, MT, sc, s, n, L);
 }
 
+inline int grid_cap(int64_t blocks);
+inline void launch_mn(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L)
+{
+    if (mn2_fits(n)) {
+        launch_mn2(s, n, m, key, stream, u, L);
+        return;
+    }
+    const unsigned gm = grid_cap((m + RT - 1) / RT);
+    smc_launch(k_mn1_count, gm, RT, 0, s, n, key, stream, u, L);
+    smc_launch(k_mn1_scan, 1, SB, 0, s, mn1_bins(n), n, L);
+    smc_launch(k_mn1_starts, (unsigned)((mn1_bins(n) + 1 + RT - 1) / RT), RT, 0, s, n, L);
+    smc_launch(k_mn1_scatter, gm, RT, 0, s, n, key, stream, u, L);
+    smc_launch(k_mn1_assign, gm, RT, 0, s, n, L);
+}
+
 inline int grid_cap(int64_t blocks)
 {
     return (int)(blocks < 1 ? 1 : (blocks > 148 * 16 ? 148 * 16 : blocks));
@@ -1850,7 +2093,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        launch_mn2(s, n, m_out, key, stream_index, u, L);
+        launch_mn(s, n, m_out, key, stream_index, u, L);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
@@ -1983,7 +2226,7 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_total + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        launch_mn2(s, n, m_total, key, stream_index, u, L);
+        launch_mn(s, n, m_total, key, stream_index, u, L);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;

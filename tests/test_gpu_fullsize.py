@@ -213,3 +213,54 @@ def test_gmm_config3_first_iterations_match_oracle():
         assert np.all(np.abs(hist[f"accept.{k}"] - ref[:, col]) <= 2), (k, hist[f"accept.{k}"], ref[:, col])
     np.testing.assert_allclose(hist["path.integrand"], ref[:, 6], rtol=1e-6)
     assert abs(lz - ref[-1, 7]) <= 1e-6 * abs(ref[-1, 7])
+
+
+N_MN1 = 3 << 25  # past the shared-memory bin geometry (mn2_fits): the global-bucket multinomial path
+
+
+@pytest.mark.parametrize("scheme,draws", [("multinomial", "explicit"), ("residual", "explicit"),
+                                          ("multinomial", "stream")])
+def test_multinomial_past_shared_memory_bins_bit_exact(scheme, draws):
+    """Config 5 reaches 2^30 for every scheme: above ~2^26 a multinomial position bin no longer
+    fits one block's shared memory and the draws go through the global-memory bucket path --
+    counts bit-exact vs the oracle there too (skewed weights; explicit and stream-N uniforms)."""
+    from paper_1306_5583_b200 import RngStreamSet, resample
+    from paper_1306_5583_b200.resample import Resampler
+    n = N_MN1
+    g = torch.Generator("cuda").manual_seed(11)
+    lw = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    w = torch.exp(lw - lw.max())
+    w = (w / w.sum()).contiguous()
+    del lw
+    if draws == "explicit":
+        u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+        counts = resample(scheme, w, u=u).cpu().numpy()
+        ref, _ = O.resample_counts(scheme, w.cpu().numpy(), u=u.cpu().numpy())
+        del u
+    else:
+        ss = RngStreamSet(n + 1, 1306)
+        os_ = O.Streams(n + 1, 1306)
+        r = Resampler(n)
+        c = torch.empty(n, dtype=torch.int32, device="cuda")
+        r(scheme, weights=w, rng=ss, stream_index=n, counts=c)
+        r.check()
+        counts = c.cpu().numpy()
+        ref, _ = O.resample_counts(scheme, w.cpu().numpy(), streams=os_, stream=n)
+        assert ss.counters_host()[n] == int(os_.counters[n])
+        del r, c
+    del w
+    torch.cuda.empty_cache()
+    assert counts.sum() == n
+    bad = np.nonzero(counts != ref)[0]
+    assert bad.size == 0, f"{bad.size} counts differ, first at {bad[:5]}"
+
+
+def test_multinomial_past_shared_memory_bins_degenerate():
+    """All the weight on one particle at N = 3 2^25: every draw lands on it."""
+    from paper_1306_5583_b200 import resample
+    n = N_MN1
+    w = torch.zeros(n, dtype=torch.float64, device="cuda")
+    w[n // 3] = 1.0
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    counts = resample("multinomial", w, u=u).cpu().numpy()
+    assert counts[n // 3] == n and counts.sum() == n
