@@ -72,6 +72,11 @@ struct RsHeader {
     double mn_rb;       // multinomial: 2^kb / Tm (bin-boundary estimate, exact fix-up)
 };
 
+struct MnGeom {
+    int kb;
+    int64_t nb, cap;
+};
+
 struct Layout {
     RsHeader *hdr;
     SMC_DEV RsHeader *hdr_w() const { return hdr; }
@@ -90,6 +95,7 @@ struct Layout {
     uint64_t *mn_pos;   // multinomial: positions by bin, `cap` slots per bin
     uint32_t *mn_start; // multinomial: first particle reached by every bin's positions (B + 1)
     uint32_t *mn_cnt, *mn_off;  // MN1: draws per position bin, bin offsets in mn_pos
+    MnGeom mg;                  // MN2 bin geometry of this n (mn_geom, evaluated on the host)
     size_t bytes;
 };
 
@@ -101,10 +107,6 @@ inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 // positions per bin (at most 4096 bins), and a fixed capacity of cap slots per bin (the
 // draws' bins are Binomial(M, 2^-kb) whatever the weights: mean + 8 sd + 64; an overflow --
 // adversarial explicit uniforms -- falls back to the direct search).
-struct MnGeom {
-    int kb;
-    int64_t nb, cap;
-};
 __host__ __device__ inline MnGeom mn_geom(int64_t n)
 {
     MnGeom g;
@@ -168,6 +170,7 @@ Layout layout(void *ws, int64_t n)
     L.qfull = (uint64_t *)take(sizeof(uint64_t) * n);
     L.cnt = (int32_t *)take(sizeof(int32_t) * n);
     const MnGeom mg = mn_geom(n);
+    L.mg = mg;
     const bool mn2 = mn2_fits(n);
     const int64_t nb1 = mn2 ? 0 : mn1_bins(n), nbm = mg.nb > nb1 ? mg.nb : nb1;
     L.mn_fill = (uint32_t *)take(sizeof(uint32_t) * (nbm + 1));
@@ -500,11 +503,11 @@ __global__ void __launch_bounds__(SB) k_rs_scan(int scheme, int64_t n, int64_t n
         }
         h->active = ok;
         h->mn_direct = 0;
-        h->mn_rb = Tm ? ldexp(1.0, mn_geom(n).kb) / (double)Tm : 0.0;
+        h->mn_rb = Tm ? ldexp(1.0, L.mg.kb) / (double)Tm : 0.0;
         s_ok = ok;
     }
     if (is_multinomial(scheme)) {  // the multinomial bins: empty, every start at the last particle
-        const MnGeom g = mn_geom(n);
+        const MnGeom g = L.mg;  // host-computed (Layout)
         for (int64_t b = threadIdx.x; b <= g.nb; b += SB) {
             L.mn_fill[b] = 0;
             L.mn_start[b] = (uint32_t)(n - 1);
@@ -658,12 +661,12 @@ __global__ void __launch_bounds__(SB) k_rs_scan1(int scheme, int64_t n, int64_t 
             }
             h->active = ok;
             h->mn_direct = 0;
-            h->mn_rb = Tm ? ldexp(1.0, mn_geom(n).kb) / (double)Tm : 0.0;
+            h->mn_rb = Tm ? ldexp(1.0, L.mg.kb) / (double)Tm : 0.0;
             s_ok = ok;
         }
     }
     if (is_multinomial(scheme)) {  // the multinomial bins: empty, every start at the last particle
-        const MnGeom g = mn_geom(n);
+        const MnGeom g = L.mg;  // host-computed (Layout)
         for (int64_t b = threadIdx.x; b <= g.nb; b += SB) {
             L.mn_fill[b] = 0;
             L.mn_start[b] = (uint32_t)(n - 1);
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     // positions iff lo_b = floor(b Tm / 2^kb) lies in [Q_{i-1}, Q_i) -- found from the two
     // ends of each particle's interval (ceil bin boundaries are monotone: usually no bin)
     const RsHeader *h = L.hdr;
-    const MnGeom g = mn_geom(n);
+    const MnGeom g = L.mg;  // host-computed (Layout)
     auto ceil_bin = [&](uint64_t X) {  // min b with floor(b Tm / 2^kb) >= X
         int64_t b = (int64_t)ceil((double)X * h->mn_rb);
         b = b < 0 ? 0 : (b > g.nb ? g.nb : b);
@@ -776,7 +779,7 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
     if (!h->active || h->trivial) return;
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0, lo = h->qoff;
     const uint64_t hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
-    const MnGeom g = mn_geom(n);
+    const MnGeom g = L.mg;  // host-computed (Layout)
     const uint64_t k0 = (uint64_t)blockIdx.x * MCH;
     if (k0 >= M) return;
     extern __shared__ __align__(16) unsigned char mn_sm[];
@@ -862,12 +865,42 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
 {
     SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
-    if (!h->active || h->trivial || h->mn_direct) return;
-    const MnGeom g = mn_geom(n);
     const int64_t b = blockIdx.x;
-    const int64_t cnt = min((int64_t)__ldg(&L.mn_fill[b]), g.cap);
+    // the block's whole first round trip at once: header, fill, the bin's particle range, and
+    // (below) the first particle steps' Q -- none depends on another (indices clamped: an inactive
+    // call leaves the bin starts unwritten)
+    const int32_t active = h->active, trivial = h->trivial, direct = h->mn_direct;
+    const uint64_t Tm = h->Tm, qoff = h->qoff;
+    const uint32_t fill = __ldg(&L.mn_fill[b]);
+    const int64_t s = min((int64_t)__ldg(&L.mn_start[b]), n - 1);
+    int64_t e = min(max(s, (int64_t)__ldg(&L.mn_start[b + 1])), n - 1);
+    const int64_t e0 = e;
+    const uint64_t *Q = L.qfull;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // the bin's particles [s, e] in contiguous per-warp chunks of whole 32-particle steps: a
+    // particle's F(Q_{i-1}) is its left neighbour's F(Q_i) (shuffle; across steps, the carry)
+    constexpr int PU = 4;  // steps of a warp with their Q loads in flight together
+    int64_t c0, c1;
+    auto chunk = [&](int64_t last) {
+        const int64_t C = (((last - s + 1) + 32 * (MT / 32) - 1) / (32 * (MT / 32))) * 32;
+        c0 = min(s + warp * C, last + 1);
+        c1 = min(c0 + C, last + 1);
+    };
+    uint64_t q[PU], qfirst = 0;
+    auto load_q = [&](int64_t i00) {
+#pragma unroll
+        for (int k = 0; k < PU; ++k) {
+            const int64_t i = i00 + 32 * k + lane;
+            q[k] = i < c1 ? __ldg(&Q[i]) : 0;
+        }
+    };
+    chunk(e);
+    load_q(c0);
+    if (lane == 0 && c0 < c1) qfirst = c0 ? __ldg(&Q[c0 - 1]) : qoff;
+    if (!active || trivial || direct) return;
+    const MnGeom g = L.mg;  // host-computed (Layout)
+    const int64_t cnt = min((int64_t)fill, g.cap);
     if (cnt == 0) return;
-    const uint64_t Tm = h->Tm;
     const uint64_t lo_b = (uint64_t)(((u128)b * Tm) >> g.kb);
     const uint64_t mmax = ((uint64_t)(b + 1) << (53 - g.kb)) - 1;
     const uint64_t hi_b = (uint64_t)(((u128)mmax * Tm) >> 53);  // the bin's largest position
@@ -891,7 +924,7 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
     // up to KPT positions per thread stay in registers with their rank in their sub-bucket (the
     // counting atomic's return value): one read of the bin and no second atomic; larger bins
     // (N > 2^25: wider bins) read their positions twice
-    constexpr int KPT = 12;
+    constexpr int KPT = 8;
     const bool inreg = cnt <= (int64_t)MT * KPT;
     uint64_t Pr[KPT];
     uint32_t sbr[KPT];
@@ -917,18 +950,18 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
         constexpr int SPT = NSB / MT;
         uint32_t c8[SPT], sum = 0;
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) {
-            const int k = threadIdx.x * SPT + q;
-            c8[q] = k < nsb ? cur[k] : 0;
-            sum += c8[q];
+        for (int k8 = 0; k8 < SPT; ++k8) {
+            const int k = threadIdx.x * SPT + k8;
+            c8[k8] = k < nsb ? cur[k] : 0;
+            sum += c8[k8];
         }
         uint32_t tot;
         uint32_t ex = block_exclusive_sum<MT, uint32_t>(sum, s_w, &tot);
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) {
-            const int k = threadIdx.x * SPT + q;
+        for (int k8 = 0; k8 < SPT; ++k8) {
+            const int k = threadIdx.x * SPT + k8;
             if (k < nsb) { offs[k] = ex; cur[k] = ex; }
-            ex += c8[q];
+            ex += c8[k8];
         }
         if (threadIdx.x == 0) offs[nsb] = tot;
     }
@@ -946,10 +979,6 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
         }
     }
     __syncthreads();
-    const uint64_t *Q = L.qfull;
-    const uint64_t qoff = h->qoff;
-    const int64_t s = __ldg(&L.mn_start[b]);
-    int64_t e = max(s, (int64_t)__ldg(&L.mn_start[b + 1]));
     if (e == n - 1) {  // the start sentinel (the last bin, or zero-weight particles to the end):
         __shared__ int64_t s_e;  // the particle of the bin's largest position instead, by search
         if (threadIdx.x == 0) {
@@ -975,18 +1004,28 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
         for (uint32_t k = offs[sb]; k < offs[sb + 1]; ++k) c += (Ps[k] < X);
         return c;
     };
-    const int lane = threadIdx.x & 31;
-    for (int64_t i0 = s + (threadIdx.x & ~31); i0 <= e; i0 += MT) {  // a warp: 32 consecutive particles
-        const int64_t i = i0 + lane;
-        const uint32_t Fi = i <= e ? F(__ldg(&Q[i])) : 0;
-        uint32_t Fp = __shfl_up_sync(0xffffffffu, Fi, 1);
-        if (lane == 0) Fp = F(i ? __ldg(&Q[i - 1]) : qoff);
-        if (i > e) continue;
-        const uint32_t c = Fi - Fp;
-        if (i == s || i == e) {  // a neighbouring bin may reach it too
-            if (c) atomicAdd(&L.cnt[i], (int)c);
-        } else {
-            L.cnt[i] = (int32_t)c;  // only this bin reaches it
+    if (e != e0) {  // the sentinel search moved the end: re-chunk (the last bin only)
+        chunk(e);
+        load_q(c0);
+        if (lane == 0 && c0 < c1) qfirst = c0 ? __ldg(&Q[c0 - 1]) : qoff;
+    }
+    uint32_t carry = lane == 0 && c0 < c1 ? F(qfirst) : 0;  // F(Q_{c0-1}), lane 0's left neighbour
+    for (int64_t i00 = c0; i00 < c1; i00 += 32 * PU) {
+        if (i00 != c0) load_q(i00);  // the first steps' Q came with the header
+#pragma unroll
+        for (int k = 0; k < PU; ++k) {
+            const int64_t i = i00 + 32 * k + lane;
+            const uint32_t Fi = i < c1 ? F(q[k]) : 0;
+            uint32_t Fp = __shfl_up_sync(0xffffffffu, Fi, 1);
+            if (lane == 0) Fp = carry;
+            carry = __shfl_sync(0xffffffffu, Fi, 31);
+            if (i >= c1) continue;
+            const uint32_t c = Fi - Fp;
+            if (i == s || i == e) {  // a neighbouring bin may reach it too
+                if (c) atomicAdd(&L.cnt[i], (int)c);
+            } else {
+                L.cnt[i] = (int32_t)c;  // only this bin reaches it
+            }
         }
     }
 }
