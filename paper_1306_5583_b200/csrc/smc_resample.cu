@@ -124,13 +124,16 @@ __host__ __device__ inline MnGeom mn_geom(int64_t n)
 // k_mn2_count: a bin's `cap` positions + 2 x 8193 sub-bucket words).  Past N ~ 2^26 a bin no
 // longer fits one block's shared memory: those N take the global-memory bucket path (MN1).
 constexpr int MT = 1024;          // threads of the multinomial kernels
-constexpr int MDPT = 12;          // draws per thread in k_mn2_scatter
-constexpr int MCH = MT * MDPT;    // draws per scatter block
+// draws per thread in k_mn2_scatter: 6 while the block's shared memory (12 B per draw + 12 B per
+// bin) lets two blocks share an SM (<= 2048 bins, N <= 2^24), else 12 (same-box A/B,
+// profiles/r2_resample_ab.txt)
+__host__ __device__ inline int mn_dpt(int64_t nb) { return nb <= 2048 ? 6 : 12; }
 constexpr int NSB = 4096;         // most sub-buckets of a bin in k_mn2_count (~2 positions each)
 constexpr size_t MN_SMEM_MAX = 232448;  // 227 KB: the sm_100 per-block opt-in maximum
 __host__ __device__ inline size_t mn2_scatter_smem(int64_t n)
 {
-    return (size_t)MCH * (8 + 2 + 2) + (size_t)mn_geom(n).nb * 12 + 64;
+    const MnGeom g = mn_geom(n);
+    return (size_t)MT * mn_dpt(g.nb) * (8 + 2 + 2) + (size_t)g.nb * 12 + 64;
 }
 __host__ __device__ inline size_t mn2_count_smem(int64_t n)
 {
@@ -780,13 +783,14 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0, lo = h->qoff;
     const uint64_t hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
     const MnGeom g = L.mg;  // host-computed (Layout)
-    const uint64_t k0 = (uint64_t)blockIdx.x * MCH;
+    const int dpt = mn_dpt(g.nb), mch = MT * dpt;
+    const uint64_t k0 = (uint64_t)blockIdx.x * mch;
     if (k0 >= M) return;
     extern __shared__ __align__(16) unsigned char mn_sm[];
     uint64_t *P_s = reinterpret_cast<uint64_t *>(mn_sm);
-    uint16_t *bin_s = reinterpret_cast<uint16_t *>(P_s + MCH);
-    uint16_t *perm_s = bin_s + MCH;
-    uint32_t *hist = reinterpret_cast<uint32_t *>(perm_s + MCH);  // counts, then the sorting cursors
+    uint16_t *bin_s = reinterpret_cast<uint16_t *>(P_s + mch);
+    uint16_t *perm_s = bin_s + mch;
+    uint32_t *hist = reinterpret_cast<uint32_t *>(perm_s + mch);  // counts, then the sorting cursors
     uint32_t *base = hist + g.nb;                                  // reserved run start per bin
     uint32_t *lofs = base + g.nb;                                  // bin's offset in the block's sorted order
     __shared__ uint32_t s_w[MT / 32 + 1];
@@ -796,7 +800,7 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
     __syncthreads();
     const int sh = 53 - g.kb;
 #pragma unroll 4
-    for (int d = 0; d < MDPT; ++d) {
+    for (int d = 0; d < dpt; ++d) {
         const int idx = d * MT + threadIdx.x;
         const uint64_t k = k0 + idx;
         uint16_t bb = 0xFFFF;  // not in this shard's slice / past the last draw
@@ -841,7 +845,7 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
         if (threadIdx.x == 0) L.hdr_w()->mn_direct = 1;
         return;
     }
-    for (int d = 0; d < MDPT; ++d) {  // counting sort in shared memory: the block's draws by bin
+    for (int d = 0; d < dpt; ++d) {  // counting sort in shared memory: the block's draws by bin
         const int idx = d * MT + threadIdx.x;
         const uint16_t bb = bin_s[idx];
         if (bb != 0xFFFF) perm_s[lofs[bb] + atomicAdd(&hist[bb], 1u)] = (uint16_t)idx;
@@ -861,7 +865,10 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
 // and per position, no search.  Interior particles are reached by this bin only (plain
 // coalesced stores); the two end particles may be shared with a neighbour (atomics).
 
-__global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
+// MTC threads: 512 (two blocks per SM) while a bin's shared memory allows it (N <= 2^25), else
+// 1024 (same-box A/B, profiles/r2_resample_ab.txt)
+template <int MTC>
+__global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout L)
 {
     SMC_PDL_WAIT();
     const RsHeader *h = L.hdr;
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
     constexpr int PU = 4;  // steps of a warp with their Q loads in flight together
     int64_t c0, c1;
     auto chunk = [&](int64_t last) {
-        const int64_t C = (((last - s + 1) + 32 * (MT / 32) - 1) / (32 * (MT / 32))) * 32;
+        const int64_t C = (((last - s + 1) + 32 * (MTC / 32) - 1) / (32 * (MTC / 32))) * 32;
         c0 = min(s + warp * C, last + 1);
         c1 = min(c0 + C, last + 1);
     };
@@ -917,37 +924,37 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
     uint64_t *Ps = reinterpret_cast<uint64_t *>(c_sm);                 // positions sorted by sub-bucket
     uint32_t *offs = reinterpret_cast<uint32_t *>(Ps + g.cap);         // sub-bucket starts (nsb + 1)
     uint32_t *cur = offs + NSB + 1;                                    // counts, then cursors
-    __shared__ uint32_t s_w[MT / 32 + 1];
-    for (int k = threadIdx.x; k <= nsb; k += MT) cur[k] = 0;
+    __shared__ uint32_t s_w[MTC / 32 + 1];
+    for (int k = threadIdx.x; k <= nsb; k += MTC) cur[k] = 0;
     __syncthreads();
     const uint64_t *pos = L.mn_pos + b * g.cap;
     // up to KPT positions per thread stay in registers with their rank in their sub-bucket (the
     // counting atomic's return value): one read of the bin and no second atomic; larger bins
     // (N > 2^25: wider bins) read their positions twice
     constexpr int KPT = 8;
-    const bool inreg = cnt <= (int64_t)MT * KPT;
+    const bool inreg = cnt <= (int64_t)MTC * KPT;
     uint64_t Pr[KPT];
     uint32_t sbr[KPT];
     if (inreg) {
 #pragma unroll
         for (int k = 0; k < KPT; ++k) {
-            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            const int64_t j = threadIdx.x + (int64_t)k * MTC;
             Pr[k] = j < cnt ? pos[j] : 0;
         }
 #pragma unroll
         for (int k = 0; k < KPT; ++k) {
-            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            const int64_t j = threadIdx.x + (int64_t)k * MTC;
             if (j < cnt) {
                 const uint32_t sb = (uint32_t)((Pr[k] - lo_b) >> sh2);
-                sbr[k] = (sb << 16) | atomicAdd(&cur[sb], 1u);  // rank < 2^16: cnt <= MT * KPT
+                sbr[k] = (sb << 16) | atomicAdd(&cur[sb], 1u);  // rank < 2^16: cnt <= MTC * KPT
             }
         }
     } else {
-        for (int64_t j = threadIdx.x; j < cnt; j += MT) atomicAdd(&cur[(pos[j] - lo_b) >> sh2], 1u);
+        for (int64_t j = threadIdx.x; j < cnt; j += MTC) atomicAdd(&cur[(pos[j] - lo_b) >> sh2], 1u);
     }
     __syncthreads();
     {  // exclusive scan of the nsb <= NSB sub-bucket counts, 4 per thread
-        constexpr int SPT = NSB / MT;
+        constexpr int SPT = NSB / MTC;
         uint32_t c8[SPT], sum = 0;
 #pragma unroll
         for (int k8 = 0; k8 < SPT; ++k8) {
@@ -956,7 +963,7 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
             sum += c8[k8];
         }
         uint32_t tot;
-        uint32_t ex = block_exclusive_sum<MT, uint32_t>(sum, s_w, &tot);
+        uint32_t ex = block_exclusive_sum<MTC, uint32_t>(sum, s_w, &tot);
 #pragma unroll
         for (int k8 = 0; k8 < SPT; ++k8) {
             const int k = threadIdx.x * SPT + k8;
@@ -969,11 +976,11 @@ __global__ void __launch_bounds__(MT) k_mn2_count(int64_t n, Layout L)
     if (inreg) {
 #pragma unroll
         for (int k = 0; k < KPT; ++k) {
-            const int64_t j = threadIdx.x + (int64_t)k * MT;
+            const int64_t j = threadIdx.x + (int64_t)k * MTC;
             if (j < cnt) Ps[offs[sbr[k] >> 16] + (sbr[k] & 0xFFFFu)] = Pr[k];
         }
     } else {
-        for (int64_t j = threadIdx.x; j < cnt; j += MT) {  // the bin's positions again (L2-hot): placed
+        for (int64_t j = threadIdx.x; j < cnt; j += MTC) {  // the bin's positions again (L2-hot): placed
             const uint64_t P = pos[j];
             Ps[atomicAdd(&cur[(P - lo_b) >> sh2], 1u)] = P;
         }
@@ -2046,14 +2053,24 @@ inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t s
         cudaFuncSetAttribute(k_mn2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         s_set = sm;
     }
-    smc_launch(k_mn2_scatter, (unsigned)((m + MCH - 1) / MCH), MT, sm, s, n, key, stream, u, L);
+    const int64_t mch = (int64_t)MT * mn_dpt(mn_geom(n).nb);
+    smc_launch(k_mn2_scatter, (unsigned)((m + mch - 1) / mch), MT, sm, s, n, key, stream, u, L);
     const size_t sc = mn2_count_smem(n);
     static size_t c_set = 0;
     if (sc > c_set) {
-        cudaFuncSetAttribute(k_mn2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+        cudaFuncSetAttribute(k_mn2_count<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
         c_set = sc;
     }
-    smc_launch(k_mn2_count, (unsigned)mn_geom(n).nb, MT, sc, s, n, L);
+    if (2 * (sc + 1024) <= 233472) {  // two blocks per SM (228 KB, 1 KB reserved per block)
+        static size_t c2_set = 0;
+        if (sc > c2_set) {
+            cudaFuncSetAttribute(k_mn2_count<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+            c2_set = sc;
+        }
+        smc_launch(k_mn2_count<512>, (unsigned)mn_geom(n).nb, 512, sc, s, n, L);
+    } else {
+        smc_launch(k_mn2_count<1024>, (unsigned)mn_geom(n).nb, 1024, sc, s, n, L);
+    }
 }
 
 inline int grid_cap(int64_t blocks);
