@@ -54,6 +54,10 @@ int smc_last_error(char *buf, size_t len);
  * NVRTC user kernels included).  No reference counterpart: instrumentation for the bench's
  * `gpu_launches` (how many of the library's kernels ran in a timed region). */
 int smc_launch_count(uint64_t *out);
+/* Checked builds (-DSMC_CHECKED=1) count violated index guards in the kernels instead of
+ * trapping; this returns their number and the first failing source line (1 = a checked
+ * build, 0 = a production build, whose count is always 0).  Test infrastructure. */
+int smc_check_failures(uint64_t *fails, uint64_t *first_line, char *file, size_t file_len);
 
 /* ------------------------------------------------------------------------ */
 /* RNG -- replaces pkg/src/smckit/rng.py                                     */

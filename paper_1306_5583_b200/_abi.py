@@ -68,6 +68,7 @@ _SIGS = {
     "smc_abi_version": ([], C.c_int),
     "smc_last_error": ([C.c_char_p, _sz], C.c_int),
     "smc_launch_count": ([_vp], C.c_int),
+    "smc_check_failures": ([_vp, _vp, C.c_char_p, _sz], C.c_int),
     "smc_philox_blocks": ([_vp, _i64, _u64, _vp, _vp], C.c_int),
     "smc_rng_fill": ([_i32, _u64, _u64, _vp, _f64, _f64, _f64, _vp, _i64, _vp], C.c_int),
     "smc_rng_draw_streams": ([_i32, _u64, _u64, _i64, _vp, _f64, _f64, _f64, _vp, _vp], C.c_int),
@@ -148,6 +149,15 @@ def launch_count():
     return int(v.value)
 
 
+def check_failures():
+    """(checked_build, violated index guards, 'file:line' of the first) -- smc_check_failures."""
+    f, ln = C.c_uint64(0), C.c_uint64(0)
+    buf = C.create_string_buffer(256)
+    checked = lib().smc_check_failures(C.byref(f), C.byref(ln), buf, 256)
+    where = f"{buf.value.decode(errors='replace')}:{ln.value}" if f.value else ""
+    return bool(checked), int(f.value), where
+
+
 def last_error():
     buf = C.create_string_buffer(512)
     lib().smc_last_error(buf, 512)
@@ -194,4 +204,6 @@ class Workspace:
         nbytes = max(int(nbytes), 256)
         if self.buf is None or self.buf.numel() < nbytes:
             self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            if os.environ.get("SMC_CHECKED_RUN"):  # checked runs: no reliance on zeroed scratch
+                self.buf.fill_(0xA5)
         return C.c_void_p(self.buf.data_ptr()), C.c_size_t(self.buf.numel())

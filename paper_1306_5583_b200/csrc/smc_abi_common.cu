@@ -33,6 +33,25 @@ extern "C" int smc_last_error(char *buf, size_t len)
     return SMC_OK;
 }
 
+extern "C" int smc_check_failures(uint64_t *fails, uint64_t *first_line, char *file, size_t file_len)
+{
+    if (!fails || !first_line) return smc_set_error(SMC_EINVAL, "smc_check_failures: null");
+    *fails = 0;
+    *first_line = 0;
+    const char *f = "";
+    for (smc_chk_reader r : smc_chk_readers()) r(fails, first_line, &f);
+    if (file && file_len) {
+        size_t k = 0;
+        for (; f[k] && k + 1 < file_len; ++k) file[k] = f[k];
+        file[k] = 0;
+    }
+#if SMC_CHECKED
+    return 1;  // a checked build
+#else
+    return 0;
+#endif
+}
+
 extern "C" int smc_launch_count(uint64_t *out)
 {
     if (!out) return SMC_EINVAL;

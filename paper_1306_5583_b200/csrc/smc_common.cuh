@@ -38,6 +38,46 @@ inline std::atomic<unsigned long long> &smc_launch_counter()
 }
 #define SMC_COUNT_LAUNCH() smc_launch_counter().fetch_add(1, std::memory_order_relaxed)
 
+// Checked build (-DSMC_CHECKED=1; tools/gpu/checked.sh): SMC_CHECK(cond) guards the shared- and
+// global-memory indices the kernels compute (staging slices, rank tables, bins, sub-buckets,
+// parent indices).  A violated check is counted, never trapped (the GPU stays healthy and the
+// test that caused it keeps running): every translation unit keeps its own device counters and
+// registers a reader, and smc_check_failures() (ABI) sums them and names the first failing line.
+// The stand-in for compute-sanitizer's memcheck on a pool where the sanitizer is closed.
+#if SMC_CHECKED
+static __device__ unsigned long long smc_chk_fail_d, smc_chk_line_d;
+#define SMC_CHECK(c)                                                                   \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            atomicAdd(&smc_chk_fail_d, 1ull);                                          \
+            atomicCAS(&smc_chk_line_d, 0ull, (unsigned long long)__LINE__);            \
+        }                                                                              \
+    } while (0)
+#else
+#define SMC_CHECK(c) do { } while (0)
+#endif
+typedef void (*smc_chk_reader)(uint64_t *fails, uint64_t *line, const char **file);
+#include <vector>
+inline std::vector<smc_chk_reader> &smc_chk_readers()
+{
+    static std::vector<smc_chk_reader> v;
+    return v;
+}
+#if SMC_CHECKED
+static void smc_chk_read_tu(uint64_t *fails, uint64_t *line, const char **file)
+{
+    unsigned long long f = 0, l = 0;
+    cudaMemcpyFromSymbol(&f, smc_chk_fail_d, sizeof f);
+    cudaMemcpyFromSymbol(&l, smc_chk_line_d, sizeof l);
+    *fails += f;
+    if (l && !*line) {
+        *line = l;
+        *file = __BASE_FILE__;
+    }
+}
+static const bool smc_chk_registered = (smc_chk_readers().push_back(&smc_chk_read_tu), true);
+#endif
+
 template <typename... KArgs, typename... Args>
 inline void smc_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args)
 {

@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         if (i < n) {
             const double prev = nl(lw_prev);  // normalized W_{t-1}; no read if equal
             double x0, x1, x2, x3;
+            SMC_CHECK(src >= 0 && src < n);
             ld_row(x_in + 4 * src, x0, x1, x2, x3);
             const uint64_t si = sbase + (uint64_t)i;
             // PAPER.md:1310-1313, evaluation order pinned: x0 += (0 + sd*z) + delta*x2

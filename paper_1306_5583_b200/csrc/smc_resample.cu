@@ -732,6 +732,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
     }
     if (i0 == 0 && h->qoff > 0) {  // the bin straddling this shard's start reaches particle 0 first
         const int64_t bq = ceil_bin(h->qoff) - 1;
+        SMC_CHECK(bq < L.mg.nb + 2);
         if (bq >= 0) L.mn_start[bq] = 0;
     }
     if (i0 < n) {
@@ -744,6 +745,7 @@ __global__ void __launch_bounds__(RT) k_rs_prefix(int scheme, WSrc src, int64_t 
             for (int j = 0; j < RI; ++j) {
                 if (v[j] > qprev && i0 + j < n) {
                     const int64_t bj = ceil_bin(v[j]);
+                    SMC_CHECK(bj <= L.mg.nb + 1);
                     for (int64_t b = bprev; b < bj; ++b) L.mn_start[b] = (uint32_t)(i0 + j);
                     bprev = bj;
                 }
@@ -810,6 +812,7 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
             P = (uint64_t)(((u128)m * Tm) >> 53);
             if (P >= lo && P < hi) {
                 bb = (uint16_t)(m >> sh);
+                SMC_CHECK(bb < g.nb);
                 atomicAdd(&hist[bb], 1u);
             }
         }
@@ -848,12 +851,14 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
     for (int d = 0; d < dpt; ++d) {  // counting sort in shared memory: the block's draws by bin
         const int idx = d * MT + threadIdx.x;
         const uint16_t bb = bin_s[idx];
+        SMC_CHECK(bb == 0xFFFF || (bb < g.nb && lofs[bb] + hist[bb] < (uint32_t)mch));
         if (bb != 0xFFFF) perm_s[lofs[bb] + atomicAdd(&hist[bb], 1u)] = (uint16_t)idx;
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tot; j += MT) {  // consecutive j: consecutive slots of a bin's run
         const int idx = perm_s[j];
         const uint32_t bb = bin_s[idx];
+        SMC_CHECK(bb < g.nb && base[bb] + (j - lofs[bb]) < (uint64_t)g.cap);
         L.mn_pos[(int64_t)bb * g.cap + base[bb] + (j - lofs[bb])] = P_s[idx];
     }
 }
@@ -946,6 +951,7 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
             const int64_t j = threadIdx.x + (int64_t)k * MTC;
             if (j < cnt) {
                 const uint32_t sb = (uint32_t)((Pr[k] - lo_b) >> sh2);
+                SMC_CHECK(sb < (uint32_t)nsb);
                 sbr[k] = (sb << 16) | atomicAdd(&cur[sb], 1u);  // rank < 2^16: cnt <= MTC * KPT
             }
         }
@@ -977,6 +983,7 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
 #pragma unroll
         for (int k = 0; k < KPT; ++k) {
             const int64_t j = threadIdx.x + (int64_t)k * MTC;
+            SMC_CHECK(j >= cnt || offs[sbr[k] >> 16] + (sbr[k] & 0xFFFFu) < (uint64_t)g.cap);
             if (j < cnt) Ps[offs[sbr[k] >> 16] + (sbr[k] & 0xFFFFu)] = Pr[k];
         }
     } else {
@@ -1028,6 +1035,7 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
             carry = __shfl_sync(0xffffffffu, Fi, 31);
             if (i >= c1) continue;
             const uint32_t c = Fi - Fp;
+            SMC_CHECK(i >= 0 && i < n);
             if (i == s || i == e) {  // a neighbouring bin may reach it too
                 if (c) atomicAdd(&L.cnt[i], (int)c);
             } else {
@@ -1197,6 +1205,7 @@ __global__ void k_mn1_scatter(int64_t n, Key key, uint64_t stream, const double 
         const bool in = k < c.M && P >= c.lo && P < c.hi;
         const uint32_t b = in ? c.bin(P) : 0u;
         const uint32_t r = agg_inc(L.mn_fill, b, in);
+        SMC_CHECK(!in || (b < c.nb && __ldg(&L.mn_off[b]) + r < (uint64_t)n));
         if (in) L.mn_pos[__ldg(&L.mn_off[b]) + r] = P;
     }
 }
@@ -1219,6 +1228,7 @@ __global__ void k_mn1_assign(int64_t n, Layout L)
         if (in) {
             const uint64_t P = L.mn_pos[j];
             const uint32_t b = c.bin(P);
+            SMC_CHECK(b < c.nb);
             lo = __ldg(&L.mn_start[b]);
             int64_t hi = __ldg(&L.mn_start[b + 1]);
             while (lo < hi) {
@@ -1491,6 +1501,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
 #pragma unroll
     for (int j = 0; j < RI; ++j) {
         if (c[j] >= 2) {  // padding slots load as 1
+            SMC_CHECK(c[j] < 2 || lp < (uint32_t)TILE);
             s_stage[lp] = base + j;
             s_stage[TILE + lp] = (int32_t)sr;
             ++lp;
@@ -1500,6 +1511,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
     __syncthreads();
     const uint32_t np = unp(agg);
     for (uint32_t k = threadIdx.x; k < np; k += RT) {
+        SMC_CHECK(ex.z + k <= (uint64_t)n);
         L.sp_idx[ex.z + k] = s_stage[k];
         L.sp_start[ex.z + k] = s_stage[TILE + k];
     }
@@ -1518,6 +1530,7 @@ __global__ void __launch_bounds__(RT) k_rs_ranks(const int32_t *__restrict__ cin
             const uint32_t mid = (lo + hi) >> 1;
             if ((uint32_t)s_stage[TILE + mid] <= r) lo = mid; else hi = mid;
         }
+        SMC_CHECK(a < (uint32_t)(n / ANCHOR + 2) && lo < np);
         L.anchor[a] = (int32_t)(ex.z + lo);
     }
 }
@@ -1846,6 +1859,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
                                              : owner(hi_s - 1);
         cnt = a1 - a0 + 1;
         for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
+            SMC_CHECK(k + 1 < (uint32_t)CSTAGE && a0 + k <= (uint64_t)n);
             s_start[k] = __ldcg(&L.sp_start[a0 + k]);
             s_idx[k] = __ldcg(&L.sp_idx[a0 + k]);
         }
@@ -1867,10 +1881,12 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
         for (uint32_t k = threadIdx.x; k < cnt; k += RT) {
             const uint32_t r0 = max((uint32_t)s_start[k], zlo), r1 = min((uint32_t)s_start[k + 1], zhi);
             if (r1 > r0 + 32) {
+                SMC_CHECK(s_nlong < TILE / 32 + 1);
                 s_long[atomicAdd(&s_nlong, 1u)] = k;  // at most TILE / 32 such runs in a tile
                 continue;
             }
             const int32_t pk = s_idx[k];
+            SMC_CHECK(r1 <= r0 || (r1 <= zlo + TILE && pk >= 0 && pk < n));
             for (uint32_t r = r0; r < r1; ++r) s_par[r - zlo] = pk;
         }
         __syncthreads();
@@ -1878,6 +1894,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
             const uint32_t k = s_long[l];
             const uint32_t r0 = max((uint32_t)s_start[k], zlo), r1 = min((uint32_t)s_start[k + 1], zhi);
             const int32_t pk = s_idx[k];
+            SMC_CHECK(r1 <= zlo + TILE && pk >= 0 && pk < n);
             for (uint32_t r = r0 + threadIdx.x; r < r1; r += RT) s_par[r - zlo] = pk;
         }
         __syncthreads();
@@ -1886,6 +1903,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
 #pragma unroll
         for (int j = 0; j < RI; ++j) {
             par[j] = b32 + j;  // survivors keep their slot
+            SMC_CHECK(!zero(j) || g < (uint32_t)TILE);
             if (zero(j)) par[j] = s_par[g++];
         }
         if (COPY32) {  // 4 row loads in flight per thread, then their stores
@@ -1919,6 +1937,7 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
                 if (g >= soff && g < soff + s_self) {
                     const int64_t s = g - soff;
                     while (lo + 1 < cnt && (int64_t)s_start[lo + 1] <= s) ++lo;
+                    SMC_CHECK(lo < cnt);
                     par[j] = s_idx[lo];
                 } else if (sc.zsp_all) {  // surplus child on another shard: read from its memory (P2P)
                     int h = 0;

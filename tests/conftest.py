@@ -37,3 +37,18 @@ def golden():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "rng_golden.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_guards(request):
+    """SMC_CHECKED_RUN=1 with a checked library (SMC_LIB_PATH, built with -DSMC_CHECKED=1;
+    tools/gpu/checked.sh): after every GPU test, no kernel index guard may have fired."""
+    yield
+    if not os.environ.get("SMC_CHECKED_RUN") or "gpu" not in request.keywords or not HAS_CUDA:
+        return
+    import torch
+    from paper_1306_5583_b200 import _abi
+    torch.cuda.synchronize()
+    checked, fails, where = _abi.check_failures()
+    assert checked, "SMC_CHECKED_RUN set but the library is not a checked build"
+    assert fails == 0, f"{fails} kernel index guard(s) fired, first at {where}"
