@@ -638,22 +638,41 @@ def run_e2e(P, s, obs, steps):
     torch.cuda.synchronize()
     hist = s._hist
     stream = torch.cuda.current_stream()
+    # the copies run on their own stream, ordered against the steps by events: step t's
+    # observation is uploaded while step t-1 computes, and record t-1 is read back while step
+    # t+1 computes -- the per-step transfers stay inside the timed region, off the step chain
+    copy = torch.cuda.Stream()
     done = [None] * (steps + 1)
+    h2d = [None] * (steps + 1)
     t0 = time.perf_counter()
+    t1 = s.iteration + 1
+    with torch.cuda.stream(copy):
+        dev_obs[t1].copy_(host_obs[t1], non_blocking=True)  # H2D: step 1's observation (16 B)
+        h2d[0] = torch.cuda.Event()
+        h2d[0].record(copy)
     for k in range(steps):
         t = s.iteration + 1
-        dev_obs[t].copy_(host_obs[t], non_blocking=True)  # H2D: this step's observation (16 B)
+        stream.wait_event(h2d[k])
         s.iterate(1, check=False)
-        # D2H: the newest COMPLETE history record.  The "pos" monitor of step t is
-        # reduced by step t+1's move (fused), so each step reads record t-1; the
-        # last record is flushed and read after the loop, inside the timed region.
-        host_rows[k].copy_(s._hist[t - 1], non_blocking=True)
-        done[k] = torch.cuda.Event()
-        done[k].record(stream)
+        stepped = torch.cuda.Event()
+        stepped.record(stream)
+        with torch.cuda.stream(copy):
+            if k + 1 < steps:  # H2D: the next step's observation (16 B), while this step computes
+                dev_obs[t + 1].copy_(host_obs[t + 1], non_blocking=True)
+                h2d[k + 1] = torch.cuda.Event()
+                h2d[k + 1].record(copy)
+            # D2H: the newest COMPLETE history record.  The "pos" monitor of step t is
+            # reduced by step t+1's move (fused), so each step reads record t-1; the
+            # last record is flushed and read after the loop, inside the timed region.
+            copy.wait_event(stepped)
+            host_rows[k].copy_(s._hist[t - 1], non_blocking=True)
+            done[k] = torch.cuda.Event()
+            done[k].record(copy)
         if k:  # streaming consumer: step k-1's record is in host memory before step k+1 is issued
             done[k - 1].synchronize()
     host_rows[steps].copy_(s.history_row(s.iteration), non_blocking=True)
     stream.synchronize()
+    copy.synchronize()
     sec = time.perf_counter() - t0
     del hist
     s.check()
