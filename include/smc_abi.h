@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SMC_ABI_VERSION 2
+#define SMC_ABI_VERSION 3
 
 #define SMC_OK 0
 #define SMC_EINVAL -1         /* invalid argument                                   */
@@ -103,6 +103,9 @@ typedef struct smc_wstate {
     int32_t status;    /* sticky device error (SMC_E*), 0 when healthy          */
     int32_t resample;  /* decision of the last smc_ess_decide     */
     int32_t err_index; /* first failing particle of `status`, as INT32_MAX - i  */
+    uint32_t lse_ticket; /* blocks of the running lse reduction that finished (the   */
+    uint32_t reserved;   /* last one combines); 0 between calls -- create the record  */
+                         /* zeroed                                                    */
 } smc_wstate;
 
 /* Every `int32_t *status` argument of this ABI points at an smc_status record (the

@@ -56,6 +56,7 @@ class SmcWState(C.Structure):
         ("log_zconst", C.c_double), ("max_raw", C.c_double), ("log_sum", C.c_double), ("w_equal", C.c_double),
         ("equal", C.c_int32), ("status", C.c_int32),
         ("resample", C.c_int32), ("err_index", C.c_int32),
+        ("lse_ticket", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 

@@ -54,14 +54,28 @@ constexpr int FG = 148;   // level-1 finalize blocks (one per SM)
 // Each level is two-phase so every exp is independent: M = max m_b, then
 // s1 = sum s1_b e^{m_b - M}, s2 = sum s2_b e^{2(m_b - M)}.  Optional monitor
 // partials (mon_parts[b] = sum_i W_i h(X_i) over block b) ride along.
-SMC_DEV void lse_slice(const LsePartial *__restrict__ parts, const double2 *__restrict__ mon, int b0, int b1,
-                       LsePartial *out, double2 *out_mon)
+// CG: the partials were written by other blocks of the SAME grid (the last-block combine):
+// loaded through L2 (ld.global.cg), never the non-coherent path.
+template <bool CG>
+SMC_DEV LsePartial ld_part(const LsePartial *p)
+{
+    if (CG) return LsePartial{__ldcg(&p->m), __ldcg(&p->s1), __ldcg(&p->s2)};
+    return *p;
+}
+template <bool CG>
+SMC_DEV double2 ld_mon(const double2 *p)
+{
+    if (CG) return __ldcg(p);
+    return *p;
+}
+template <bool CG = false>
+SMC_DEV void lse_slice(const LsePartial *parts, const double2 *mon, int b0, int b1, LsePartial *out, double2 *out_mon)
 {
     __shared__ double sm_a[FB / 32], sm_b[FB / 32], sm_c[FB / 32], sm_d[FB / 32];
     __shared__ double s_M;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double m = -INFINITY;
-    for (int b = b0 + threadIdx.x; b < b1; b += FB) m = fmax(m, parts[b].m);
+    for (int b = b0 + threadIdx.x; b < b1; b += FB) m = fmax(m, ld_part<CG>(parts + b).m);
     m = warp_max(m);
     if (lane == 0) sm_a[warp] = m;
     __syncthreads();
@@ -74,13 +88,17 @@ SMC_DEV void lse_slice(const LsePartial *__restrict__ parts, const double2 *__re
     const double M = s_M;
     double s1 = 0.0, s2 = 0.0, h0 = 0.0, h1 = 0.0;
     for (int b = b0 + threadIdx.x; b < b1; b += FB) {
-        const LsePartial p = parts[b];
+        const LsePartial p = ld_part<CG>(parts + b);
         if (p.m != -INFINITY) {
             const double f = exp(p.m - M);
             s1 += p.s1 * f;
             s2 += p.s2 * (f * f);
         }
-        if (mon) { h0 += mon[b].x; h1 += mon[b].y; }
+        if (mon) {
+            const double2 hm = ld_mon<CG>(mon + b);
+            h0 += hm.x;
+            h1 += hm.y;
+        }
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
@@ -96,15 +114,6 @@ SMC_DEV void lse_slice(const LsePartial *__restrict__ parts, const double2 *__re
         *out = t;
         *out_mon = make_double2(H0, H1);
     }
-}
-
-__global__ void __launch_bounds__(FB) k_lse_level1(const LsePartial *__restrict__ parts, int nparts,
-                                                    const double2 *__restrict__ mon, LsePartial *l2, double2 *l2mon)
-{
-    SMC_PDL_WAIT();
-    const int per = (nparts + FG - 1) / FG;
-    const int b0 = min(nparts, (int)blockIdx.x * per), b1 = min(nparts, b0 + per);
-    lse_slice(parts, mon, b0, b1, l2 + blockIdx.x, l2mon + blockIdx.x);
 }
 
 // The state update shared by the single-GPU finalize and the multi-GPU combine.
@@ -133,18 +142,35 @@ SMC_DEV void apply_lse(smc_wstate *st, LsePartial t, int64_t n, int mode, int ac
     }
 }
 
-// partial_out != NULL (a shard of a multi-GPU system): export {max, sum e,
-// sum e^2, monitor0, monitor1} instead of updating the state; the ranks then
-// allgather and smc_weights_combine them in rank order.
-__global__ void __launch_bounds__(FB) k_lse_finalize(const LsePartial *__restrict__ l2, const double2 *__restrict__ l2mon,
-                                                      int has_mon, smc_wstate *st, int64_t n, int mode,
-                                                      int accumulate_nc, double *mon_out, double *partial_out)
+// One launch for both levels: FG blocks each combine a slice of the block partials; the last
+// block to finish (a ticket in the weight record, reset by that block) combines the FG results
+// in index order -- the same arithmetic as two launches, one launch gap less per weight update.
+// partial_out != NULL (a shard of a multi-GPU system): export {max, sum e, sum e^2, monitor0,
+// monitor1} instead of updating the state; the ranks then allgather and smc_weights_combine them
+// in rank order.
+__global__ void __launch_bounds__(FB) k_lse_reduce(const LsePartial *__restrict__ parts, int nparts,
+                                                   const double2 *__restrict__ mon, LsePartial *l2, double2 *l2mon,
+                                                   smc_wstate *st, int64_t n, int mode, int accumulate_nc,
+                                                   double *mon_out, double *partial_out)
 {
     SMC_PDL_WAIT();
+    const int per = (nparts + FG - 1) / FG;
+    const int b0 = min(nparts, (int)blockIdx.x * per), b1 = min(nparts, b0 + per);
+    lse_slice(parts, mon, b0, b1, l2 + blockIdx.x, l2mon + blockIdx.x);
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {  // this block's l2 entry (written by thread 0 above) before its ticket
+        __threadfence();
+        s_last = atomicAdd(&st->lse_ticket, 1u) == (unsigned)FG - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     __shared__ LsePartial s_t;
     __shared__ double2 s_h;
-    lse_slice(l2, has_mon ? l2mon : nullptr, 0, FG, &s_t, &s_h);
+    const bool has_mon = mon != nullptr;
+    lse_slice<true>(l2, has_mon ? l2mon : nullptr, 0, FG, &s_t, &s_h);
     if (threadIdx.x == 0) {
+        st->lse_ticket = 0;
         const LsePartial t = s_t;
         if (partial_out) {
             partial_out[0] = t.m;
@@ -283,9 +309,8 @@ void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st
 {
     LsePartial *l2 = (LsePartial *)scratch;
     double2 *l2mon = (double2 *)(l2 + FG);
-    smc_launch(k_lse_level1, FG, FB, 0, s, parts, nparts, mon_parts, l2, l2mon);
-    smc_launch(k_lse_finalize, 1, FB, 0, s, l2, l2mon, mon_parts != nullptr, st, n, mode, accumulate_nc, mon_out,
-                                    partial_out);
+    smc_launch(k_lse_reduce, FG, FB, 0, s, parts, nparts, mon_parts, l2, l2mon, st, n, mode, accumulate_nc, mon_out,
+               partial_out);
 }
 
 extern "C" int smc_weights_combine(const double *partials, int G, smc_wstate *st, int64_t n_total, int mode,

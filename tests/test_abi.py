@@ -34,7 +34,7 @@ def test_exports_every_header_symbol():
 
 def test_host_only_entry_points():
     lib = _abi.load()
-    assert lib.smc_abi_version() == 2
+    assert lib.smc_abi_version() == 3
     assert lib.smc_resample_workspace_bytes(1 << 20) > (1 << 20) * 20
     assert lib.smc_weights_workspace_bytes(1000) > 0
     assert lib.smc_pf_workspace_bytes(1000) > 0
@@ -55,7 +55,7 @@ def test_argument_validation_without_gpu():
 
 
 def test_wstate_layout_matches_header():
-    assert _abi.WSTATE_BYTES == 80
+    assert _abi.WSTATE_BYTES == 88
     assert _abi.WSTATE_OFF["status"] == 68 and _abi.WSTATE_OFF["resample"] == 72
     # the smc_status convention: the first failing index sits 8 bytes after the status word
     assert _abi.WSTATE_OFF["err_index"] == _abi.WSTATE_OFF["status"] + 8

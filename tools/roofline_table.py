@@ -18,8 +18,7 @@ ALG = {
     "k_rs_assign": N * (4 + 4),
     "k_rs_scan": 8192 * 16 * 2,
     "k_rs_zsp_scan": 8192 * 8 * 2,
-    "k_lse_level1": (N // 1024) * 24,
-    "k_lse_finalize": 148 * 24,
+    "k_lse_reduce": (N // 1024) * 24 + 148 * 24,
 }
 
 
