@@ -268,6 +268,33 @@ SMC_HD double exp(double x, const ExpEntry *tab)
     return x < -746.0 ? 0.0 : (x > XMAX ? INFINITY : res);  // exp(-746) rounds to +0
 }
 
+// The GMM likelihood's exp: a 256-entry table (2^(j/256), tools/gen_logtab.py) halves the
+// reduced argument, |r| <= ln2/512, so a degree-4 polynomial suffices (<= 0.6 ulp,
+// tests/test_fastmath.py): one fp64 FMA per call fewer than exp_nonpos (the likelihood's hot loop is fp64-issue
+// bound).  Same contract as exp_nonpos (x <= 0, below 2^-1022 flushed to +0); table layout
+// (stride, off) as there.
+SMC_TABLE ExpEntry kExpTab256[256] = {
+#include "smc_exptab256.inc"
+};
+SMC_HD double exp_nonpos256(double x, const ExpEntry *tab, int stride = 1, int off = 0)
+{
+    const double SH = 0x1.8p52;
+    double kd = fma_(x, 0x1.71547652b82fep+8, SH);  // round(x 256/ln2) in the low word
+    const int64_t k = (int32_t)(uint32_t)bits(kd);
+    kd -= SH;
+    double r = fma_(-kd, 0x1.62e42fefc0000p-9, x);  // ln2/256 hi (35 bits: kd hi exact)
+    r = fma_(-kd, -0x1.c610ca86c3899p-45, r);
+    // 1/6 + (5/4) h^2 / 120 (h = ln2/512): the r^5/120 term economized into r^3 (max truncation
+    // 1.2e-17 instead of 3.8e-17)
+    double p = fma_(r, 1.0 / 24, 0x1.555557e54fd54p-3);
+    p = fma_(r, p, 0.5);
+    p = fma_(r * r, p, r);
+    const ExpEntry t = tab[(k & 255) * stride + off];
+    const double m = fma_(t.hi, p, t.lo) + t.hi;
+    const double res = from_bits(bits(m) + ((uint64_t)(k >> 8) << 52));
+    return x < -708.0 ? 0.0 : res;  // -inf included
+}
+
 // exp(x) for x <= 0 with the table: no overflow side and no subnormal results
 // (below 2^-1022 it flushes to +0) -- for sums whose largest term is exp(0) = 1,
 // where anything that small is far below their rounding (the GMM likelihood).

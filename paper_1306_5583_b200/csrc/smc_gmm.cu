@@ -73,7 +73,8 @@ SMC_DEV double log_likelihood_direct(const Param<R> &p, const double *__restrict
 // groups -- the random exp indices no longer conflict (the single table measured 764 M of
 // 1322 M shared wavefronts as conflicts, profiles/r1_ncu_gmm_mh.txt).
 constexpr int TAB_COPIES = 8;
-constexpr size_t TAB_BYTES = 128 * TAB_COPIES * sizeof(smc_fm::ExpEntry);
+constexpr int TAB_N = 256;  // exp_nonpos256's table
+constexpr size_t TAB_BYTES = TAB_N * TAB_COPIES * sizeof(smc_fm::ExpEntry);
 
 template <int R>
 SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, int nd,
@@ -113,7 +114,7 @@ SMC_DEV double log_likelihood(const Param<R> &p, const double *__restrict__ y, i
             double S = 1.0;
 #pragma unroll
             for (int j = 0; j + 1 < R; ++j)
-                S += smc_fm::exp_nonpos((j < im ? x[j] : x[j + 1]) - m, tab, TAB_COPIES, (int)(threadIdx.x % TAB_COPIES));
+                S += smc_fm::exp_nonpos256((j < im ? x[j] : x[j + 1]) - m, tab, TAB_COPIES, (int)(threadIdx.x % TAB_COPIES));
             msum += m;
             prod *= S;  // prod in [1, 2) times S in [1, R]: normal; peel the exponent off
             const uint64_t pb = smc_fm::bits(prod);
@@ -154,7 +155,7 @@ SMC_DEV double log_prior(const Param<R> &p, const Hyper &h)
 
 SMC_DEV void stage_data(const double *__restrict__ data, int nd, smc_fm::ExpEntry *s_tab, double *s_y)
 {
-    for (int k = threadIdx.x; k < 128 * TAB_COPIES; k += blockDim.x) s_tab[k] = smc_fm::kExpTab[k / TAB_COPIES];
+    for (int k = threadIdx.x; k < TAB_N * TAB_COPIES; k += blockDim.x) s_tab[k] = smc_fm::kExpTab256[k / TAB_COPIES];
     for (int k = threadIdx.x; k < nd; k += blockDim.x) s_y[k] = data[k];
     __syncthreads();
 }

@@ -13,4 +13,5 @@ extern "C" double fm_logprod(const double *x, long n)
 extern "C" void fm_exp_weight(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp_weight(x[i]); }
 extern "C" void fm_exp_nonpos(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp_nonpos(x[i], smc_fm::kExpTab); }
 extern "C" void fm_div10(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::div10(x[i]); }
+extern "C" void fm_exp_nonpos256(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp_nonpos256(x[i], smc_fm::kExpTab256); }
 extern "C" void fm_exp_nonpos_cb(const double *x, double *y, long n) { for (long i = 0; i < n; ++i) y[i] = smc_fm::exp_nonpos_cb(x[i], smc_fm::kExpTab); }

@@ -23,7 +23,7 @@ def fm():
                     os.path.join(HERE, "fastmath_host.cpp")], check=True)
     lib = ctypes.CDLL(so)
     P = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
-    for f in (lib.fm_log, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_exp_nonpos_cb, lib.fm_cos_bm, lib.fm_sqrt_bm, lib.fm_div10):
+    for f in (lib.fm_log, lib.fm_exp, lib.fm_exp_weight, lib.fm_exp_nonpos, lib.fm_exp_nonpos256, lib.fm_exp_nonpos_cb, lib.fm_cos_bm, lib.fm_sqrt_bm, lib.fm_div10):
         f.argtypes = [P, P, ctypes.c_long]
     lib.fm_logprod.argtypes = [P, ctypes.c_long]
     lib.fm_logprod.restype = ctypes.c_double
@@ -136,6 +136,19 @@ def test_exp_nonpos(fm):
     got = fm("fm_exp_nonpos", xs)
     assert ulp_err(got, [decimal.Decimal(float(x)).exp() for x in xs]) <= 0.52
     edge = fm("fm_exp_nonpos", np.array([-708.5, -745.0, -1e6, -np.inf]))
+    assert np.all(edge == 0.0)
+
+
+def test_exp_nonpos256(fm):
+    """smc_fm::exp_nonpos256 (the GMM likelihood's exp: 2^(j/256) table, degree-4 polynomial):
+    <= 0.6 ulp on [-708, 0] (0.52 for the degree-5 exp_nonpos; the terms it feeds are summed
+    into S >= 1), +0 below."""
+    decimal.getcontext().prec = 60
+    rng = np.random.default_rng(9)
+    xs = np.concatenate([rng.uniform(-707.9, 0, 3000), rng.uniform(-2, 0, 3000), [0.0, -0.0, -1e-300, -707.9]])
+    got = fm("fm_exp_nonpos256", xs)
+    assert ulp_err(got, [decimal.Decimal(float(x)).exp() for x in xs]) <= 0.6
+    edge = fm("fm_exp_nonpos256", np.array([-708.5, -745.0, -1e6, -np.inf]))
     assert np.all(edge == 0.0)
 
 
