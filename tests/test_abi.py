@@ -39,6 +39,8 @@ def test_host_only_entry_points():
     assert lib.smc_weights_workspace_bytes(1000) > 0
     assert lib.smc_pf_workspace_bytes(1000) > 0
     assert lib.smc_weighted_reduce_workspace_bytes(1000, 2) > 0
+    # a production build: no index guards compiled in, nothing to report (no CUDA call made)
+    assert _abi.check_failures() == (False, 0, "")
 
 
 def test_argument_validation_without_gpu():
