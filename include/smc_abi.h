@@ -54,6 +54,12 @@ int smc_last_error(char *buf, size_t len);
  * NVRTC user kernels included).  No reference counterpart: instrumentation for the bench's
  * `gpu_launches` (how many of the library's kernels ran in a timed region). */
 int smc_launch_count(uint64_t *out);
+/* Host-orchestration helper of a CUDA-graph-captured sampler loop (no reference counterpart:
+ * the reference has no device history): hist[(*t - 1) * ncols + c] = row_prev[c], then
+ * *t += 1, then obs_out[0..1] = obs[2 * *t .. +1] while *t < nobs -- the per-step history /
+ * cursor / observation bookkeeping as ONE launch (t, obs_out, hist: device). */
+int smc_graph_advance(const double *obs, int64_t nobs, double *obs_out, const double *row_prev, double *hist,
+                      int64_t ncols, int64_t *t, void *stream);
 /* Checked builds (-DSMC_CHECKED=1) count violated index guards in the kernels instead of
  * trapping; this returns their number and the first failing source line (1 = a checked
  * build, 0 = a production build, whose count is always 0).  Test infrastructure. */

@@ -70,6 +70,7 @@ _SIGS = {
     "smc_last_error": ([C.c_char_p, _sz], C.c_int),
     "smc_launch_count": ([_vp], C.c_int),
     "smc_check_failures": ([_vp, _vp, C.c_char_p, _sz], C.c_int),
+    "smc_graph_advance": ([_vp, _i64, _vp, _vp, _vp, _i64, _vp, _vp], C.c_int),
     "smc_philox_blocks": ([_vp, _i64, _u64, _vp, _vp], C.c_int),
     "smc_rng_fill": ([_i32, _u64, _u64, _vp, _f64, _f64, _f64, _vp, _i64, _vp], C.c_int),
     "smc_rng_draw_streams": ([_i32, _u64, _u64, _i64, _vp, _f64, _f64, _f64, _vp, _vp], C.c_int),

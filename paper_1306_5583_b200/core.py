@@ -472,20 +472,25 @@ class Sampler:
         stage, tdev = gb["stage"], gb["t"]
         mon = {name: self._col[f"{name}.0"] for name in self.monitors}
 
+        nobs_dev = v.obs.shape[0]
+
         def step(slot):
             prev = 1 - slot
-            gb["obs"].copy_(v.obs.index_select(0, tdev))  # this step's observation, by device t
-            v.graph_obs = gb["obs"]
+            v.graph_obs = gb["obs"]  # this step's observation (gathered by the previous advance)
             accs = [apply_move(op, sysm, self.iteration + 1) for op in self.move_queue]
-            self._hist.index_copy_(0, tdev - 1, stage[prev:prev + 1])  # previous row, monitor now fused in
+            # one launch: previous row (its monitor now fused in) -> history[t - 1], t += 1, the
+            # next step's observation -> gb["obs"]
+            _abi.call("smc_graph_advance", _abi.ptr(v.obs), nobs_dev, _abi.ptr(gb["obs"]),
+                      ctypes.c_void_p(stage[prev].data_ptr()), _abi.ptr(self._hist), ncols, _abi.ptr(tdev),
+                      _abi.stream())
             self._after_moves(self.iteration + 1, stage[slot], accs)
-            tdev.add_(1)
 
         # entry: the last eager row continues as the "previous" staging row
         stage[1].copy_(self._hist[t0])
         for name, col in mon.items():
             sysm.pending_monitors[name] = (stage[1].data_ptr() + 8 * col, t0)
         tdev.fill_(t0 + 1)
+        gb["obs"].copy_(v.obs[t0 + 1:t0 + 2])  # the first replayed step's observation
         # everything the capture bakes in as a launch argument: buffers, and the sampler's public
         # knobs (threshold, scheme, RNG seed) -- a changed knob must not replay the old value
         key = (v._cur, v.pending is not None, self._hist.data_ptr(), v.obs.data_ptr(),

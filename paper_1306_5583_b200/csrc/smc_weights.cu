@@ -313,6 +313,32 @@ void smc_launch_lse_finalize(const LsePartial *parts, int nparts, smc_wstate *st
                partial_out);
 }
 
+// One step of a captured sampler loop's bookkeeping (core.Sampler._iterate_graph), one launch
+// instead of four framework kernels per step: the previous step's history row (its fused
+// monitor now complete) into the history at the device cursor t - 1, the cursor advanced, and
+// the next step's observation gathered into the fixed buffer the captured move reads.
+__global__ void k_graph_advance(const double *__restrict__ obs, int64_t nobs, double *__restrict__ obs_out,
+                                const double *__restrict__ row_prev, double *__restrict__ hist, int64_t ncols,
+                                int64_t *t)
+{
+    SMC_PDL_WAIT();
+    const int64_t tc = *t;
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < ncols; c += blockDim.x) hist[(tc - 1) * ncols + c] = row_prev[c];
+    if (threadIdx.x < 2 && tc + 1 < nobs) obs_out[threadIdx.x] = obs[2 * (tc + 1) + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) *t = tc + 1;
+}
+
+extern "C" int smc_graph_advance(const double *obs, int64_t nobs, double *obs_out, const double *row_prev,
+                                 double *hist, int64_t ncols, int64_t *t, void *stream)
+{
+    if (!obs || nobs < 1 || !obs_out || !row_prev || !hist || ncols < 1 || ncols > 1024 || !t)
+        return smc_set_error(SMC_EINVAL, "smc_graph_advance: bad args");
+    smc_launch(k_graph_advance, 1, 64, 0, (cudaStream_t)stream, obs, nobs, obs_out, row_prev, hist, ncols, t);
+    return smc_check_launch("smc_graph_advance");
+}
+
 extern "C" int smc_weights_combine(const double *partials, int G, smc_wstate *st, int64_t n_total, int mode,
                                    int accumulate_nc, double *monitor_out, void *stream)
 {
