@@ -246,6 +246,12 @@ def run_reference(args):
     n = particles_per_gpu(args, world)
     n_work = n * world
     ns = n_work if n_work <= N_DEFAULT else N_DEFAULT
+    # the whole run stays within a few minutes: at ~1.5 s per 2^24 step on 16 host threads, a long
+    # --steps (the default 600) takes bounded samples -- the largest power-of-two N whose
+    # warmup + steps fit ~150 s (a per-particle-step rate; `same_config` then says false)
+    per_ps = 9e-8 * 16 / max(cores, 1)  # host seconds per particle-step (measured: 1.47 s / 2^24 at 16)
+    while ns > (1 << 16) and (args.warmup + args.steps) * ns * per_ps > 150.0:
+        ns //= 2
     obs = bench_obs(args.steps + args.warmup + 2)
     times = cpu_baseline_pf(ns, args.warmup + args.steps, args.scheme, obs, cores)
     t = sum(times[args.warmup:])
