@@ -218,6 +218,26 @@ def test_gmm_config3_first_iterations_match_oracle():
 N_MN1 = 3 << 25  # past the shared-memory bin geometry (mn2_fits): the global-bucket multinomial path
 
 
+@pytest.mark.parametrize("n", [1 << 26])
+def test_multinomial_wide_bins_bit_exact(n):
+    """2^26: the shared-memory bins at their widest (one 1024-thread count block per SM, 12 draws
+    per scatter thread) -- counts bit-exact vs the oracle on skewed weights."""
+    from paper_1306_5583_b200 import resample
+    g = torch.Generator("cuda").manual_seed(12)
+    lw = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    w = torch.exp(lw - lw.max())
+    w = (w / w.sum()).contiguous()
+    del lw
+    u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    counts = resample("multinomial", w, u=u).cpu().numpy()
+    ref, _ = O.resample_counts("multinomial", w.cpu().numpy(), u=u.cpu().numpy())
+    del w, u
+    torch.cuda.empty_cache()
+    assert counts.sum() == n
+    bad = np.nonzero(counts != ref)[0]
+    assert bad.size == 0, f"{bad.size} counts differ, first at {bad[:5]}"
+
+
 @pytest.mark.parametrize("scheme,draws", [("multinomial", "explicit"), ("residual", "explicit"),
                                           ("multinomial", "stream")])
 def test_multinomial_past_shared_memory_bins_bit_exact(scheme, draws):
