@@ -27,6 +27,13 @@ constexpr int PB = PF_PB;
 #define PF_UNROLL 1  // particles of a thread interleaved by the compiler (ILP vs registers)
 #endif
 constexpr int kPfUnroll = PF_UNROLL;
+#ifndef PF_SWP
+#define PF_SWP 0  // software-pipelined move body (next particle's draws beside this one's Box-Muller)
+#endif
+template <bool B>
+struct BoolTag {
+    static constexpr bool value = B;
+};
 constexpr int MB = PB * PF_PPT;  // particles per move block
 #ifndef SMC_MOVE_WS_DEFAULT
 #define SMC_MOVE_WS_DEFAULT 0  // the single-role move; the warp-specialized k_pf_move_ws measured slower (profiles/r2_move_ws_ab.txt)
@@ -183,6 +190,67 @@ __global__ void __launch_bounds__(PB, PF_MIN_BLOCKS) k_pf_move(const double *x_i
         if (nl.needs_raw()) lw_nx = lw_raw[base];
     }
     tab_store(tabs, tr);
+#if PF_SWP
+    // Software-pipelined body (uniform counts, every particle of the thread in range): the
+    // Philox draws of particle q + 1 are computed in the same basic block as particle q's
+    // Box-Muller transforms, so each warp's instruction stream mixes IMAD.WIDE / LOP3 (FMA and
+    // ALU pipes) with the fp64 work instead of alternating a Philox phase and an fp64 phase.
+    // Same arithmetic per particle: bit-identical to the loop below.
+    if (UC && PPT > 1 && base + (int64_t)(PPT - 1) * PB < n) {
+        double2 a[4];
+        {
+            uint64_t m[8];
+            draws_uniform<8>(ctr_u, sbase + (uint64_t)base, key, m);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[j] = box_muller_args(m[2 * j], m[2 * j + 1]);
+        }
+        auto body = [&](int q, auto next) {
+            constexpr bool NEXT = decltype(next)::value;
+            const int64_t i = base + (int64_t)q * PB;
+            const int64_t src = s_src[q][threadIdx.x];
+            const double lw_prev = lw_nx;
+            if (NEXT && nl.needs_raw()) lw_nx = lw_raw[i + PB];
+            const double prev = nl(lw_prev);
+            double x0, x1, x2, x3;
+            SMC_CHECK(src >= 0 && src < n);
+            ld_row(x_in + 4 * src, x0, x1, x2, x3);
+            const uint64_t si = sbase + (uint64_t)i;
+            double2 an[4];
+            if constexpr (NEXT) {
+                uint64_t m[8];
+                draws_uniform<8>(ctr_u, si + PB, key, m);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) an[j] = box_muller_args(m[2 * j], m[2 * j + 1]);
+            }
+            double z[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) z[j] = box_muller_from(a[j], FmTabs{tabs.log, tabs.cos});
+            if constexpr (NEXT) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a[j] = an[j];
+            }
+            if (MON) {
+                const double w = nl.eq ? w_equal : smc_fm::exp(prev, tabs.exp);
+                h0 += w * x0;
+                h1 += w * x1;
+            }
+            x0 = x0 + ((0.0 + k.sd_pos * z[0]) + k.delta * x2);
+            x1 = x1 + ((0.0 + k.sd_pos * z[1]) + k.delta * x3);
+            x2 = x2 + (0.0 + k.sd_vel * z[2]);
+            x3 = x3 + (0.0 + k.sd_vel * z[3]);
+            st_row(x_out + 4 * i, x0, x1, x2, x3);
+            const double incw = cv_llh(x0, x1, xo, yo, tabs.log);
+            if (incw_out) incw_out[i] = incw;
+            double v = prev + incw;
+            if (isnan(v) || v == INFINITY) { raise_status_at(&st->status, SMC_ENORMALIZE, (int64_t)si); v = -INFINITY; }
+            lw_raw[i] = v;
+            s_v[q][threadIdx.x] = v;
+        };
+#pragma unroll 1
+        for (int q = 0; q < PPT - 1; ++q) body(q, BoolTag<true>{});
+        body(PPT - 1, BoolTag<false>{});
+    } else
+#endif
 #pragma unroll kPfUnroll
     for (int q = 0; q < PPT; ++q) {
         const int64_t i = base + (int64_t)q * PB;
