@@ -120,20 +120,26 @@ __host__ __device__ inline MnGeom mn_geom(int64_t n)
     return g;
 }
 
-// The binned kernels' shared memory (k_mn2_scatter: a block's 12288 draws + 3 words per bin;
+// The binned kernels' shared memory (k_mn2_scatter: a block's 12288 draws (10 B each) + 3 words per bin;
 // k_mn2_count: a bin's `cap` positions + 2 x 8193 sub-bucket words).  Past N ~ 2^26 a bin no
 // longer fits one block's shared memory: those N take the global-memory bucket path (MN1).
 constexpr int MT = 1024;          // threads of the multinomial kernels
-// draws per thread in k_mn2_scatter: 6 while the block's shared memory (12 B per draw + 12 B per
+// draws per thread in k_mn2_scatter: 6 while the block's shared memory (10 B per draw + 12 B per
 // bin) lets two blocks share an SM (<= 2048 bins, N <= 2^24), else 12 (same-box A/B,
 // profiles/r2_resample_ab.txt)
 __host__ __device__ inline int mn_dpt(int64_t nb) { return nb <= 2048 ? 6 : 12; }
 constexpr int NSB = 4096;         // most sub-buckets of a bin in k_mn2_count (~2 positions each)
+#ifndef MN_SCATTER_MINB
+#define MN_SCATTER_MINB 2  // k_mn2_scatter<6> blocks per SM (2: 32 registers, the draws' positions partly spilled)
+#endif
+#ifndef MN_FU
+#define MN_FU 4  // positions of a sub-bucket k_mn2_count's F(X) checks predicated before its remainder loop
+#endif
 constexpr size_t MN_SMEM_MAX = 232448;  // 227 KB: the sm_100 per-block opt-in maximum
 __host__ __device__ inline size_t mn2_scatter_smem(int64_t n)
 {
     const MnGeom g = mn_geom(n);
-    return (size_t)MT * mn_dpt(g.nb) * (8 + 2 + 2) + (size_t)g.nb * 12 + 64;
+    return (size_t)MT * mn_dpt(g.nb) * (8 + 2) + (size_t)g.nb * 12 + 64;
 }
 __host__ __device__ inline size_t mn2_count_smem(int64_t n)
 {
@@ -776,7 +782,12 @@ SMC_DEV uint64_t mn_m(uint64_t k, uint64_t c0, const Key &key, uint64_t stream, 
     return u ? (uint64_t)(u[k] * TWO53) : draw53(c0 + k, stream, key);
 }
 
-__global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u,
+// DPT draws per thread (mn_dpt): each draw's position and (bin, rank-in-block) stay in
+// registers from the drawing pass, the rank being the return of the shared counting atomic, so
+// the sort is one pass of direct stores (no second atomic, no permutation array), and the runs'
+// global atomics are issued before the block scan and consumed after the sort.
+template <int DPT>
+__global__ void __launch_bounds__(MT, DPT == 6 ? MN_SCATTER_MINB : 1) k_mn2_scatter(int64_t n, Key key, uint64_t stream, const double *__restrict__ u,
                                                     Layout L)
 {
     SMC_PDL_WAIT();
@@ -785,81 +796,90 @@ __global__ void __launch_bounds__(MT) k_mn2_scatter(int64_t n, Key key, uint64_t
     const uint64_t M = h->M, Tm = h->Tm, c0 = h->c0, lo = h->qoff;
     const uint64_t hi = __ldg(&L.qfull[n - 1]);  // inclusive Q (k_rs_prefix): this shard's end
     const MnGeom g = L.mg;  // host-computed (Layout)
-    const int dpt = mn_dpt(g.nb), mch = MT * dpt;
+    constexpr int mch = MT * DPT;
     const uint64_t k0 = (uint64_t)blockIdx.x * mch;
     if (k0 >= M) return;
     extern __shared__ __align__(16) unsigned char mn_sm[];
-    uint64_t *P_s = reinterpret_cast<uint64_t *>(mn_sm);
-    uint16_t *bin_s = reinterpret_cast<uint16_t *>(P_s + mch);
-    uint16_t *perm_s = bin_s + mch;
-    uint32_t *hist = reinterpret_cast<uint32_t *>(perm_s + mch);  // counts, then the sorting cursors
-    uint32_t *base = hist + g.nb;                                  // reserved run start per bin
-    uint32_t *lofs = base + g.nb;                                  // bin's offset in the block's sorted order
+    uint64_t *Ps = reinterpret_cast<uint64_t *>(mn_sm);       // the block's positions, sorted by bin
+    uint16_t *bs = reinterpret_cast<uint16_t *>(Ps + mch);    // their bins
+    uint32_t *hist = reinterpret_cast<uint32_t *>(bs + mch);  // per-bin draw counts of the block
+    uint32_t *lofs = hist + g.nb;                             // bin's offset in the block's sorted order
+    uint32_t *boff = lofs + g.nb;                             // run start in the bin's region - lofs (mod 2^32)
     __shared__ uint32_t s_w[MT / 32 + 1];
     __shared__ int s_over;
     for (int64_t b = threadIdx.x; b < g.nb; b += MT) hist[b] = 0;
     if (threadIdx.x == 0) s_over = 0;
     __syncthreads();
     const int sh = 53 - g.kb;
-#pragma unroll 4
-    for (int d = 0; d < dpt; ++d) {
-        const int idx = d * MT + threadIdx.x;
-        const uint64_t k = k0 + idx;
-        uint16_t bb = 0xFFFF;  // not in this shard's slice / past the last draw
-        uint64_t P = 0;
+    uint64_t P[DPT];
+    uint32_t br[DPT];  // (bin << 16) | rank among the block's draws of that bin; ~0 = none
+#pragma unroll
+    for (int d = 0; d < DPT; ++d) {
+        const uint64_t k = k0 + (uint64_t)(d * MT + threadIdx.x);
+        br[d] = 0xFFFFFFFFu;
+        P[d] = 0;
         if (k < M) {
             const uint64_t m = mn_m(k, c0, key, stream, u);
-            P = (uint64_t)(((u128)m * Tm) >> 53);
-            if (P >= lo && P < hi) {
-                bb = (uint16_t)(m >> sh);
+            const uint64_t p = (uint64_t)(((u128)m * Tm) >> 53);
+            if (p >= lo && p < hi) {  // in this shard's slice
+                const uint32_t bb = (uint32_t)(m >> sh);
                 SMC_CHECK(bb < g.nb);
-                atomicAdd(&hist[bb], 1u);
+                P[d] = p;
+                br[d] = (bb << 16) | atomicAdd(&hist[bb], 1u);  // rank < mch <= 2^16
             }
         }
-        P_s[idx] = P;
-        bin_s[idx] = bb;
     }
     __syncthreads();
-    // per bin: the block's run in the bin's region (one global atomic), and the bins' offsets in
-    // the block's sorted order (exclusive scan over the nb <= 4096 bins, 4 per thread)
+    // per bin: the block's run in the bin's region (one global atomic, its result consumed only
+    // after the sort), and the bins' offsets in the block's sorted order (exclusive scan over the
+    // nb <= 4096 bins, 4 per thread)
     constexpr int BPT = 4;
-    uint32_t loc[BPT], sum = 0;
+    uint32_t loc[BPT], rg[BPT], lq[BPT], sum = 0;
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
         const int64_t b = (int64_t)threadIdx.x * BPT + q;
         loc[q] = b < g.nb ? hist[b] : 0;
         sum += loc[q];
-        if (b < g.nb && loc[q]) {
-            const uint32_t r = atomicAdd(&L.mn_fill[b], loc[q]);
-            base[b] = r;
-            if (r + loc[q] > (uint64_t)g.cap) s_over = 1;
-        }
+        rg[q] = (b < g.nb && loc[q]) ? atomicAdd(&L.mn_fill[b], loc[q]) : 0u;
     }
     uint32_t tot;
     uint32_t ex = block_exclusive_sum<MT, uint32_t>(sum, s_w, &tot);
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
         const int64_t b = (int64_t)threadIdx.x * BPT + q;
-        if (b < g.nb) { lofs[b] = ex; hist[b] = 0; }
+        lq[q] = ex;
+        if (b < g.nb) lofs[b] = ex;
         ex += loc[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int d = 0; d < DPT; ++d) {  // the sort: every draw straight to its slot
+        if (br[d] != 0xFFFFFFFFu) {
+            const uint32_t bb = br[d] >> 16;
+            const uint32_t j = lofs[bb] + (br[d] & 0xFFFFu);
+            SMC_CHECK(j < (uint32_t)mch);
+            Ps[j] = P[d];
+            bs[j] = (uint16_t)bb;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int64_t b = (int64_t)threadIdx.x * BPT + q;
+        if (b < g.nb && loc[q]) {
+            boff[b] = rg[q] - lq[q];
+            if ((uint64_t)rg[q] + loc[q] > (uint64_t)g.cap) s_over = 1;
+        }
     }
     __syncthreads();
     if (s_over) {  // a bin overflowed (adversarial uniforms): the direct search handles the call
         if (threadIdx.x == 0) L.hdr_w()->mn_direct = 1;
         return;
     }
-    for (int d = 0; d < dpt; ++d) {  // counting sort in shared memory: the block's draws by bin
-        const int idx = d * MT + threadIdx.x;
-        const uint16_t bb = bin_s[idx];
-        SMC_CHECK(bb == 0xFFFF || (bb < g.nb && lofs[bb] + hist[bb] < (uint32_t)mch));
-        if (bb != 0xFFFF) perm_s[lofs[bb] + atomicAdd(&hist[bb], 1u)] = (uint16_t)idx;
-    }
-    __syncthreads();
     for (uint32_t j = threadIdx.x; j < tot; j += MT) {  // consecutive j: consecutive slots of a bin's run
-        const int idx = perm_s[j];
-        const uint32_t bb = bin_s[idx];
-        SMC_CHECK(bb < g.nb && base[bb] + (j - lofs[bb]) < (uint64_t)g.cap);
-        L.mn_pos[(int64_t)bb * g.cap + base[bb] + (j - lofs[bb])] = P_s[idx];
+        const uint32_t bb = bs[j];
+        const uint32_t slot = boff[bb] + j;
+        SMC_CHECK(bb < g.nb && slot < (uint64_t)g.cap);
+        L.mn_pos[(int64_t)bb * g.cap + slot] = Ps[j];
     }
 }
 
@@ -1014,8 +1034,14 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
         if (X <= lo_b) return 0;
         if (X > hi_b) return offs[nsb];
         const int sb = (int)((X - lo_b) >> sh2);
-        uint32_t c = offs[sb];
-        for (uint32_t k = offs[sb]; k < offs[sb + 1]; ++k) c += (Ps[k] < X);
+        const uint32_t a = offs[sb], z = offs[sb + 1];
+        uint32_t c = a;
+        // the sub-bucket's first MN_FU positions predicated, not looped: a warp no longer runs
+        // its lanes' longest scan (~6 for ~2 positions per sub-bucket) iteration by iteration;
+        // the rare remainder loops
+#pragma unroll
+        for (int t = 0; t < MN_FU; ++t) c += (a + t < z && Ps[a + t] < X) ? 1u : 0u;
+        for (uint32_t k = a + MN_FU; k < z; ++k) c += (Ps[k] < X);
         return c;
     };
     if (e != e0) {  // the sentinel search moved the end: re-chunk (the last bin only)
@@ -2069,11 +2095,16 @@ inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t s
     const size_t sm = mn2_scatter_smem(n);
     static size_t s_set = 0;  // opt in to > 48 KB of dynamic shared memory once (per size)
     if (sm > s_set) {
-        cudaFuncSetAttribute(k_mn2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_mn2_scatter<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaFuncSetAttribute(k_mn2_scatter<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         s_set = sm;
     }
-    const int64_t mch = (int64_t)MT * mn_dpt(mn_geom(n).nb);
-    smc_launch(k_mn2_scatter, (unsigned)((m + mch - 1) / mch), MT, sm, s, n, key, stream, u, L);
+    const int dpt = mn_dpt(mn_geom(n).nb);
+    const int64_t mch = (int64_t)MT * dpt;
+    if (dpt == 6)
+        smc_launch(k_mn2_scatter<6>, (unsigned)((m + mch - 1) / mch), MT, sm, s, n, key, stream, u, L);
+    else
+        smc_launch(k_mn2_scatter<12>, (unsigned)((m + mch - 1) / mch), MT, sm, s, n, key, stream, u, L);
     const size_t sc = mn2_count_smem(n);
     static size_t c_set = 0;
     if (sc > c_set) {
