@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(RT, LW || RES ? RS_TILES_MINB : RS_TILES_MINB_
         anybad |= wb > 0x3FF0000000000000ull && wb != 0x8000000000000000ull;
         const uint64_t q = (uint64_t)(W * 9223372036854775808.0);  // floor(W 2^63), A.1
         uint64_t qr = 0;
+        int32_t fi = 0;
         sq += q;
         if (RES) {
             const double x = m_out * W;  // fl(M W_i), exactly rounded (no FMA: --fmad=false)
@@ -312,10 +313,13 @@ __global__ void __launch_bounds__(RT, LW || RES ? RS_TILES_MINB : RS_TILES_MINB_
             qr = (uint64_t)((x - f) * rscale);
             sqr += qr;
             sf += (int64_t)f;
+            fi = (int32_t)f;
         }
         if (in) {
             qb[li] = RES ? qr : q;  // the searched quantity, for passes M and B1
-            if (MULTI) L.cnt[base + li] = 0;
+            // the draws' histogram starts from the residual floors f_i (0 for multinomial): the
+            // draw kernels add onto it, and pass B1 reads the finished counts without re-deriving f
+            if (MULTI) L.cnt[base + li] = fi;
         }
     }
     if (__any_sync(0xffffffffu, anybad)) {  // rare: name the first bad weight
@@ -892,7 +896,7 @@ __global__ void __launch_bounds__(MT, DPT == 6 ? MN_SCATTER_MINB : 1) k_mn2_scat
 
 // MTC threads: 512 (two blocks per SM) while a bin's shared memory allows it (N <= 2^25), else
 // 1024 (same-box A/B, profiles/r2_resample_ab.txt)
-template <int MTC>
+template <int MTC, bool ADD>  // ADD: residual -- the counts add onto the floors f_i pass A left in the buffer
 __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout L)
 {
     SMC_PDL_WAIT();
@@ -919,11 +923,13 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
         c1 = min(c0 + C, last + 1);
     };
     uint64_t q[PU], qfirst = 0;
+    int32_t fl[PU];  // residual: the floors f_i already in the histogram buffer, loaded with Q
     auto load_q = [&](int64_t i00) {
 #pragma unroll
         for (int k = 0; k < PU; ++k) {
             const int64_t i = i00 + 32 * k + lane;
             q[k] = i < c1 ? __ldg(&Q[i]) : 0;
+            fl[k] = ADD && i < c1 ? L.cnt[i] : 0;
         }
     };
     chunk(e);
@@ -1065,7 +1071,7 @@ __global__ void __launch_bounds__(MTC, 1024 / MTC) k_mn2_count(int64_t n, Layout
             if (i == s || i == e) {  // a neighbouring bin may reach it too
                 if (c) atomicAdd(&L.cnt[i], (int)c);
             } else {
-                L.cnt[i] = (int32_t)c;  // only this bin reaches it
+                L.cnt[i] = fl[k] + (int32_t)c;  // only this bin reaches it (+ f_i: residual)
             }
         }
     }
@@ -1602,8 +1608,9 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
         uint64_t q[RI];
         int32_t f[RI];
         uint64_t loc = 0;
-        if (!RES) {
+        if (!RES || MULTI) {
             // q_i was materialized by pass A: no exp / quantization here, 64 contiguous bytes per thread
+            // (residual-multinomial: the floors f_i are already in the draws' histogram, pass A)
             if (!MULTI) {
                 load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, q, s_q, 0ull);  // coalesced
             } else {
@@ -1641,8 +1648,7 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
         }
         if (MULTI) {
             int32_t h4[RI];
-            if (RES) __syncthreads();  // the staging above may still be reading s_fb
-            load_blocked<RT, RI, int32_t>(L.cnt, tbase, n, h4, s_fb, 0);  // the draws' histogram
+            load_blocked<RT, RI, int32_t>(L.cnt, tbase, n, h4, s_fb, 0);  // the draws' histogram (+ f_i)
 #pragma unroll
             for (int j = 0; j < RI; ++j) c[j] = (full || base + j < n) ? f[j] + h4[j] : 1;
         } else {
@@ -2090,7 +2096,9 @@ __global__ void __launch_bounds__(RT) k_gather(char *__restrict__ dst, const cha
 
 // The multinomial draws' two kernels (m: the largest draw count; blocks past the call's
 // own count exit at once).
-inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L)
+// add: residual -- the histogram buffer holds the floors f_i (pass A), the counts add onto them
+inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L,
+                       int add)
 {
     const size_t sm = mn2_scatter_smem(n);
     static size_t s_set = 0;  // opt in to > 48 KB of dynamic shared memory once (per size)
@@ -2108,26 +2116,31 @@ inline void launch_mn2(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t s
     const size_t sc = mn2_count_smem(n);
     static size_t c_set = 0;
     if (sc > c_set) {
-        cudaFuncSetAttribute(k_mn2_count<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+        cudaFuncSetAttribute(k_mn2_count<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+        cudaFuncSetAttribute(k_mn2_count<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
         c_set = sc;
     }
     if (2 * (sc + 1024) <= 233472) {  // two blocks per SM (228 KB, 1 KB reserved per block)
         static size_t c2_set = 0;
         if (sc > c2_set) {
-            cudaFuncSetAttribute(k_mn2_count<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+            cudaFuncSetAttribute(k_mn2_count<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
+            cudaFuncSetAttribute(k_mn2_count<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sc);
             c2_set = sc;
         }
-        smc_launch(k_mn2_count<512>, (unsigned)mn_geom(n).nb, 512, sc, s, n, L);
+        if (add) smc_launch(k_mn2_count<512, true>, (unsigned)mn_geom(n).nb, 512, sc, s, n, L);
+        else smc_launch(k_mn2_count<512, false>, (unsigned)mn_geom(n).nb, 512, sc, s, n, L);
     } else {
-        smc_launch(k_mn2_count<1024>, (unsigned)mn_geom(n).nb, 1024, sc, s, n, L);
+        if (add) smc_launch(k_mn2_count<1024, true>, (unsigned)mn_geom(n).nb, 1024, sc, s, n, L);
+        else smc_launch(k_mn2_count<1024, false>, (unsigned)mn_geom(n).nb, 1024, sc, s, n, L);
     }
 }
 
 inline int grid_cap(int64_t blocks);
-inline void launch_mn(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L)
+inline void launch_mn(cudaStream_t s, int64_t n, int64_t m, Key key, uint64_t stream, const double *u, Layout L,
+                      int add)
 {
     if (mn2_fits(n)) {
-        launch_mn2(s, n, m, key, stream, u, L);
+        launch_mn2(s, n, m, key, stream, u, L, add);
         return;
     }
     const unsigned gm = grid_cap((m + RT - 1) / RT);
@@ -2199,7 +2212,7 @@ extern "C" int smc_resample(int scheme, const double *w, const double *lw_raw, c
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_out + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        launch_mn(s, n, m_out, key, stream_index, u, L);
+        launch_mn(s, n, m_out, key, stream_index, u, L, scheme == SMC_RESIDUAL);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
@@ -2332,7 +2345,7 @@ extern "C" int smc_resample_shard_counts(int scheme, const double *w, const doub
     if (scheme == SMC_MULTINOMIAL || scheme == SMC_RESIDUAL) {
         const unsigned gm = grid_cap((m_total + RT - 1) / RT);
         smc_launch(k_rs_prefix, (unsigned)nt, RT, 0, s, scheme, src, n, mo, rscale, L);
-        launch_mn(s, n, m_total, key, stream_index, u, L);
+        launch_mn(s, n, m_total, key, stream_index, u, L, scheme == SMC_RESIDUAL);
         smc_launch(k_rs_multinomial, gm, RT, 0, s, n, key, stream_index, u, L);  // exits unless mn_direct
     }
     int32_t *cout = counts ? counts : L.cnt;
