@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(RT, LW || RES ? RS_TILES_MINB : RS_TILES_MINB_
             qb[li] = RES ? qr : q;  // the searched quantity, for passes M and B1
             // the draws' histogram starts from the residual floors f_i (0 for multinomial): the
             // draw kernels add onto it, and pass B1 reads the finished counts without re-deriving f
-            if (MULTI) L.cnt[base + li] = fi;
+            if (MULTI || RES) L.cnt[base + li] = fi;  // residual-stratified / -systematic: B1 reads f_i here
         }
     }
     if (__any_sync(0xffffffffu, anybad)) {  // rare: name the first bad weight
@@ -1608,44 +1608,23 @@ __global__ void __launch_bounds__(RT, RS_COUNTS_MINB) k_rs_counts(int scheme, WS
         uint64_t q[RI];
         int32_t f[RI];
         uint64_t loc = 0;
-        if (!RES || MULTI) {
-            // q_i was materialized by pass A: no exp / quantization here, 64 contiguous bytes per thread
-            // (residual-multinomial: the floors f_i are already in the draws' histogram, pass A)
-            if (!MULTI) {
-                load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, q, s_q, 0ull);  // coalesced
-            } else {
-#pragma unroll
-                for (int j = 0; j < RI; ++j) q[j] = 0;  // multinomial: counts come from the histogram
-            }
-#pragma unroll
-            for (int j = 0; j < RI; ++j) { f[j] = 0; loc += q[j]; }
+        // q_i (q'_i for the residual schemes) was materialized by pass A, and the residual floors
+        // f_i too (in the histogram buffer): no exp / quantization here, 64 + 32 contiguous bytes
+        // per thread (residual-multinomial: the floors are already in the draws' histogram)
+        if (!MULTI) {
+            load_blocked<RT, RI, uint64_t>(L.qfull, tbase, n, q, s_q, 0ull);  // coalesced
         } else {
-            const NormLw nl = src.norm();
-            // stage: coalesced striped loads -> q' and f -> shared memory -> blocked per thread
-            double r[RI];
 #pragma unroll
-            for (int j = 0; j < RI; ++j) {
-                const int64_t i = tbase + j * RT + threadIdx.x;
-                r[j] = (full || i < n) ? src.raw(i, nl) : 0.0;
-            }
-            bool bad = false;
-#pragma unroll
-            for (int j = 0; j < RI; ++j) {
-                const int li = j * RT + threadIdx.x;
-                const int64_t i = tbase + li;
-                Quant qq{0, 0, 0};
-                if (full || i < n) qq = quantize(src.weight(r[j], nl), true, m_out, rscale, bad);
-                s_q[pad16(li)] = qq.qr;
-                s_fb[pad16(li)] = (int32_t)qq.f;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < RI; ++j) {
-                q[j] = s_q[pad16(threadIdx.x * RI + j)];
-                f[j] = s_fb[pad16(threadIdx.x * RI + j)];
-                loc += q[j];
-            }
+            for (int j = 0; j < RI; ++j) q[j] = 0;  // multinomial: counts come from the histogram
         }
+        if (RES && !MULTI) {
+            load_blocked<RT, RI, int32_t>(L.cnt, tbase, n, f, s_fb, 0);
+        } else {
+#pragma unroll
+            for (int j = 0; j < RI; ++j) f[j] = 0;
+        }
+#pragma unroll
+        for (int j = 0; j < RI; ++j) loc += q[j];
         if (MULTI) {
             int32_t h4[RI];
             load_blocked<RT, RI, int32_t>(L.cnt, tbase, n, h4, s_fb, 0);  // the draws' histogram (+ f_i)
