@@ -108,8 +108,14 @@ def test_spec_examples_on_device():
         assert list(c) == [3, 0, 0] and list(p) == [0, 0, 0]
     c, p = gpu_resample("systematic", [0.5, 0.5], u=[0.3])
     assert list(c) == [1, 1]
-    c, _ = gpu_resample("residual", [0.5, 0.3, 0.2], u=[0.0], m_out=10)
-    assert list(c) == [5, 3, 2]
+    for s in ("residual", "residual_stratified", "residual_systematic"):  # floors only (no leftovers)
+        c, p = gpu_resample(s, [0.5, 0.3, 0.2], u=[0.0], m_out=10)
+        assert list(c) == [5, 3, 2], s
+    for s in ("residual", "residual_stratified", "residual_systematic"):  # floors + leftovers, M != N
+        w = [0.55, 0.25, 0.2]
+        c, _ = gpu_resample(s, w, u=[0.3, 0.7, 0.9], m_out=7)
+        ref, _ = O.resample_counts(s, np.array(w), u=np.array([0.3, 0.7, 0.9]), m_out=7)
+        assert list(c) == list(ref) and sum(c) == 7, (s, list(c), list(ref))
     from paper_1306_5583_b200 import replication_to_parents
     assert replication_to_parents([2, 0, 1]).tolist() == [0, 0, 2]
     assert replication_to_parents([0, 3, 0]).tolist() == [1, 1, 1]
