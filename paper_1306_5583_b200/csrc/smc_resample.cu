@@ -1794,8 +1794,18 @@ SMC_DEV int64_t surplus_owner(const int32_t *anchor, const int32_t *sp_start, in
 // slot's row is overwritten by its parent's as soon as the parent is known (sources have
 // count >= 2, destinations count 0: disjoint), saving the separate copy pass and
 // its re-read of the parent vector.
+// Pass C (the index-only variant) at 8 blocks per SM: 32 registers, and the partial-tile store
+// staging aliased onto the parent staging (25.9 KB of shared memory instead of 35.4) -- a
+// latency-bound pass, so the extra resident warps pay: the PF resample phase at 2^24 0.2025 -> 0.1956 ms
+// (same-box A/B, profiles/r2_assign_occupancy_ab.txt)
+#ifndef RS_ASSIGN_ALIAS
+#define RS_ASSIGN_ALIAS 1
+#endif
+#ifndef RS_ASSIGN_MINB
+#define RS_ASSIGN_MINB 8
+#endif
 template <bool SHARD, bool COPY32 = false>
-__global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
+__global__ void __launch_bounds__(RT, (!SHARD && !COPY32) ? RS_ASSIGN_MINB : 1) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
                                                   int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
     SMC_PDL_WAIT();
@@ -1814,7 +1824,13 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
         return;
     }
     __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
+#if RS_ASSIGN_ALIAS
+    // the partial-tile store staging reuses the parent staging (dead by then: barrier below)
+    static_assert(tile_smem_elems<int32_t, RT, RI>() <= CSTAGE, "s_io fits in s_start");
+    int32_t *const s_io = s_start;
+#else
     __shared__ int32_t s_io[tile_smem_elems<int32_t, RT, RI>()];
+#endif
     __shared__ uint32_t sm32[RT / 32 + 1];
     __shared__ int64_t s_soffs[SMC_MAX_SHARDS + 1], s_zs[3];
     const int64_t tbase = t * TILE;
@@ -1975,6 +1991,9 @@ __global__ void __launch_bounds__(RT) k_rs_assign(const int32_t *__restrict__ ci
             }
         }
     }
+#if RS_ASSIGN_ALIAS
+    __syncthreads();  // every thread is done with s_start before the staging reuses it
+#endif
     store_blocked<RT, RI, int32_t>(parents, tbase, n, par, s_io);  // coalesced
 }
 
