@@ -1805,7 +1805,7 @@ SMC_DEV int64_t surplus_owner(const int32_t *anchor, const int32_t *sp_start, in
 #define RS_ASSIGN_MINB 8
 #endif
 template <bool SHARD, bool COPY32 = false>
-__global__ void __launch_bounds__(RT, (!SHARD && !COPY32) ? RS_ASSIGN_MINB : 1) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
+__global__ void __launch_bounds__(RT, (!SHARD && !COPY32) ? RS_ASSIGN_MINB : 0) k_rs_assign(const int32_t *__restrict__ cin, int64_t n,
                                                   int32_t *__restrict__ parents, ShardC sc, Layout L)
 {
     SMC_PDL_WAIT();
@@ -1824,13 +1824,12 @@ __global__ void __launch_bounds__(RT, (!SHARD && !COPY32) ? RS_ASSIGN_MINB : 1) 
         return;
     }
     __shared__ int32_t s_start[CSTAGE], s_idx[CSTAGE];
-#if RS_ASSIGN_ALIAS
-    // the partial-tile store staging reuses the parent staging (dead by then: barrier below)
+    // index-only variant: the partial-tile store staging reuses the parent staging (dead by then:
+    // barrier below).  Not with the fused row copy, whose stores would wait on that barrier.
+    constexpr bool kAlias = RS_ASSIGN_ALIAS && !SHARD && !COPY32;
     static_assert(tile_smem_elems<int32_t, RT, RI>() <= CSTAGE, "s_io fits in s_start");
-    int32_t *const s_io = s_start;
-#else
-    __shared__ int32_t s_io[tile_smem_elems<int32_t, RT, RI>()];
-#endif
+    __shared__ int32_t s_io_own[kAlias ? 1 : tile_smem_elems<int32_t, RT, RI>()];
+    int32_t *const s_io = kAlias ? s_start : s_io_own;
     __shared__ uint32_t sm32[RT / 32 + 1];
     __shared__ int64_t s_soffs[SMC_MAX_SHARDS + 1], s_zs[3];
     const int64_t tbase = t * TILE;
@@ -1991,9 +1990,7 @@ __global__ void __launch_bounds__(RT, (!SHARD && !COPY32) ? RS_ASSIGN_MINB : 1) 
             }
         }
     }
-#if RS_ASSIGN_ALIAS
-    __syncthreads();  // every thread is done with s_start before the staging reuses it
-#endif
+    if (kAlias) __syncthreads();  // every thread is done with s_start before the staging reuses it
     store_blocked<RT, RI, int32_t>(parents, tbase, n, par, s_io);  // coalesced
 }
 
